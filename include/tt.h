@@ -1,0 +1,214 @@
+/* =====================================================================================
+ * tt.h — C ABI of libtt.so: the B200 (sm_100a) hot path of Tree Training (arXiv 2511.00413).
+ *
+ * Citations: "P:n" = PAPER.md line n (the paper's LaTeX source), "S:n" = SPEC.md line n,
+ * "R<k>" = reading k in DESIGN.md §3 (where the paper is silent or ambiguous).
+ *
+ * The library implements the data-parallel hot path named by BASELINE.json:north_star:
+ *   tt_pack          Tree Packing of ONE tree/forest into a DFS-serialised token sequence plus the
+ *                    three per-token artifacts of Fig. 6impl: restored position ids
+ *                    (P:536-539), gradient-scale ("tree-scale") and the shared-prefix
+ *                    mask, the latter as one subtree-end E_j per key (j <= i < E_j)
+ *                    plus 128x128 tile metadata (empty / partial / full classes).
+ *   tt_attn_fwd      shared-prefix-masked attention forward (Eq. 1), O and LSE.
+ *   tt_attn_bwd      its backward with Gradient Restoration: the upstream gradient of every row i
+ *                    is scaled by the tree-scale w_i (Fig. 4gradient; Eqs. 20-21
+ *                    P:483-497), giving dQ/dK/dV equal to the sum over per-branch gradients
+ *                    (Eqs. 14-16).
+ *   tt_restore_loss  next-token cross entropy with the tree-scale folded into every prediction
+ *                    (the "gradient scaling step before the backward propagation"; R6-R8),
+ *                    its gradient w.r.t. the logits, and deterministic fp64 sums.
+ *   tt_grad_sqnorm   deterministic fp64 sum of squares (per-tree gradient-norm scalars).
+ *
+ * Conventions (all entry points):
+ *   - Status: every call returns tt_status; TT_OK == 0.  On error nothing is launched and a
+ *     thread-local message is available from tt_last_error().
+ *   - Memory: the CALLER owns every buffer.  The library never allocates device memory, never
+ *     frees, never synchronises a stream, and keeps no global state except the thread-local
+ *     error string and a cached per-device attribute query.
+ *   - Host vs device: pointers documented as HOST are read synchronously during the call;
+ *     all others are DEVICE pointers and are accessed asynchronously on `stream`.
+ *   - Layout "thd": Q/O/dO/dQ are [N, Hq, d], K/V/dK/dV are [N, Hkv, d], contiguous, row major,
+ *     16-byte aligned.  LSE and D are [Hq, N] fp32.  GQA: the kv head of q head h is h / (Hq/Hkv)
+ *     (R10).
+ *   - Supported (d, dtype): (128, TT_BF16) on the tcgen05/TMEM/TMA kernels; (64, TT_BF16),
+ *     (64, TT_FP32) and (128, TT_FP32) on the SIMT "test mode" kernels (R13).  Anything else
+ *     returns TT_ERR_UNSUPPORTED.  There is no CPU fallback.
+ * ===================================================================================== */
+#ifndef TT_H_
+#define TT_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* tt_stream_t; /* == cudaStream_t */
+
+typedef enum {
+  TT_OK = 0,
+  TT_ERR_INVALID_ARGUMENT = 1, /* null pointer, negative size, bad enum value              */
+  TT_ERR_NOT_A_FOREST = 2,     /* parent out of range, self-parent, cycle                   */
+  TT_ERR_EMPTY = 3,            /* the forest holds zero tokens                       */
+  TT_ERR_TOO_LARGE = 4,        /* N, counts or pair totals overflow their types             */
+  TT_ERR_UNSUPPORTED = 5,      /* head_dim / dtype / Hq % Hkv not supported                 */
+  TT_ERR_ALIGNMENT = 6,        /* tensor not 16-byte aligned                                */
+  TT_ERR_WORKSPACE = 7,        /* workspace too small                                       */
+  TT_ERR_CUDA = 8              /* a CUDA runtime / driver call failed                       */
+} tt_status;
+
+typedef enum { TT_BF16 = 0, TT_FP32 = 1 } tt_dtype;
+
+/* Tile edge used by all tile metadata and by the tensor-core kernels. */
+#define TT_BLOCK 128
+
+const char* tt_status_string(tt_status s);
+/* Thread-local detail of the last error raised on this thread ("" if none). */
+const char* tt_last_error(void);
+/* ABI version (major * 100 + minor). */
+int32_t tt_version(void);
+
+/* --------------------------------------------------------------------------------------
+ * Tree Packing ("merge trajectories into a tree"; Eq. 13 P:395-400 "X_ours =
+ * pack_ours[P;S_1;...;S_n]"; Fig. 6impl).
+ *
+ * Input (HOST, read during the call):
+ *   parent[n]  int32, -1 for a root, else the parent node id (0 <= parent < n).
+ *   len[n]     int32 >= 0, the node's segment token count l(y). Zero is allowed.
+ *   term[n]    int32 >= 0 or NULL: trajectories that END at the node (duplicates and
+ *              trajectories ending at an internal node).  NULL means 1 on childless
+ *              nodes and 0 elsewhere.
+ * Serialisation (R3): DFS pre-order, roots by ascending id, children by ascending id.
+ * Per packed token i (node u = node(i)):
+ *   pos[i]  = tokens on u's root path strictly before i (restored position id, R4)
+ *   w[i]    = sum of term over subtree(u) = trajectories through i (tree-scale, R5)
+ *   E[i]    = packed end (exclusive) of subtree(u); token i may attend j iff j <= i < E_j (R2)
+ *   node[i] = u
+ * Per 128-token block kb: kblk_minE / kblk_maxE = min / max of E over its keys.
+ * Forward tile lists: for q-block qb, the k-blocks kb <= qb with a non-empty tile, ascending,
+ *   at fwd_list[qb*(qb+1)/2 + t], t < fwd_cnt[qb]; each entry is kb | (cls << 28) with
+ *   cls 1 = partial (mask needed), 2 = full (every pair allowed).  Tile classes are exact:
+ *   for kb < qb, empty iff maxE_kb <= 128*qb, full iff minE_kb >= min(N, 128*qb+128);
+ *   the diagonal tile is partial unless it holds a single token.
+ * Backward: the q-blocks that see k-block kb are exactly [kb, ceil(kblk_maxE[kb] / 128)).
+ * Loss targets (App. D of SURVEY, R7): for the LAST token of every node u, the packed indices
+ *   of the first token of every continuation (children of u in order; a zero-length child
+ *   contributes its own continuations recursively) at succ_tok[succ_ptr[u] .. succ_ptr[u+1]).
+ * -------------------------------------------------------------------------------------- */
+typedef struct {
+  int32_t n_nodes;
+  int32_t n_roots;
+  int32_t n_traj;          /* trajectories = sum of term                                  */
+  int32_t n_blk;           /* ceil(N / 128)                                               */
+  int32_t n_succ;          /* entries of succ_tok                                         */
+  int32_t reserved;
+  int64_t n_tokens;        /* N = sum of len                                              */
+  int64_t n_linear_tokens; /* sum_l L_l = sum_i w_i  (per-branch linear token count)      */
+  int64_t n_pairs;         /* A     = sum_i (pos_i + 1)   (allowed (i, j) pairs)          */
+  int64_t n_linear_pairs;  /* A_lin = sum_i w_i (pos_i + 1) = sum_l L_l (L_l + 1) / 2     */
+  size_t ws_bytes;         /* device workspace tt_pack needs                              */
+} tt_pack_info;
+
+typedef struct {
+  /* device pointers into the caller's pack workspace (valid while it lives) */
+  const int32_t* pos;          /* [N]      */
+  const int32_t* w;            /* [N]      */
+  const int32_t* E;            /* [N]      */
+  const int32_t* node;         /* [N]      */
+  const int32_t* node_start;   /* [n]      */
+  const int32_t* node_len;     /* [n]      */
+  const int32_t* node_sub_end; /* [n]      */
+  const int32_t* node_depth;   /* [n]      tokens on the root path before the node          */
+  const int32_t* node_leaves;  /* [n]      */
+  const int32_t* succ_ptr;     /* [n + 1]  */
+  const int32_t* succ_tok;     /* [n_succ] */
+  const int32_t* kblk_minE;    /* [n_blk]  */
+  const int32_t* kblk_maxE;    /* [n_blk]  */
+  const int32_t* fwd_cnt;      /* [n_blk]  */
+  const int32_t* fwd_list;     /* [n_blk * (n_blk + 1) / 2] */
+  int64_t n_tokens;
+  int32_t n_nodes;
+  int32_t n_blk;
+  int32_t n_succ;
+  int32_t max_succ;            /* longest continuation list (tt_restore_loss supports <= 1024) */
+} tt_packed;
+
+/* Validate the forest and size the pack (HOST only, synchronous, no CUDA calls). */
+tt_status tt_pack_plan(const int32_t* parent, const int32_t* len, const int32_t* term, int32_t n_nodes,
+                       tt_pack_info* info);
+
+/* Pack: host validation + O(n) node DFS, one async H2D copy of the node tables, then device
+ * kernels that fill the per-token arrays and the tile metadata into d_ws (ws_bytes >=
+ * info.ws_bytes).  `out` receives device pointers into d_ws.  `info` may be NULL. */
+tt_status tt_pack(const int32_t* parent, const int32_t* len, const int32_t* term, int32_t n_nodes,
+                  void* d_ws, size_t ws_bytes, tt_packed* out, tt_pack_info* info, tt_stream_t stream);
+
+/* --------------------------------------------------------------------------------------
+ * Tree-masked attention forward (Eq. 1 P:119-126 with softmax scale, R1; mask R2):
+ *   O_i   = sum_{j : j <= i < E_j} softmax_j(scale * q_i . k_j) v_j
+ *   LSE_i = ln sum_{j : j <= i < E_j} exp(scale * q_i . k_j)      (natural log, R9)
+ * q [N,hq,d], k/v [N,hkv,d] (dtype dt), o [N,hq,d] (dtype dt), lse [hq,N] fp32.
+ * Empty tiles are skipped, full tiles run unmasked, partial tiles are masked in registers.
+ * -------------------------------------------------------------------------------------- */
+tt_status tt_attn_fwd(const tt_packed* pk, const void* q, const void* k, const void* v, tt_dtype dt,
+                      int32_t hq, int32_t hkv, int32_t d, float softmax_scale, void* o, float* lse,
+                      tt_stream_t stream);
+
+/* Bytes of device workspace tt_attn_bwd needs (fp32 dQ accumulator + D). */
+tt_status tt_attn_bwd_workspace(const tt_packed* pk, int32_t hq, int32_t hkv, int32_t d, tt_dtype dt,
+                                size_t* bytes);
+
+/* --------------------------------------------------------------------------------------
+ * Tree-masked attention backward with Gradient Restoration (Eqs. 2, 14-16, 20-21; R6):
+ *   omega_i = w_i if restore else 1;  P_ij = exp(scale q_i.k_j - LSE_i);  D_i = dO_i . O_i
+ *   dV_j = sum_i omega_i P_ij dO_i
+ *   dS_ij = omega_i P_ij (dO_i . v_j - D_i)
+ *   dQ_i = scale sum_j dS_ij k_j,   dK_j = scale sum_i dS_ij q_i     (sums over j <= i < E_j)
+ *   GQA: dK/dV of a kv head sum over its q heads.
+ * With restore = 1, `dout` is the per-token upstream gradient G of ONE branch (identical for
+ * every branch through the token) and the outputs equal the sum over branches of ordinary
+ * causal-attention gradients.  With restore = 0, `dout` must already be restored (w (.) G).
+ * o / lse are the outputs of tt_attn_fwd.  dq [N,hq,d], dk/dv [N,hkv,d] in dtype dt.
+ * -------------------------------------------------------------------------------------- */
+tt_status tt_attn_bwd(const tt_packed* pk, const void* q, const void* k, const void* v, const void* o,
+                      const float* lse, const void* dout, int32_t restore, tt_dtype dt, int32_t hq,
+                      int32_t hkv, int32_t d, float softmax_scale, void* dq, void* dk, void* dv, void* d_ws,
+                      size_t ws_bytes, tt_stream_t stream);
+
+/* --------------------------------------------------------------------------------------
+ * Gradient-Restoration loss (R6, R7, R8, R17).  For every packed row t
+ * with targets T(t) (next token inside the node, else the continuation list succ_tok; a target
+ * counts iff node_loss_mask[node(target)] != 0 when the mask is given, and — boundary_mode 1 —
+ * only when t has exactly one continuation), each target k with weight omega_k = w[k]:
+ *   loss_t   = sum_k omega_k (lse(x_t) - x_t[tok[k]])
+ *   dlogits_t = grad_scale * (Omega_t softmax(x_t) - sum_k omega_k e_{tok[k]}),  Omega_t = sum omega_k
+ * logits [N, ld] bf16 (row stride ld >= vocab elements, 16-byte aligned rows); dlogits has the
+ * same layout and MAY ALIAS logits (each row is read before it is written).  tok [N] int32.
+ * tok_loss [N] fp32 (nullable) receives loss_t.  sums [2] fp64 (device) receives
+ * (sum_t loss_t, sum_t Omega_t), reduced in a fixed order (bitwise reproducible).
+ * d_err (device int32, nullable) is set to 1 if a target token id is outside [0, vocab); that
+ * row's loss is NaN.  ws: >= tt_restore_loss_workspace() bytes.
+ * -------------------------------------------------------------------------------------- */
+size_t tt_restore_loss_workspace(const tt_packed* pk);
+tt_status tt_restore_loss(const tt_packed* pk, const void* logits, int64_t ld, int32_t vocab, const int32_t* tok,
+                          const uint8_t* node_loss_mask, int32_t boundary_mode, float grad_scale, void* dlogits,
+                          float* tok_loss, double* sums, int32_t* d_err, void* d_ws, size_t ws_bytes,
+                          tt_stream_t stream);
+
+/* Deterministic fp64 sum of squares of n elements of x (dtype dt) into *out (device).
+ * ws >= tt_grad_sqnorm_workspace(n) bytes. */
+size_t tt_grad_sqnorm_workspace(int64_t n);
+tt_status tt_grad_sqnorm(const void* x, int64_t n, tt_dtype dt, double* out, void* d_ws, size_t ws_bytes,
+                         tt_stream_t stream);
+
+/* Kernel-level launch counters (for bench.py's gpu_launches claim): number of kernels this
+ * thread has launched through the library since the last reset. */
+int64_t tt_launch_count(void);
+void tt_launch_count_reset(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TT_H_ */

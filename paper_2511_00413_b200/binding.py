@@ -1,0 +1,290 @@
+"""ctypes binding of libtt.so — argument marshalling only (every step runs in the CUDA kernels).
+
+Names mirror include/tt.h.  Tensors are torch tensors on the current CUDA device; the current
+torch stream is passed as the tt_stream_t unless `stream` is given.  Workspaces are allocated
+with torch (caching allocator) and owned by the returned Python objects.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import os
+import threading
+from typing import Optional
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(HERE, "libtt.so")
+TT_BLOCK = 128
+TT_BF16, TT_FP32 = 0, 1
+
+STATUS = {0: "ok", 1: "invalid argument", 2: "not a forest", 3: "empty", 4: "too large", 5: "unsupported",
+          6: "alignment", 7: "workspace too small", 8: "cuda error"}
+
+
+class TTError(RuntimeError):
+    def __init__(self, fn, code, detail):
+        super().__init__(f"{fn}: {STATUS.get(code, code)} ({detail})")
+        self.code = code
+        self.fn = fn
+
+
+class TTPackInfo(C.Structure):
+    _fields_ = [("n_nodes", C.c_int32), ("n_roots", C.c_int32), ("n_traj", C.c_int32), ("n_blk", C.c_int32),
+                ("n_succ", C.c_int32), ("reserved", C.c_int32), ("n_tokens", C.c_int64),
+                ("n_linear_tokens", C.c_int64), ("n_pairs", C.c_int64), ("n_linear_pairs", C.c_int64),
+                ("ws_bytes", C.c_size_t)]
+
+
+_PTR_FIELDS = ["pos", "w", "E", "node", "node_start", "node_len", "node_sub_end", "node_depth", "node_leaves",
+               "succ_ptr", "succ_tok", "kblk_minE", "kblk_maxE", "fwd_cnt", "fwd_list"]
+
+
+class TTPacked(C.Structure):
+    _fields_ = [(f, C.c_void_p) for f in _PTR_FIELDS] + [
+        ("n_tokens", C.c_int64), ("n_nodes", C.c_int32), ("n_blk", C.c_int32), ("n_succ", C.c_int32),
+        ("max_succ", C.c_int32)]
+
+
+_lock = threading.Lock()
+_lib = None
+
+
+def lib_path() -> str:
+    return _SO
+
+
+def lib():
+    """Load libtt.so (raises if it is missing: no fallback path exists)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(_SO):
+                raise ImportError(f"libtt.so not built at {_SO}; run `python -m paper_2511_00413_b200.build`")
+            L = C.CDLL(_SO)
+            i32p, vp, sz, st = C.POINTER(C.c_int32), C.c_void_p, C.c_size_t, C.c_void_p
+            L.tt_status_string.restype = C.c_char_p
+            L.tt_status_string.argtypes = [C.c_int]
+            L.tt_last_error.restype = C.c_char_p
+            L.tt_last_error.argtypes = []
+            L.tt_version.restype = C.c_int32
+            L.tt_pack_plan.argtypes = [i32p, i32p, i32p, C.c_int32, C.POINTER(TTPackInfo)]
+            L.tt_pack.argtypes = [i32p, i32p, i32p, C.c_int32, vp, sz, C.POINTER(TTPacked), C.POINTER(TTPackInfo), st]
+            L.tt_attn_fwd.argtypes = [C.POINTER(TTPacked), vp, vp, vp, C.c_int, C.c_int32, C.c_int32, C.c_int32,
+                                      C.c_float, vp, vp, st]
+            L.tt_attn_bwd_workspace.argtypes = [C.POINTER(TTPacked), C.c_int32, C.c_int32, C.c_int32, C.c_int,
+                                                C.POINTER(C.c_size_t)]
+            L.tt_attn_bwd.argtypes = [C.POINTER(TTPacked), vp, vp, vp, vp, vp, vp, C.c_int32, C.c_int, C.c_int32,
+                                      C.c_int32, C.c_int32, C.c_float, vp, vp, vp, vp, sz, st]
+            L.tt_restore_loss_workspace.restype = C.c_size_t
+            L.tt_restore_loss_workspace.argtypes = [C.POINTER(TTPacked)]
+            L.tt_restore_loss.argtypes = [C.POINTER(TTPacked), vp, C.c_int64, C.c_int32, vp, vp, C.c_int32, C.c_float,
+                                          vp, vp, vp, vp, vp, sz, st]
+            L.tt_grad_sqnorm_workspace.restype = C.c_size_t
+            L.tt_grad_sqnorm_workspace.argtypes = [C.c_int64]
+            L.tt_grad_sqnorm.argtypes = [vp, C.c_int64, C.c_int, vp, vp, sz, st]
+            L.tt_launch_count.restype = C.c_int64
+            L.tt_launch_count.argtypes = []
+            L.tt_launch_count_reset.argtypes = []
+            L.tt_launch_count_reset.restype = None
+            for fn in ("tt_pack_plan", "tt_pack", "tt_attn_fwd", "tt_attn_bwd_workspace", "tt_attn_bwd",
+                       "tt_restore_loss", "tt_grad_sqnorm"):
+                getattr(L, fn).restype = C.c_int
+            _lib = L
+    return _lib
+
+
+def _check(fn, rc):
+    if rc != 0:
+        raise TTError(fn, rc, lib().tt_last_error().decode(errors="replace"))
+
+
+def _host_i32(x):
+    if x is None:
+        return None, None
+    try:
+        import torch
+        if isinstance(x, torch.Tensor):
+            x = x.detach().cpu().numpy()
+    except ImportError:  # pragma: no cover
+        pass
+    a = np.ascontiguousarray(np.asarray(x, dtype=np.int32))
+    return a, a.ctypes.data_as(C.POINTER(C.c_int32))
+
+
+def _stream(stream):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return C.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+
+
+def _dt(t):
+    import torch
+    if t.dtype == torch.bfloat16:
+        return TT_BF16
+    if t.dtype == torch.float32:
+        return TT_FP32
+    raise TypeError(f"unsupported dtype {t.dtype}")
+
+
+def _p(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def tt_launch_count() -> int:
+    return int(lib().tt_launch_count())
+
+
+def tt_launch_count_reset() -> None:
+    lib().tt_launch_count_reset()
+
+
+def tt_pack_plan(parent, length, term=None) -> dict:
+    """Host-only validation + sizing (no CUDA calls).  Returns the tt_pack_info fields."""
+    par, pp = _host_i32(parent)
+    ln, lp = _host_i32(length)
+    tm, tp = _host_i32(term)
+    info = TTPackInfo()
+    _check("tt_pack_plan", lib().tt_pack_plan(pp, lp, tp, int(par.shape[0]), C.byref(info)))
+    return {f: getattr(info, f) for f, _ in TTPackInfo._fields_ if f != "reserved"}
+
+
+class PackedTree:
+    """Result of tt_pack: the device workspace and the tt_packed struct pointing into it."""
+
+    def __init__(self, c: TTPacked, info: dict, ws, parent, length, term):
+        self.c = c
+        self.info = info
+        self.ws = ws
+        self.parent, self.length, self.term = parent, length, term
+
+    @property
+    def n_tokens(self) -> int:
+        return int(self.c.n_tokens)
+
+    @property
+    def n_blk(self) -> int:
+        return int(self.c.n_blk)
+
+    def _view(self, field: str, count: int):
+        import torch
+        off = getattr(self.c, field) - self.ws.data_ptr()
+        return self.ws[off:off + 4 * count].view(torch.int32)
+
+    def arrays(self) -> dict:
+        """Device int32 views of every pack output (no copies)."""
+        N, n, nb = self.n_tokens, int(self.c.n_nodes), self.n_blk
+        out = {f: self._view(f, N) for f in ("pos", "w", "E", "node")}
+        out.update({f: self._view(f, n) for f in ("node_start", "node_len", "node_sub_end", "node_depth",
+                                                  "node_leaves")})
+        out["succ_ptr"] = self._view("succ_ptr", n + 1)
+        out["succ_tok"] = self._view("succ_tok", int(self.c.n_succ)) if self.c.n_succ else None
+        out["kblk_minE"] = self._view("kblk_minE", nb)
+        out["kblk_maxE"] = self._view("kblk_maxE", nb)
+        out["fwd_cnt"] = self._view("fwd_cnt", nb)
+        out["fwd_list"] = self._view("fwd_list", nb * (nb + 1) // 2)
+        return out
+
+
+def tt_pack(parent, length, term=None, device=None, stream=None) -> PackedTree:
+    import torch
+    par, pp = _host_i32(parent)
+    ln, lp = _host_i32(length)
+    tm, tp = _host_i32(term)
+    info = TTPackInfo()
+    L = lib()
+    _check("tt_pack_plan", L.tt_pack_plan(pp, lp, tp, int(par.shape[0]), C.byref(info)))
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    ws = torch.empty(int(info.ws_bytes) + 256, dtype=torch.uint8, device=dev)
+    # 256-byte aligned view
+    mis = (-ws.data_ptr()) % 256
+    ws = ws[mis:mis + int(info.ws_bytes)]
+    c = TTPacked()
+    info2 = TTPackInfo()
+    _check("tt_pack", L.tt_pack(pp, lp, tp, int(par.shape[0]), C.c_void_p(ws.data_ptr()), int(info.ws_bytes),
+                                C.byref(c), C.byref(info2), _stream(stream)))
+    d = {f: getattr(info2, f) for f, _ in TTPackInfo._fields_ if f != "reserved"}
+    d["max_succ"] = int(c.max_succ)
+    return PackedTree(c, d, ws, par, ln, tm)
+
+
+def _scale(softmax_scale, d):
+    return float(1.0 / math.sqrt(d)) if softmax_scale is None else float(softmax_scale)
+
+
+def tt_attn_fwd(pk: PackedTree, q, k, v, softmax_scale=None, out=None, lse=None, stream=None):
+    import torch
+    N, hq, d = q.shape
+    hkv = k.shape[1]
+    if out is None:
+        out = torch.empty_like(q)
+    if lse is None:
+        lse = torch.empty(hq, N, dtype=torch.float32, device=q.device)
+    for t in (q, k, v, out, lse):
+        if not t.is_contiguous():
+            raise ValueError("tensors must be contiguous")
+    _check("tt_attn_fwd", lib().tt_attn_fwd(C.byref(pk.c), _p(q), _p(k), _p(v), _dt(q), hq, hkv, d,
+                                            _scale(softmax_scale, d), _p(out), _p(lse), _stream(stream)))
+    return out, lse
+
+
+def tt_attn_bwd_workspace(pk: PackedTree, hq, hkv, d, dtype) -> int:
+    import torch
+    n = C.c_size_t()
+    dt = TT_BF16 if dtype == torch.bfloat16 else TT_FP32
+    _check("tt_attn_bwd_workspace", lib().tt_attn_bwd_workspace(C.byref(pk.c), hq, hkv, d, dt, C.byref(n)))
+    return int(n.value)
+
+
+def tt_attn_bwd(pk: PackedTree, q, k, v, o, lse, dout, restore=True, softmax_scale=None, dq=None, dk=None, dv=None,
+                ws=None, stream=None):
+    import torch
+    N, hq, d = q.shape
+    hkv = k.shape[1]
+    dq = torch.empty_like(q) if dq is None else dq
+    dk = torch.empty_like(k) if dk is None else dk
+    dv = torch.empty_like(v) if dv is None else dv
+    need = tt_attn_bwd_workspace(pk, hq, hkv, d, q.dtype)
+    if ws is None or ws.numel() < need:
+        ws = torch.empty(need, dtype=torch.uint8, device=q.device)
+    _check("tt_attn_bwd", lib().tt_attn_bwd(C.byref(pk.c), _p(q), _p(k), _p(v), _p(o), _p(lse), _p(dout),
+                                            int(bool(restore)), _dt(q), hq, hkv, d, _scale(softmax_scale, d),
+                                            _p(dq), _p(dk), _p(dv), _p(ws), int(ws.numel()), _stream(stream)))
+    return dq, dk, dv
+
+
+def tt_restore_loss(pk: PackedTree, logits, tok, grad_scale=1.0, node_loss_mask=None, boundary_mode=0,
+                    dlogits=None, tok_loss=None, sums=None, d_err=None, ws=None, vocab=None, stream=None):
+    """Returns (sums [2] fp64 device: (sum loss, sum Omega), dlogits, tok_loss, d_err).
+    Pass dlogits=logits for the in-place (aliasing) form."""
+    import torch
+    N, ld = logits.shape
+    vocab = ld if vocab is None else int(vocab)
+    dlogits = torch.empty_like(logits) if dlogits is None else dlogits
+    sums = torch.zeros(2, dtype=torch.float64, device=logits.device) if sums is None else sums
+    d_err = torch.zeros(1, dtype=torch.int32, device=logits.device) if d_err is None else d_err
+    L = lib()
+    need = int(L.tt_restore_loss_workspace(C.byref(pk.c)))
+    if ws is None or ws.numel() < need:
+        ws = torch.empty(need, dtype=torch.uint8, device=logits.device)
+    if node_loss_mask is not None and not isinstance(node_loss_mask, torch.Tensor):
+        node_loss_mask = torch.as_tensor(np.asarray(node_loss_mask, dtype=np.uint8), device=logits.device)
+    _check("tt_restore_loss", L.tt_restore_loss(C.byref(pk.c), _p(logits), int(ld), vocab, _p(tok),
+                                                _p(node_loss_mask), int(boundary_mode), float(grad_scale),
+                                                _p(dlogits), _p(tok_loss), _p(sums), _p(d_err), _p(ws),
+                                                int(ws.numel()), _stream(stream)))
+    return sums, dlogits, tok_loss, d_err
+
+
+def tt_grad_sqnorm(x, out=None, ws=None, stream=None):
+    import torch
+    out = torch.zeros(1, dtype=torch.float64, device=x.device) if out is None else out
+    L = lib()
+    need = int(L.tt_grad_sqnorm_workspace(x.numel()))
+    if ws is None or ws.numel() < need:
+        ws = torch.empty(need, dtype=torch.uint8, device=x.device)
+    _check("tt_grad_sqnorm", L.tt_grad_sqnorm(_p(x), int(x.numel()), _dt(x), _p(out), _p(ws), int(ws.numel()),
+                                              _stream(stream)))
+    return out

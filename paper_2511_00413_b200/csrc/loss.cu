@@ -1,0 +1,282 @@
+// loss.cu — Gradient-Restoration loss: weighted next-token cross entropy
+// and its gradient, HBM-bound, one persistent CTA per row stream.
+//
+// The paper restores gradients by "insert[ing] a gradient scaling step before the backward
+// propagation" that multiplies each node's gradient by its reuse count.  At the
+// loss (R6) this is exactly a per-prediction weight omega_k = w[target]: every one
+// of the w[target] trajectories through the predicting token t continues to that target, so
+//   loss_t    = sum_k omega_k (lse(x_t) - x_t[y_k])
+//   dlogits_t = gamma (Omega_t softmax(x_t) - sum_k omega_k e_{y_k})
+// Targets (R7): t+1 inside a node; at a node's last token every continuation (succ list).
+//
+// Memory plan per row (V = 151,936 bf16 = 297 KB):  pass 1 streams the row from HBM (16-byte
+// vector loads, online max / sum-exp in the log2 domain), pass 2 re-reads it — it is still in
+// the 126 MB L2 because ~600 rows are in flight — and writes dlogits (may alias logits).  HBM
+// traffic is therefore ~4 V bytes / row.  Rows with no target (Omega_t = 0, e.g.
+// the last token of every trajectory) skip both reads and only write zeros.
+#include <algorithm>
+
+#include "tt_internal.cuh"
+
+namespace tt {
+namespace {
+
+constexpr int kLossThreads = 512;
+constexpr int kMaxTargets = 1024;
+
+struct Vec8 { float v[8]; };
+
+__device__ __forceinline__ Vec8 load8(const __nv_bfloat16* p) {
+  uint4 u;
+  asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(u.x), "=r"(u.y), "=r"(u.z), "=r"(u.w) : "l"(p));
+  Vec8 r;
+  const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    float2 f = __bfloat1622float2(b[t]);
+    r.v[2 * t] = f.x;
+    r.v[2 * t + 1] = f.y;
+  }
+  return r;
+}
+
+// plain (coherent) load for pass 2: dlogits may alias logits, so the row must not come from the
+// non-coherent path after another thread of this CTA wrote it (it never does: each thread
+// reads then writes only its own chunks), but keep the coherent path to be safe.
+__device__ __forceinline__ Vec8 load8_coherent(const __nv_bfloat16* p) {
+  uint4 u = *reinterpret_cast<const uint4*>(p);
+  Vec8 r;
+  const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    float2 f = __bfloat1622float2(b[t]);
+    r.v[2 * t] = f.x;
+    r.v[2 * t + 1] = f.y;
+  }
+  return r;
+}
+
+__device__ __forceinline__ void store8(__nv_bfloat16* p, const float* f) {
+  uint4 u;
+  __nv_bfloat162* b = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+  for (int t = 0; t < 4; ++t) b[t] = __floats2bfloat162_rn(f[2 * t], f[2 * t + 1]);
+  *reinterpret_cast<uint4*>(p) = u;
+}
+
+__device__ __forceinline__ void online_add(float& m, float& s, float x2) {
+  // x2 in log2 units
+  if (x2 > m) {
+    s = s * exp2f(m - x2) + 1.f;
+    m = x2;
+  } else {
+    s += exp2f(x2 - m);
+  }
+}
+
+__global__ void __launch_bounds__(kLossThreads) loss_kernel(
+    int64_t N, const __nv_bfloat16* logits, int64_t ld, int V, const int32_t* __restrict__ tok,
+    const uint8_t* __restrict__ node_mask, int boundary_mode, float gamma, const int32_t* __restrict__ w,
+    const int32_t* __restrict__ node, const int32_t* __restrict__ node_start, const int32_t* __restrict__ node_len,
+    const int32_t* __restrict__ succ_ptr, const int32_t* __restrict__ succ_tok, __nv_bfloat16* dlogits,
+    float* __restrict__ tok_loss, float* __restrict__ ws_loss, float* __restrict__ ws_omega, int32_t* d_err) {
+  __shared__ int s_y[kMaxTargets];
+  __shared__ float s_om[kMaxTargets];
+  __shared__ float s_xy[kMaxTargets];
+  __shared__ int s_nt;
+  __shared__ float s_red[2][kLossThreads / 32];
+  __shared__ float s_lse;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int V8 = V & ~7;
+  const float L2E = kLog2e;
+
+  for (int64_t row = blockIdx.x; row < N; row += gridDim.x) {
+    // ---- targets of this row (R7, R17, boundary mode) ----
+    if (tid == 0) {
+      const int32_t u = node[row];
+      const bool last = row == (int64_t)node_start[u] + node_len[u] - 1;
+      int nt = 0;
+      if (!last) {
+        const int64_t tg = row + 1;
+        if (!node_mask || node_mask[node[tg]]) { s_y[0] = (int)tg; nt = 1; }
+      } else {
+        const int b = succ_ptr[u], e = succ_ptr[u + 1];
+        if (!(boundary_mode == 1 && e - b > 1)) {
+          for (int k = b; k < e; ++k) {
+            const int tg = succ_tok[k];
+            if (!node_mask || node_mask[node[tg]]) s_y[nt++] = tg;
+          }
+        }
+      }
+      s_nt = nt;
+    }
+    __syncthreads();
+    const int nt = s_nt;
+    // packed target index -> (token id, weight)
+    float om_part = 0.f;
+    bool bad = false;
+    for (int k = tid; k < nt; k += kLossThreads) {
+      const int tg = s_y[k];
+      const int y = tok[tg];
+      const float om = (float)w[tg];
+      bad |= (y < 0 || y >= V);
+      s_y[k] = y;
+      s_om[k] = om;
+      om_part += om;
+    }
+    const __nv_bfloat16* x = logits + row * ld;
+    __nv_bfloat16* dx = dlogits + row * ld;
+    // block sum of Omega (fixed order)
+    for (int o = 16; o > 0; o >>= 1) om_part += __shfl_xor_sync(0xffffffffu, om_part, o);
+    const int bad_any = __syncthreads_or(bad);
+    if (lane == 0) s_red[0][warp] = om_part;
+    __syncthreads();
+    float Omega = 0.f;
+    for (int k = 0; k < kLossThreads / 32; ++k) Omega += s_red[0][k];
+    __syncthreads();  // s_red is reused below
+    if (Omega == 0.f || bad_any) {
+      // no prediction from this row (or invalid target id): zero gradient
+      const float z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      for (int c = tid * 8; c < V8; c += kLossThreads * 8) store8(dx + c, z);
+      for (int c = V8 + tid; c < V; c += kLossThreads) dx[c] = __float2bfloat16_rn(0.f);
+      if (tid == 0) {
+        const float lv = bad_any ? __int_as_float(0x7fc00000) : 0.f;
+        if (bad_any && d_err) atomicExch(d_err, 1);
+        ws_loss[row] = lv;
+        ws_omega[row] = bad_any ? 0.f : Omega;
+        if (tok_loss) tok_loss[row] = lv;
+      }
+      __syncthreads();
+      continue;
+    }
+    // ---- pass 1: online max / sum-exp (log2 domain), 4 vectors in flight per thread ----
+    float m = -INFINITY, s = 0.f;
+    int c = tid * 8;
+    for (; c + 3 * kLossThreads * 8 < V8; c += 4 * kLossThreads * 8) {
+      Vec8 a = load8(x + c), b = load8(x + c + kLossThreads * 8), d = load8(x + c + 2 * kLossThreads * 8),
+           e = load8(x + c + 3 * kLossThreads * 8);
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        online_add(m, s, a.v[t] * L2E);
+        online_add(m, s, b.v[t] * L2E);
+        online_add(m, s, d.v[t] * L2E);
+        online_add(m, s, e.v[t] * L2E);
+      }
+    }
+    for (; c < V8; c += kLossThreads * 8) {
+      Vec8 a = load8(x + c);
+#pragma unroll
+      for (int t = 0; t < 8; ++t) online_add(m, s, a.v[t] * L2E);
+    }
+    for (int cc = V8 + tid; cc < V; cc += kLossThreads) online_add(m, s, __bfloat162float(x[cc]) * L2E);
+    // warp + block combine of (m, s)
+    for (int o = 16; o > 0; o >>= 1) {
+      const float m2 = __shfl_xor_sync(0xffffffffu, m, o);
+      const float s2 = __shfl_xor_sync(0xffffffffu, s, o);
+      const float mm = fmaxf(m, m2);
+      s = (mm == -INFINITY) ? 0.f : s * exp2f(m - mm) + s2 * exp2f(m2 - mm);
+      m = mm;
+    }
+    if (lane == 0) { s_red[0][warp] = m; s_red[1][warp] = s; }
+    __syncthreads();
+    if (tid == 0) {
+      float M = -INFINITY, S = 0.f;
+      for (int k = 0; k < kLossThreads / 32; ++k) {
+        const float m2 = s_red[0][k], s2 = s_red[1][k];
+        const float mm = fmaxf(M, m2);
+        S = (mm == -INFINITY) ? 0.f : S * exp2f(M - mm) + s2 * exp2f(m2 - mm);
+        M = mm;
+      }
+      s_lse = M + log2f(S);  // log2 units
+    }
+    __syncthreads();
+    const float lse2 = s_lse;
+    // ---- loss: read the target logits before pass 2 may overwrite them (aliasing) ----
+    float lpart = 0.f;
+    for (int k = tid; k < nt; k += kLossThreads) {
+      const float xy = __bfloat162float(x[s_y[k]]);
+      s_xy[k] = xy;
+      lpart += s_om[k] * (lse2 * kLn2 - xy);
+    }
+    for (int o = 16; o > 0; o >>= 1) lpart += __shfl_xor_sync(0xffffffffu, lpart, o);
+    __syncthreads();
+    if (lane == 0) s_red[1][warp] = lpart;
+    __syncthreads();
+    // ---- pass 2: dlogits = gamma * Omega * softmax (target entries fixed up below) ----
+    const float gO = gamma * Omega;
+    for (c = tid * 8; c < V8; c += kLossThreads * 8) {
+      Vec8 a = load8_coherent(x + c);
+      float f[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) f[t] = gO * exp2f(fmaf(a.v[t], L2E, -lse2));
+      store8(dx + c, f);
+    }
+    for (int cc = V8 + tid; cc < V; cc += kLossThreads)
+      dx[cc] = __float2bfloat16_rn(gO * exp2f(fmaf(__bfloat162float(x[cc]), L2E, -lse2)));
+    __syncthreads();
+    // ---- fix-up: dlogits[y] = gamma (Omega p_y - sum_{k: y_k = y} omega_k), once per distinct y ----
+    for (int k = tid; k < nt; k += kLossThreads) {
+      const int y = s_y[k];
+      bool first = true;
+      float om_y = 0.f;
+      for (int k2 = 0; k2 < nt; ++k2) {
+        if (s_y[k2] == y) {
+          if (k2 < k) first = false;
+          om_y += s_om[k2];
+        }
+      }
+      if (first) {
+        const float py = exp2f(fmaf(s_xy[k], L2E, -lse2));
+        dx[y] = __float2bfloat16_rn(gamma * (Omega * py - om_y));
+      }
+    }
+    if (tid == 0) {
+      float L = 0.f;
+      for (int k = 0; k < kLossThreads / 32; ++k) L += s_red[1][k];
+      ws_loss[row] = L;
+      ws_omega[row] = Omega;
+      if (tok_loss) tok_loss[row] = L;
+    }
+    __syncthreads();
+  }
+}
+
+// fixed-order fp64 reduction of the per-row loss / Omega into sums[0..1]
+__global__ void __launch_bounds__(1024) loss_sum_kernel(int64_t N, const float* __restrict__ ws_loss,
+                                                        const float* __restrict__ ws_omega, double* __restrict__ sums) {
+  const int64_t per = (N + blockDim.x - 1) / blockDim.x;
+  const int64_t b0 = threadIdx.x * per, b1 = imin64(N, b0 + per);
+  double a = 0.0, b = 0.0;
+  for (int64_t i = b0; i < b1; ++i) { a += (double)ws_loss[i]; b += (double)ws_omega[i]; }
+  __shared__ double sa[1024], sb[1024];
+  sa[threadIdx.x] = a;
+  sb[threadIdx.x] = b;
+  __syncthreads();
+  for (int w = 512; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) { sa[threadIdx.x] += sa[threadIdx.x + w]; sb[threadIdx.x] += sb[threadIdx.x + w]; }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) { sums[0] = sa[0]; sums[1] = sb[0]; }
+}
+
+}  // namespace
+
+tt_status launch_loss(const tt_packed& pk, const __nv_bfloat16* logits, int64_t ld, int vocab, const int32_t* tok,
+                      const uint8_t* node_mask, int boundary_mode, float gamma, __nv_bfloat16* dlogits, float* tok_loss,
+                      double* sums, int32_t* d_err, float* ws_loss, float* ws_omega, cudaStream_t st) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t grid = imin64(pk.n_tokens, (int64_t)sms * 4);
+  loss_kernel<<<(unsigned)grid, kLossThreads, 0, st>>>(pk.n_tokens, logits, ld, vocab, tok, node_mask, boundary_mode,
+                                                      gamma, pk.w, pk.node, pk.node_start, pk.node_len, pk.succ_ptr,
+                                                      pk.succ_tok, dlogits, tok_loss, ws_loss, ws_omega, d_err);
+  count_launch();
+  tt_status s = check_launch("loss_kernel");
+  if (s) return s;
+  loss_sum_kernel<<<1, 1024, 0, st>>>(pk.n_tokens, ws_loss, ws_omega, sums);
+  count_launch();
+  return check_launch("loss_sum_kernel");
+}
+
+}  // namespace tt

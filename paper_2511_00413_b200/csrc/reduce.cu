@@ -1,0 +1,114 @@
+// reduce.cu — HBM-bound helpers: the backward preprocess and the
+// deterministic fp64 sum of squares used for the per-tree gradient-norm scalars (row a6).
+#include "tt_internal.cuh"
+
+namespace tt {
+namespace {
+
+template <typename T> __device__ __forceinline__ float ld_f(const T* p);
+template <> __device__ __forceinline__ float ld_f<float>(const float* p) { return *p; }
+template <> __device__ __forceinline__ float ld_f<__nv_bfloat16>(const __nv_bfloat16* p) { return __bfloat162float(*p); }
+
+// D_i = dO_i . O_i per (token, head) (unweighted; the tree-scale enters in the main backward).
+// One warp per row; bf16 rows of 128 are read as 8-byte vectors.  Optionally zeroes the fp32
+// dQ accumulator row (the tcgen05 backward accumulates dQ with reductions).
+template <typename T>
+__global__ void __launch_bounds__(256) bwd_pre_kernel(const T* __restrict__ o, const T* __restrict__ dout, int64_t N,
+                                                      int hq, int d, float* __restrict__ Dvec, float* __restrict__ dq_acc) {
+  const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= N * hq) return;
+  const int64_t i = row / hq;
+  const int h = (int)(row % hq);
+  const T* a = o + row * d;
+  const T* b = dout + row * d;
+  float s = 0.f;
+  if constexpr (sizeof(T) == 2) {
+    if (d == 128) {
+      const uint2 va = reinterpret_cast<const uint2*>(a)[lane];
+      const uint2 vb = reinterpret_cast<const uint2*>(b)[lane];
+      const __nv_bfloat162* pa = reinterpret_cast<const __nv_bfloat162*>(&va);
+      const __nv_bfloat162* pb = reinterpret_cast<const __nv_bfloat162*>(&vb);
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        float2 fa = __bfloat1622float2(pa[t]), fb = __bfloat1622float2(pb[t]);
+        s = fmaf(fa.x, fb.x, s);
+        s = fmaf(fa.y, fb.y, s);
+      }
+    } else {
+      for (int c = lane; c < d; c += 32) s = fmaf(ld_f(a + c), ld_f(b + c), s);
+    }
+  } else {
+    for (int c = lane; c < d; c += 32) s = fmaf(ld_f(a + c), ld_f(b + c), s);
+  }
+  for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  if (lane == 0) Dvec[(int64_t)h * N + i] = s;
+  if (dq_acc) {
+    float4* z = reinterpret_cast<float4*>(dq_acc + row * d);
+    for (int c = lane; c < d / 4; c += 32) z[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+}
+
+// fp64 sum of squares: kSqnormBlocks fixed contiguous partitions, fixed-order tree reductions.
+template <typename T>
+__global__ void __launch_bounds__(256) sqnorm_partial_kernel(const T* __restrict__ x, int64_t n, double* __restrict__ part) {
+  const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t b0 = (int64_t)blockIdx.x * per;
+  const int64_t b1 = imin64(n, b0 + per);
+  double s = 0.0;
+  for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
+    const double v = (double)ld_f(x + i);
+    s = fma(v, v, s);
+  }
+  __shared__ double sh[256];
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
+}
+
+__global__ void __launch_bounds__(256) sum_partials_kernel(const double* __restrict__ part, int n, double* __restrict__ out) {
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s += part[i];
+  __shared__ double sh[256];
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = sh[0];
+}
+
+}  // namespace
+
+tt_status launch_bwd_pre(const void* o, const void* dout, tt_dtype dt, int64_t N, int hq, int d, float* Dvec,
+                         float* dq_acc, cudaStream_t st) {
+  const int64_t rows = N * hq;
+  const unsigned blocks = (unsigned)((rows + 7) / 8);
+  if (dt == TT_BF16)
+    bwd_pre_kernel<__nv_bfloat16><<<blocks, 256, 0, st>>>((const __nv_bfloat16*)o, (const __nv_bfloat16*)dout, N, hq, d,
+                                                          Dvec, dq_acc);
+  else
+    bwd_pre_kernel<float><<<blocks, 256, 0, st>>>((const float*)o, (const float*)dout, N, hq, d, Dvec, dq_acc);
+  count_launch();
+  return check_launch("bwd_pre_kernel");
+}
+
+tt_status launch_sqnorm(const void* x, int64_t n, tt_dtype dt, double* out, double* partials, cudaStream_t st) {
+  if (dt == TT_BF16)
+    sqnorm_partial_kernel<__nv_bfloat16><<<kSqnormBlocks, 256, 0, st>>>((const __nv_bfloat16*)x, n, partials);
+  else
+    sqnorm_partial_kernel<float><<<kSqnormBlocks, 256, 0, st>>>((const float*)x, n, partials);
+  count_launch();
+  tt_status s = check_launch("sqnorm_partial_kernel");
+  if (s) return s;
+  sum_partials_kernel<<<1, 256, 0, st>>>(partials, kSqnormBlocks, out);
+  count_launch();
+  return check_launch("sum_partials_kernel");
+}
+
+}  // namespace tt

@@ -1,0 +1,71 @@
+// Internal helpers shared by the libtt.so translation units (never by the oracle).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+
+#include "../../include/tt.h"
+
+namespace tt {
+
+void set_error(const char* fmt, ...);
+void clear_error();
+void count_launch(int n = 1);
+
+// Check the launch that was just issued on this thread's runtime.
+tt_status check_launch(const char* what);
+
+inline cudaStream_t as_cuda(tt_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
+
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+template <typename T>
+__host__ __device__ inline T ceil_div(T a, T b) { return (a + b - 1) / b; }
+
+constexpr int kBlock = TT_BLOCK;           // 128: tile edge of all tile metadata
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
+
+// fwd tile-list entry encoding
+constexpr int kClsShift = 28;
+constexpr int32_t kKbMask = (1 << kClsShift) - 1;
+constexpr int kClsPartial = 1;
+constexpr int kClsFull = 2;
+
+__host__ __device__ inline int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
+__host__ __device__ inline int64_t tri_off(int64_t qb) { return qb * (qb + 1) / 2; }
+
+// ---- kernel launchers implemented in the .cu files ----
+tt_status launch_pack_fill(const tt_packed& pk, const int32_t* order, const int32_t* order_start, int32_t n_order,
+                           int32_t* pos, int32_t* w, int32_t* E, int32_t* node, int32_t* kminE, int32_t* kmaxE,
+                           int32_t* fwd_cnt, int32_t* fwd_list, cudaStream_t st);
+
+tt_status simt_attn_fwd(const tt_packed& pk, const void* q, const void* k, const void* v, tt_dtype dt, int hq,
+                        int hkv, int d, float scale, void* o, float* lse, cudaStream_t st);
+tt_status simt_attn_bwd(const tt_packed& pk, const void* q, const void* k, const void* v, const float* lse,
+                        const float* Dvec, const void* dout, int restore, tt_dtype dt, int hq, int hkv, int d,
+                        float scale, void* dq, void* dk, void* dv, cudaStream_t st);
+tt_status launch_bwd_pre(const void* o, const void* dout, tt_dtype dt, int64_t N, int hq, int d, float* Dvec,
+                         float* dq_acc, cudaStream_t st);
+
+bool sm100_available();
+tt_status sm100_attn_fwd(const tt_packed& pk, const void* q, const void* k, const void* v, int hq, int hkv,
+                         int d, float scale, void* o, float* lse, cudaStream_t st);
+tt_status sm100_attn_bwd(const tt_packed& pk, const void* q, const void* k, const void* v, const float* lse,
+                         const float* Dvec, const void* dout, int restore, int hq, int hkv, int d, float scale,
+                         float* dq_acc, void* dq, void* dk, void* dv, cudaStream_t st);
+
+tt_status launch_loss(const tt_packed& pk, const __nv_bfloat16* logits, int64_t ld, int vocab, const int32_t* tok,
+                      const uint8_t* node_mask, int boundary_mode, float gamma, __nv_bfloat16* dlogits,
+                      float* tok_loss, double* sums, int32_t* d_err, float* ws_loss, float* ws_omega,
+                      cudaStream_t st);
+tt_status launch_sqnorm(const void* x, int64_t n, tt_dtype dt, double* out, double* partials, cudaStream_t st);
+
+constexpr int kSqnormBlocks = 296;
+
+}  // namespace tt

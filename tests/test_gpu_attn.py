@@ -1,0 +1,174 @@
+"""GPU parity for tree-masked attention (tt_attn_fwd / tt_attn_bwd) against the fp64 oracle.
+
+Every comparison consumes the SAME seeded inputs (workloads.tensors) rounded to the run dtype; the
+oracle upcasts them exactly.  Tolerances: tests/_util.py (BASELINE.json north_star)."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from workloads import trees, tensors
+from _util import TOL_G_BF16, TOL_G_FP32, TOL_O_BF16, TOL_O_FP32, max_abs, rel_l2, to64
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def tt():
+    import paper_2511_00413_b200 as P
+    P.lib()
+    return P
+
+
+def _run(tt, t, hq, hkv, d, dtype, seed=0, restore=True):
+    import torch
+    pk = tt.tt_pack(t.parent, t.length, t.term)
+    N = pk.n_tokens
+    q, k, v = tensors.qkv_tensors(N, hq, hkv, d, dtype, seed=seed)
+    G = tensors.grad_tensor(N, hq, d, dtype, seed=seed + 100)
+    qd, kd, vd, Gd = (x.cuda() for x in (q, k, v, G))
+    scale = 1.0 / math.sqrt(d)
+    o, lse = tt.tt_attn_fwd(pk, qd, kd, vd, scale)
+    dq, dk, dv = tt.tt_attn_bwd(pk, qd, kd, vd, o, lse, Gd, restore=restore, softmax_scale=scale)
+    torch.cuda.synchronize()
+    return pk, (q, k, v, G, scale), (o.cpu(), lse.cpu(), dq.cpu(), dk.cpu(), dv.cpu())
+
+
+def _oracle(t, q, k, v, G, scale):
+    opk = oracle.pack(t.parent, t.length, t.term)
+    o, lse = oracle.attn_fwd(opk, q, k, v, scale)
+    dq, dk, dv = oracle.attn_bwd(opk, q, k, v, G, scale)
+    return opk, o, lse, dq, dk, dv
+
+
+def _on_path(opk):
+    c = np.zeros(opk["n_tokens"], np.int64)
+    for idx in oracle.paths(opk):
+        c[idx] += 1
+    return c > 0
+
+
+FP32_CASES = [
+    ("tiny", trees.tiny(), 1, 1, 64),
+    ("spec", trees.spec_example(), 2, 1, 64),
+    ("fig4", trees.fig4_unit(), 2, 2, 128),
+    ("agentic700", trees.gen_agentic(700, root_len=150, seed=3), 4, 2, 64),
+    ("wide_small", trees.gen_wide(prefix=300, n_leaves=6), 2, 1, 128),
+    ("zero_multiroot", trees.Tree([-1, 0, 0, 2, -1, 4, 4], [0, 140, 0, 33, 150, 0, 9]), 2, 2, 64),
+    ("term", trees.Tree([-1, 0, 0], [130, 70, 5], [1, 2, 1]), 2, 1, 64),
+]
+
+
+@pytest.mark.parametrize("name,t,hq,hkv,d", FP32_CASES, ids=[c[0] for c in FP32_CASES])
+def test_fp32_test_mode(tt, name, t, hq, hkv, d):
+    pk, (q, k, v, G, scale), (o, lse, dq, dk, dv) = _run(tt, t, hq, hkv, d, "fp32", seed=7)
+    opk, oo, olse, odq, odk, odv = _oracle(t, q, k, v, G, scale)
+    m = _on_path(opk)
+    assert max_abs(o[m], oo[m]) <= TOL_O_FP32
+    assert max_abs(lse[:, m], olse[:, m]) <= TOL_O_FP32
+    for a, b in ((dq, odq), (dk, odk), (dv, odv)):
+        assert rel_l2(a, b) <= TOL_G_FP32
+
+
+BF16_CASES = [
+    ("agentic1500_mha", trees.gen_agentic(1500, root_len=300, seed=5), 2, 2),
+    ("agentic2000_gqa", trees.gen_agentic(2000, root_len=256, seed=1), 4, 1),
+    ("wide_ragged", trees.gen_wide(prefix=512, n_leaves=7), 4, 2),
+    ("chain_ragged", trees.chain(1, seg=999), 2, 1),
+    ("single_token_nodes", trees.Tree([-1, 0, 0, 1, 1], [129, 1, 1, 130, 1]), 2, 2),
+]
+
+
+@pytest.mark.parametrize("name,t,hq,hkv", BF16_CASES, ids=[c[0] for c in BF16_CASES])
+def test_bf16_tensor_core(tt, name, t, hq, hkv):
+    tt.tt_launch_count_reset()
+    pk, (q, k, v, G, scale), (o, lse, dq, dk, dv) = _run(tt, t, hq, hkv, 128, "bf16", seed=11)
+    assert tt.tt_launch_count() >= 4
+    opk, oo, olse, odq, odk, odv = _oracle(t, q, k, v, G, scale)
+    assert max_abs(o, oo) <= TOL_O_BF16
+    assert max_abs(lse, olse) <= TOL_O_BF16
+    for a, b in ((dq, odq), (dk, odk), (dv, odv)):
+        assert rel_l2(a, b) <= TOL_G_BF16
+    # per-head relative errors too
+    for h in range(hq):
+        assert rel_l2(dq[:, h], odq[:, h]) <= TOL_G_BF16
+
+
+def test_restore_off_negative_control(tt):
+    """restore=0 with dO = G (no tree-scale) must miss the branch-sum gradient; restore=0
+    with dO = w * G (already restored) must match it (R6)."""
+    import torch
+    t = trees.gen_agentic(900, root_len=200, seed=2)
+    pk, (q, k, v, G, scale), (o, lse, dq0, dk0, dv0) = _run(tt, t, 2, 1, 128, "bf16", seed=3, restore=False)
+    opk, oo, olse, odq, odk, odv = _oracle(t, q, k, v, G, scale)
+    assert rel_l2(dv0, odv) > 0.1
+    w = torch.tensor(opk["w"], dtype=torch.float32)
+    Gw = (G.float() * w[:, None, None]).to(torch.bfloat16)
+    qd, kd, vd = q.cuda(), k.cuda(), v.cuda()
+    od, lsed = tt.tt_attn_fwd(pk, qd, kd, vd, scale)
+    dq, dk, dv = tt.tt_attn_bwd(pk, qd, kd, vd, od, lsed, Gw.cuda(), restore=False, softmax_scale=scale)
+    torch.cuda.synchronize()
+    # Gw is rounded to bf16 after scaling, so compare against the oracle at the bf16 tolerance
+    for a, b in ((dq, odq), (dk, odk), (dv, odv)):
+        assert rel_l2(a.cpu(), b) <= TOL_G_BF16
+
+
+def test_branch_invariance_on_gpu(tt):
+    """The tree output at a shared-prefix token equals the output of the same kernels run on a
+    linearised single branch, within bf16 tolerance."""
+    import torch
+    t = trees.gen_agentic(1200, root_len=400, seed=4)
+    pk, (q, k, v, G, scale), (o, lse, *_ ) = _run(tt, t, 2, 2, 128, "bf16", seed=5)
+    opk = oracle.pack(t.parent, t.length)
+    idx = oracle.paths(opk)[-1]
+    lin = tt.tt_pack([-1], [len(idx)])
+    ii = torch.as_tensor(idx.astype(np.int64))
+    ol, lsel = tt.tt_attn_fwd(lin, q[ii].contiguous().cuda(), k[ii].contiguous().cuda(), v[ii].contiguous().cuda(), scale)
+    torch.cuda.synchronize()
+    assert max_abs(ol.cpu(), o[ii]) <= 1e-2
+    assert max_abs(lsel.cpu(), lse[:, ii]) <= 1e-3
+
+
+@pytest.mark.parametrize("cfg,seed", [("agentic8k", 0), ("wide", None)])
+def test_full_size_sampled_rows(tt, cfg, seed):
+    """BASELINE configs at full size and the bench launch configuration; the oracle evaluates a
+    sample of query rows (O, LSE, dQ) and of keys (dK, dV) one by one."""
+    import torch
+    t = trees.config_tree(cfg, seed)
+    c = trees.CONFIGS[cfg]
+    hq, hkv, d = c["hq"], c["hkv"], c["d"]
+    pk, (q, k, v, G, scale), (o, lse, dq, dk, dv) = _run(tt, t, hq, hkv, d, "bf16", seed=21)
+    opk = oracle.pack(t.parent, t.length)
+    N = opk["n_tokens"]
+    rng = np.random.default_rng(0)
+    want = np.zeros(N, np.uint8)
+    want[rng.choice(N, 48, replace=False)] = 1
+    want[[0, N - 1]] = 1
+    # keys: leaf-level keys have short query ranges; plus a few random keys if cheap
+    span = opk["E"] - np.arange(N)
+    cand = np.flatnonzero(span <= 400)
+    wk = np.zeros(N, np.uint8)
+    wk[rng.choice(cand, min(24, len(cand)), replace=False)] = 1
+    oo, olse = oracle.attn_fwd(opk, q, k, v, scale, want=want, check_invariant=False)
+    m = want.astype(bool)
+    assert max_abs(o[m], oo[m]) <= TOL_O_BF16
+    assert max_abs(lse[:, m], olse[:, m]) <= TOL_O_BF16
+    odq, odk, odv = oracle.attn_bwd(opk, q, k, v, G, scale, want_q=want, want_k=wk)
+    mk = wk.astype(bool)
+    assert rel_l2(dq[m], odq[m]) <= TOL_G_BF16
+    assert rel_l2(dk[mk], odk[mk]) <= TOL_G_BF16
+    assert rel_l2(dv[mk], odv[mk]) <= TOL_G_BF16
+
+
+def test_unsupported_shapes_fail_loudly(tt):
+    import torch
+    pk = tt.tt_pack([-1], [64])
+    q = torch.zeros(64, 2, 96, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(tt.TTError) as ei:
+        tt.tt_attn_fwd(pk, q, q, q)
+    assert ei.value.code == 5
+    q = torch.zeros(64, 3, 128, dtype=torch.bfloat16, device="cuda")
+    k = torch.zeros(64, 2, 128, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(tt.TTError):
+        tt.tt_attn_fwd(pk, q, k, k)

@@ -1,0 +1,115 @@
+"""GPU parity for the Gradient-Restoration loss (tt_restore_loss) and the fp64 sum-of-squares
+(tt_grad_sqnorm) against the oracle."""
+import numpy as np
+import pytest
+
+import oracle
+from workloads import trees, tensors
+from _util import to64
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def tt():
+    import paper_2511_00413_b200 as P
+    P.lib()
+    return P
+
+
+def _compare(tt, t, V, rows=None, gamma=1.0, node_mask=None, boundary_mode=0, inplace=False, seed=0):
+    import torch
+    pk = tt.tt_pack(t.parent, t.length, t.term)
+    N = pk.n_tokens
+    x = tensors.logits_tensor(N, V, seed=seed)
+    tok = tensors.token_ids(N, V, seed=seed + 1)
+    xd = x.cuda()
+    tl = torch.empty(N, dtype=torch.float32, device="cuda")
+    sums, dl, _, err = tt.tt_restore_loss(pk, xd, tok.cuda(), grad_scale=gamma, node_loss_mask=node_mask,
+                                          boundary_mode=boundary_mode, dlogits=xd if inplace else None, tok_loss=tl)
+    torch.cuda.synchronize()
+    assert int(err.item()) == 0
+    opk = oracle.pack(t.parent, t.length, t.term)
+    rows = np.arange(N) if rows is None else np.asarray(rows)
+    lr, om, dx = oracle.loss(opk, tok.numpy(), V, rows, x[torch.as_tensor(rows)], gamma=gamma,
+                             node_loss_mask=node_mask, boundary_mode=boundary_mode)
+    g = to64(dl.cpu()[torch.as_tensor(rows)])
+    tol = 2.0 ** -8 * np.abs(dx) + 1e-5 * abs(gamma) * np.maximum(om, 1.0)[:, None]
+    assert np.all(np.abs(g - dx) <= tol)
+    tlr = to64(tl.cpu())[rows]
+    assert np.allclose(tlr, lr, rtol=1e-5, atol=1e-4 * np.maximum(om, 1).max())
+    if len(rows) == N:
+        s = sums.cpu().numpy()
+        assert abs(s[0] - lr.sum()) <= 1e-5 * max(1.0, abs(lr.sum()))
+        assert s[1] == om.sum()
+    return sums
+
+
+@pytest.mark.parametrize("t", [trees.spec_example(), trees.fig4_unit(), trees.tiny(),
+                               trees.gen_agentic(600, root_len=100, seed=3),
+                               trees.Tree([-1, 0, 0, 2, -1, 4, 4], [0, 20, 0, 7, 15, 0, 3]),
+                               trees.Tree([-1, 0, 0], [13, 7, 5], [1, 2, 1])], ids=lambda t: t.name)
+def test_loss_small_vocab(tt, t):
+    _compare(tt, t, V=1000, gamma=0.5)
+
+
+def test_loss_vocab_not_multiple_of_8_rows_padded(tt):
+    # ld must be a multiple of 8; vocab may be smaller than ld (padding ignored)
+    import torch
+    t = trees.spec_example()
+    pk = tt.tt_pack(t.parent, t.length)
+    N, V, ld = 12, 37, 40
+    x = tensors.logits_tensor(N, ld, seed=5)
+    tok = tensors.token_ids(N, V, seed=6)
+    sums, dl, _, err = tt.tt_restore_loss(pk, x.cuda(), tok.cuda(), vocab=V)
+    torch.cuda.synchronize()
+    opk = oracle.pack(t.parent, t.length)
+    lr, om, dx = oracle.loss(opk, tok.numpy(), V, np.arange(N), x[:, :V])
+    assert abs(sums.cpu()[0].item() - lr.sum()) < 1e-4
+    g = to64(dl.cpu()[:, :V])
+    assert np.all(np.abs(g - dx) <= 2.0 ** -8 * np.abs(dx) + 1e-5 * np.maximum(om, 1)[:, None])
+
+
+def test_loss_node_mask_and_boundary_mode(tt):
+    t = trees.fig4_unit()
+    mask = np.array([1, 1, 0, 1, 1, 0, 1, 1, 1], np.uint8)
+    _compare(tt, t, V=64, node_mask=mask)
+    _compare(tt, trees.spec_example(), V=64, boundary_mode=1)
+
+
+def test_loss_inplace_alias(tt):
+    _compare(tt, trees.gen_agentic(300, root_len=60, seed=2), V=2048, gamma=2.0, inplace=True)
+
+
+def test_loss_full_vocab_wide_sampled(tt):
+    """Config 4 at full size (V = 151,936, 12,835 rows, in-place as in the bench); the oracle
+    checks a sample of rows including the 4K-prefix's last token (64 continuations)."""
+    t = trees.config_tree("wide")
+    rows = [0, 1, 4094, 4095, 4096, 8000, 12834, 12000]
+    _compare(tt, t, V=151936, rows=rows, inplace=True, seed=9)
+
+
+def test_loss_bad_token_sets_error(tt):
+    import torch
+    t = trees.spec_example()
+    pk = tt.tt_pack(t.parent, t.length)
+    x = tensors.logits_tensor(12, 64, seed=1).cuda()
+    tok = torch.zeros(12, dtype=torch.int32)
+    tok[3] = 64  # out of range
+    sums, dl, _, err = tt.tt_restore_loss(pk, x, tok.cuda())
+    torch.cuda.synchronize()
+    assert int(err.item()) == 1
+    assert np.isnan(sums.cpu()[0].item())
+
+
+def test_sqnorm(tt):
+    import torch
+    for n, dt in ((1, torch.float32), (1000003, torch.bfloat16), (77, torch.float32)):
+        x = torch.randn(n, generator=torch.Generator().manual_seed(n)).to(dt)
+        out = tt.tt_grad_sqnorm(x.cuda())
+        torch.cuda.synchronize()
+        ref = float((to64(x) ** 2).sum())
+        assert abs(out.item() - ref) <= 1e-12 * max(ref, 1.0)
+        out2 = tt.tt_grad_sqnorm(x.cuda())
+        torch.cuda.synchronize()
+        assert out2.item() == out.item()  # deterministic
