@@ -15,11 +15,6 @@ bool sm100_available() {
   return cached == 1;
 }
 
-tt_status sm100_attn_fwd(const tt_packed& pk, const void* q, const void* k, const void* v, int hq, int hkv, int d,
-                         float scale, void* o, float* lse, cudaStream_t st) {
-  return simt_attn_fwd(pk, q, k, v, TT_BF16, hq, hkv, d, scale, o, lse, st);
-}
-
 tt_status sm100_attn_bwd(const tt_packed& pk, const void* q, const void* k, const void* v, const float* lse,
                          const float* Dvec, const void* dout, int restore, int hq, int hkv, int d, float scale,
                          float* dq_acc, void* dq, void* dk, void* dv, cudaStream_t st) {

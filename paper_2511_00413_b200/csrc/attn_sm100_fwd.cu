@@ -1,0 +1,391 @@
+// attn_sm100_fwd.cu — tree-masked attention forward on sm_100a tensor cores (tcgen05 + TMEM + TMA).
+//
+// What it computes (Eq. 1, with an explicit softmax scale R1 and the shared-prefix mask
+// of P:531-533 in its interval form j <= i < E_j, R2):
+//   O_i = sum_j softmax_j(scale q_i.k_j) v_j,   LSE_i = ln sum_j exp(scale q_i.k_j)
+//
+// Design.  One CTA owns two adjacent 128-row query tiles (q-blocks 2p, 2p+1) of one
+// head and walks the UNION of their non-empty k-tiles in ascending order (the pack's tile lists);
+// empty tiles are never loaded or multiplied, full tiles run unmasked, partial tiles are masked in
+// registers.  K/V tiles are shared by both query tiles, so each TMA'd K/V byte feeds two MMAs.
+//   warp 0      TMA producer: Q0/Q1 once, then K/V(+E) tiles into a 2-stage ring (SWIZZLE_128B)
+//   warp 1      TMEM allocator (512 columns: S0 | S1 | O0 | O1) and MMA issuer (one thread):
+//               S_i = Q_i K^T (SS, M=N=128, K=128) into TMEM, then O_i += P_i V with P_i read from
+//               TMEM (TS) — FA4-style order PV_0, S_0', PV_1, S_1'
+//   warps 2-5   softmax of query tile 0 (one thread per row: tcgen05.ld 32x32b gives each thread
+//   warps 6-9   softmax of query tile 1  its row, so row max / row sum are thread-local; the TMEM
+//               lane quadrant of a warp is warp % 4)
+// Softmax keeps the running max in log2 units and only rescales the O accumulator in TMEM when
+// the max grows by more than 2^8 (stale-max trick; exact after the final 1/l).  P (bf16) is
+// written back over S in TMEM and consumed by the TS MMA; the epilogue divides by l and stores
+// O (bf16) and LSE (fp32, natural log).
+#include <cudaTypedefs.h>
+
+#include "sm100_ptx.cuh"
+#include "tt_internal.cuh"
+
+namespace tt {
+namespace {
+using namespace sm100;
+
+constexpr int kD = 128;
+constexpr int kStages = 2;
+constexpr int kFwdThreads = 320;  // 10 warps: producer, MMA, 2 x 4 softmax warps
+constexpr uint32_t kTileBytes = 128 * kD * 2;  // 32 KB: two 16 KB SWIZZLE_128B chunks (d 0-63 | 64-127)
+constexpr uint32_t kChunkBytes = 128 * 64 * 2;
+constexpr uint32_t kOffQ = 0;                       // Q0, Q1
+constexpr uint32_t kOffKV = 2 * kTileBytes;         // stage s: K at +s*64K, V at +s*64K+32K
+constexpr uint32_t kOffE = kOffKV + kStages * 2 * kTileBytes;  // E of the stage's 128 keys (512 B)
+constexpr uint32_t kOffBar = kOffE + kStages * 512;
+constexpr uint32_t kNumBars = 1 + 2 * kStages + 6;
+constexpr uint32_t kOffMisc = kOffBar + kNumBars * 8;
+constexpr uint32_t kOffTiles = kOffMisc + 16;
+constexpr float kRescaleThreshold = 8.0f;  // log2 units
+
+struct FwdParams {
+  int64_t N;
+  int hq, hkv, nb, npairs;
+  float scale_log2;
+  const int32_t* E;
+  const int32_t* fwd_cnt;
+  const int32_t* fwd_list;
+  __nv_bfloat16* o;
+  float* lse;
+};
+
+__device__ __forceinline__ int tile_cls(int32_t e, int i) { return (e >> (28 + 2 * i)) & 3; }
+
+__global__ void __launch_bounds__(kFwdThreads, 1)
+    tree_attn_fwd_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                        const __grid_constant__ CUtensorMap tmV, const FwdParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBar);
+  uint64_t* bar_q = bars;
+  uint64_t* full = bars + 1;
+  uint64_t* empty = bars + 1 + kStages;
+  uint64_t* s_full = bars + 1 + 2 * kStages;
+  uint64_t* p_full = s_full + 2;
+  uint64_t* o_full = s_full + 4;
+  uint32_t* misc = reinterpret_cast<uint32_t*>(smem + kOffMisc);  // [0] tmem base, [1] n tiles
+  int32_t* tiles = reinterpret_cast<int32_t*>(smem + kOffTiles);
+  uint8_t* flags0 = reinterpret_cast<uint8_t*>(tiles + 2 * p.nb + 4);
+  uint8_t* flags1 = flags0 + p.nb + 4;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int pair = p.npairs - 1 - (int)(blockIdx.x / p.hq);  // heavy (late) query blocks first
+  const int h = (int)(blockIdx.x % p.hq);
+  const int hk = h / (p.hq / p.hkv);
+  const int qa = 2 * pair;
+  const bool has1 = qa + 1 < p.nb;
+  const int kb_end = has1 ? qa + 2 : qa + 1;
+
+  // ---- merged tile list of the two query blocks: kb | cls0 << 28 | cls1 << 30 ----
+  for (int k = threadIdx.x; k < kb_end; k += kFwdThreads) { flags0[k] = 0; flags1[k] = 0; }
+  __syncthreads();
+  {
+    const int n0 = p.fwd_cnt[qa];
+    const int32_t* l0 = p.fwd_list + tri_off(qa);
+    for (int k = threadIdx.x; k < n0; k += kFwdThreads) flags0[l0[k] & kKbMask] = (uint8_t)(l0[k] >> kClsShift);
+    if (has1) {
+      const int n1 = p.fwd_cnt[qa + 1];
+      const int32_t* l1 = p.fwd_list + tri_off(qa + 1);
+      for (int k = threadIdx.x; k < n1; k += kFwdThreads) flags1[l1[k] & kKbMask] = (uint8_t)(l1[k] >> kClsShift);
+    }
+  }
+  __syncthreads();
+  if (warp == 0) {
+    int cnt = 0;
+    for (int base = 0; base < kb_end; base += 32) {
+      const int kb = base + lane;
+      const int v = kb < kb_end ? (flags0[kb] | (flags1[kb] << 2)) : 0;
+      const unsigned bal = __ballot_sync(0xffffffffu, v != 0);
+      if (v) tiles[cnt + __popc(bal & ((1u << lane) - 1u))] = kb | (v << kClsShift);
+      cnt += __popc(bal);
+    }
+    if (lane == 0) misc[1] = cnt;
+  } else if (warp == 1) {
+    if (lane == 0) {
+      mbar_init(bar_q, 1);
+      for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+      for (int i = 0; i < 2; ++i) { mbar_init(&s_full[i], 1); mbar_init(&p_full[i], 128); mbar_init(&o_full[i], 1); }
+      mbar_fence_init();
+    }
+    __syncwarp();
+    tmem_alloc(&misc[0], 512);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const int T = (int)misc[1];
+  const uint32_t tmem = misc[0];
+
+  if (warp < 2) {
+    if (warp == 0 && lane == 0) {
+      // ===================== TMA producer =====================
+      tma_prefetch(&tmQ);
+      tma_prefetch(&tmK);
+      tma_prefetch(&tmV);
+      mbar_expect_tx(bar_q, (has1 ? 2 : 1) * kTileBytes);
+      for (int i = 0; i < (has1 ? 2 : 1); ++i)
+        for (int c = 0; c < 2; ++c)
+          tma_load_3d(smem + kOffQ + i * kTileBytes + c * kChunkBytes, &tmQ, bar_q, c * 64, h, (qa + i) * 128);
+      for (int t = 0; t < T; ++t) {
+        const int s = t % kStages;
+        if (t >= kStages) mbar_wait(&empty[s], ((t / kStages) - 1) & 1);
+        const int kb = tiles[t] & kKbMask;
+        uint8_t* kd = smem + kOffKV + s * 2 * kTileBytes;
+        mbar_expect_tx(&full[s], 2 * kTileBytes + 512);
+        bulk_load_1d(smem + kOffE + s * 512, p.E + (int64_t)kb * 128, 512, &full[s]);
+        for (int c = 0; c < 2; ++c) tma_load_3d(kd + c * kChunkBytes, &tmK, &full[s], c * 64, hk, kb * 128);
+        for (int c = 0; c < 2; ++c)
+          tma_load_3d(kd + kTileBytes + c * kChunkBytes, &tmV, &full[s], c * 64, hk, kb * 128);
+      }
+    } else if (warp == 1 && lane == 0) {
+      // ===================== MMA issuer =====================
+      constexpr uint32_t idS = idesc_bf16(128, 128, 0, 0);  // Q (K-major) x K^T (K-major)
+      constexpr uint32_t idO = idesc_bf16(128, 128, 0, 1);  // P (TMEM, K-major) x V (MN-major)
+      int last[2] = {-1, -1};
+      for (int t = 0; t < T; ++t) {
+        if (tile_cls(tiles[t], 0)) last[0] = t;
+        if (tile_cls(tiles[t], 1)) last[1] = t;
+      }
+      const uint32_t qbase = smem_u32(smem + kOffQ);
+      auto issue_S = [&](int i, int t) {
+        const uint32_t kbase = smem_u32(smem + kOffKV + (t % kStages) * 2 * kTileBytes);
+        const uint32_t qb = qbase + i * kTileBytes;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t off = (kk >> 2) * kChunkBytes + (kk & 3) * 32;
+          mma_ss(tmem + 128 * i, sdesc(qb + off, 16, 1024), sdesc(kbase + off, 16, 1024), idS, kk > 0);
+        }
+        mma_commit(&s_full[i]);
+      };
+      uint32_t pph[2] = {0, 0};
+      bool first[2] = {true, true};
+      mbar_wait(bar_q, 0);
+      if (T > 0) {
+        mbar_wait(&full[0], 0);
+        tc_fence_after();
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+          if (tile_cls(tiles[0], i)) issue_S(i, 0);
+      }
+      for (int t = 0; t < T; ++t) {
+        const int s = t % kStages;
+        const uint32_t vbase = smem_u32(smem + kOffKV + s * 2 * kTileBytes + kTileBytes);
+        bool waited = false;
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          if (tile_cls(tiles[t], i)) {
+            mbar_wait(&p_full[i], pph[i]);
+            pph[i] ^= 1;
+            tc_fence_after();
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk)
+              mma_ts(tmem + 256 + 128 * i, tmem + 128 * i + kk * 8, sdesc(vbase + kk * 2048, kChunkBytes, 1024), idO,
+                     (!first[i] || kk > 0) ? 1u : 0u);
+            first[i] = false;
+            if (t == last[i]) mma_commit(&o_full[i]);
+          }
+          if (t + 1 < T && tile_cls(tiles[t + 1], i)) {
+            if (!waited) {
+              mbar_wait(&full[(t + 1) % kStages], ((t + 1) / kStages) & 1);
+              tc_fence_after();
+              waited = true;
+            }
+            issue_S(i, t + 1);
+          }
+        }
+        mma_commit(&empty[s]);
+      }
+    }
+  } else {
+    // ===================== softmax warpgroups =====================
+    const int i = (warp - 2) >> 2;  // query tile
+    const int q = warp & 3;         // TMEM lane quadrant
+    const int r = q * 32 + lane;
+    const int64_t row = (int64_t)(qa + i) * 128 + r;
+    const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
+    const uint32_t tS = tl + 128 * i;
+    const uint32_t tO = tl + 256 + 128 * i;
+    const float sl2 = p.scale_log2;
+    float m = -INFINITY, l = 0.f;
+    uint32_t sph = 0;
+    bool first = true;
+    if (i == 0 || has1) {
+      for (int t = 0; t < T; ++t) {
+        const int32_t e = tiles[t];
+        const int cls = tile_cls(e, i);
+        if (!cls) continue;
+        const int kb = e & kKbMask;
+        const int64_t j0 = (int64_t)kb * 128;
+        mbar_wait(&s_full[i], sph);
+        sph ^= 1;
+        tc_fence_after();
+        uint32_t s[128];
+        tmem_ld32(tS + 0, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
+        tmem_ld32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
+        tmem_ld32(tS + 64, *reinterpret_cast<uint32_t(*)[32]>(&s[64]));
+        tmem_ld32(tS + 96, *reinterpret_cast<uint32_t(*)[32]>(&s[96]));
+        tmem_wait_ld();
+        // ---- mask (partial tiles, and key columns past N on the ragged last block) ----
+        if (cls == kClsPartial) {
+          const int4* Es = reinterpret_cast<const int4*>(smem + kOffE + (t % kStages) * 512);
+          const int64_t jmax = p.N - j0;  // keys c >= jmax do not exist
+#pragma unroll
+          for (int c4 = 0; c4 < 32; ++c4) {
+            const int4 ev = Es[c4];
+            const int ee[4] = {ev.x, ev.y, ev.z, ev.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int c = 4 * c4 + u;
+              const bool ok = (c < jmax) && (j0 + c <= row) && (row < (int64_t)ee[u]);
+              if (!ok) s[c] = __float_as_uint(-INFINITY);
+            }
+          }
+        } else if (j0 + 128 > p.N) {
+          const int64_t jmax = p.N - j0;
+#pragma unroll
+          for (int c = 0; c < 128; ++c)
+            if (c >= jmax) s[c] = __float_as_uint(-INFINITY);
+        }
+        // ---- row max (log2 units) ----
+        float mx = -INFINITY;
+#pragma unroll
+        for (int c = 0; c < 128; ++c) mx = fmaxf(mx, __uint_as_float(s[c]));
+        const float m_new = fmaxf(m, mx * sl2);
+        const bool resc = (m == -INFINITY) ? (m_new != -INFINITY) : (m_new > m + kRescaleThreshold);
+        const float m_use = resc ? m_new : m;
+        const float corr = (m == -INFINITY) ? 0.f : ex2(m - m_use);
+        const float mb = (m_use == -INFINITY) ? 0.f : m_use;
+        // ---- P = exp2(s * scale_log2 - m), packed bf16 in place (s[0..63]) ----
+        float lsum0 = 0.f, lsum1 = 0.f;
+#pragma unroll
+        for (int c = 0; c < 128; c += 2) {
+          const float p0 = ex2(fmaf(__uint_as_float(s[c]), sl2, -mb));
+          const float p1 = ex2(fmaf(__uint_as_float(s[c + 1]), sl2, -mb));
+          lsum0 += p0;
+          lsum1 += p1;
+          s[c >> 1] = pack_bf16(p0, p1);
+        }
+        l = l * corr + (lsum0 + lsum1);
+        m = m_use;
+        // ---- lazy rescale of the O accumulator (PV of the previous tile has completed: its
+        //      commit precedes the s_full arrival we waited on) ----
+        if (!first && __any_sync(0xffffffffu, resc)) {
+#pragma unroll 1
+          for (int cc = 0; cc < 4; ++cc) {
+            uint32_t ov[32];
+            tmem_ld32(tO + 32 * cc, ov);
+            tmem_wait_ld();
+#pragma unroll
+            for (int u = 0; u < 32; ++u) ov[u] = __float_as_uint(__uint_as_float(ov[u]) * corr);
+            tmem_st32(tO + 32 * cc, ov);
+          }
+        }
+        tmem_st32(tS + 0, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
+        tmem_st32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(&p_full[i]);
+        first = false;
+      }
+      // ---- epilogue: O / l -> bf16, LSE ----
+      mbar_wait(&o_full[i], 0);
+      tc_fence_after();
+      const float inv = (l > 0.f) ? 1.f / l : 0.f;
+      __nv_bfloat16* orow = p.o + (row * p.hq + h) * kD;
+#pragma unroll 1
+      for (int cc = 0; cc < 4; ++cc) {
+        uint32_t ov[32];
+        tmem_ld32(tO + 32 * cc, ov);
+        tmem_wait_ld();
+        if (row < p.N) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int u = 0; u < 16; ++u)
+            pk[u] = pack_bf16(__uint_as_float(ov[2 * u]) * inv, __uint_as_float(ov[2 * u + 1]) * inv);
+          uint4* dst = reinterpret_cast<uint4*>(orow + 32 * cc);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) dst[u] = make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+        }
+      }
+      if (row < p.N) p.lse[(int64_t)h * p.N + row] = (m + __log2f(l)) * kLn2;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------------------ host side
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult qr;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &qr) == cudaSuccess &&
+        qr == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }
+  return fn;
+}
+
+// [rows, heads, d] bf16 ("thd") as a 3-D tensor map with a {64, 1, box_rows} SWIZZLE_128B box.
+tt_status make_tmap_thd(CUtensorMap* m, const void* ptr, int64_t rows, int heads, int d, int box_rows,
+                        CUtensorMapDataType dt, int elem_bytes, CUtensorMapSwizzle sw, int box_inner) {
+  auto fn = encode_fn();
+  if (!fn) { set_error("cuTensorMapEncodeTiled unavailable"); return TT_ERR_CUDA; }
+  cuuint64_t dims[3] = {(cuuint64_t)d, (cuuint64_t)heads, (cuuint64_t)rows};
+  cuuint64_t strides[2] = {(cuuint64_t)d * elem_bytes, (cuuint64_t)heads * d * elem_bytes};
+  cuuint32_t box[3] = {(cuuint32_t)box_inner, 1, (cuuint32_t)box_rows};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = fn(m, dt, 3, const_cast<void*>(ptr), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) { set_error("cuTensorMapEncodeTiled failed (%d)", (int)r); return TT_ERR_CUDA; }
+  return TT_OK;
+}
+
+size_t sm100_fwd_smem_bytes(int nb) {
+  return 1024 + kOffTiles + (size_t)(2 * nb + 4) * 4 + 2 * (size_t)(nb + 4) + 16;
+}
+
+tt_status sm100_attn_fwd(const tt_packed& pk, const void* q, const void* k, const void* v, int hq, int hkv, int d,
+                         float scale, void* o, float* lse, cudaStream_t st) {
+  if (d != kD) { set_error("sm100_attn_fwd: d must be 128"); return TT_ERR_UNSUPPORTED; }
+  const int nb = pk.n_blk;
+  const size_t smem = sm100_fwd_smem_bytes(nb);
+  if (smem > 232448) { set_error("sm100_attn_fwd: %d blocks exceed the tile-list smem budget", nb); return TT_ERR_TOO_LARGE; }
+  CUtensorMap mq, mk, mv;
+  tt_status s;
+  if ((s = make_tmap_thd(&mq, q, pk.n_tokens, hq, d, 128, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, CU_TENSOR_MAP_SWIZZLE_128B, 64))) return s;
+  if ((s = make_tmap_thd(&mk, k, pk.n_tokens, hkv, d, 128, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, CU_TENSOR_MAP_SWIZZLE_128B, 64))) return s;
+  if ((s = make_tmap_thd(&mv, v, pk.n_tokens, hkv, d, 128, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, CU_TENSOR_MAP_SWIZZLE_128B, 64))) return s;
+  FwdParams prm;
+  prm.N = pk.n_tokens;
+  prm.hq = hq;
+  prm.hkv = hkv;
+  prm.nb = nb;
+  prm.npairs = (nb + 1) / 2;
+  prm.scale_log2 = scale * kLog2e;
+  prm.E = pk.E;
+  prm.fwd_cnt = pk.fwd_cnt;
+  prm.fwd_list = pk.fwd_list;
+  prm.o = static_cast<__nv_bfloat16*>(o);
+  prm.lse = lse;
+  cudaError_t e = cudaFuncSetAttribute(tree_attn_fwd_sm100, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) { set_error("sm100_attn_fwd: smem attribute: %s", cudaGetErrorString(e)); return TT_ERR_CUDA; }
+  const unsigned grid = (unsigned)prm.npairs * hq;
+  tree_attn_fwd_sm100<<<grid, kFwdThreads, smem, st>>>(mq, mk, mv, prm);
+  count_launch();
+  return check_launch("tree_attn_fwd_sm100");
+}
+
+}  // namespace tt

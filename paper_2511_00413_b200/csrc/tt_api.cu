@@ -166,10 +166,12 @@ static PackLayout pack_layout(int64_t N, int32_t n, int32_t n_succ, int32_t n_or
   PackLayout L{};
   L.nb = (int32_t)ceil_div<int64_t>(N, kBlock);
   size_t o = 0;
-  L.off_pos = o; o = al256(o + N * 4);
-  L.off_w = o; o = al256(o + N * 4);
-  L.off_E = o; o = al256(o + N * 4);
-  L.off_node = o; o = al256(o + N * 4);
+  // per-token arrays are padded to whole 128-token blocks (kernels bulk-copy E per block)
+  const size_t Np = (size_t)L.nb * kBlock;
+  L.off_pos = o; o = al256(o + Np * 4);
+  L.off_w = o; o = al256(o + Np * 4);
+  L.off_E = o; o = al256(o + Np * 4);
+  L.off_node = o; o = al256(o + Np * 4);
   L.off_kmin = o; o = al256(o + (size_t)L.nb * 4);
   L.off_kmax = o; o = al256(o + (size_t)L.nb * 4);
   L.off_fcnt = o; o = al256(o + (size_t)L.nb * 4);

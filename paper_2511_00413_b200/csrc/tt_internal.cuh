@@ -9,6 +9,8 @@
 #include <cstdio>
 #include <string>
 
+#include <cuda.h>
+
 #include "../../include/tt.h"
 
 namespace tt {
@@ -54,6 +56,8 @@ tt_status launch_bwd_pre(const void* o, const void* dout, tt_dtype dt, int64_t N
                          float* dq_acc, cudaStream_t st);
 
 bool sm100_available();
+tt_status make_tmap_thd(CUtensorMap* m, const void* ptr, int64_t rows, int heads, int d, int box_rows,
+                        CUtensorMapDataType dt, int elem_bytes, CUtensorMapSwizzle sw, int box_inner);
 tt_status sm100_attn_fwd(const tt_packed& pk, const void* q, const void* k, const void* v, int hq, int hkv,
                          int d, float scale, void* o, float* lse, cudaStream_t st);
 tt_status sm100_attn_bwd(const tt_packed& pk, const void* q, const void* k, const void* v, const float* lse,
