@@ -15,11 +15,4 @@ bool sm100_available() {
   return cached == 1;
 }
 
-tt_status sm100_attn_bwd(const tt_packed& pk, const void* q, const void* k, const void* v, const float* lse,
-                         const float* Dvec, const void* dout, int restore, int hq, int hkv, int d, float scale,
-                         float* dq_acc, void* dq, void* dk, void* dv, cudaStream_t st) {
-  (void)dq_acc;
-  return simt_attn_bwd(pk, q, k, v, lse, Dvec, dout, restore, TT_BF16, hq, hkv, d, scale, dq, dk, dv, st);
-}
-
 }  // namespace tt
