@@ -1,0 +1,529 @@
+#!/usr/bin/env python
+"""bench.py — Tree Training hot path on B200: one JSON line per run (driver contract).
+
+A "step" is one pass of the whole hot path of SURVEY.md §8(a) over one tree per rank:
+  a1 tt_pack (host DFS + device fill/tile lists)   a2 tt_attn_fwd   a3 tt_restore_loss
+  a4+a5 tt_attn_bwd (preprocess + main + dQ convert)   a6 tt_grad_sqnorm x3 + NCCL all_gather
+  of the per-tree fp64 scalars (N > 1).
+Default workload (N = 1): BASELINE.json configs[1] "agentic tree 8K packed tokens, branching
+factor 2-4, depth 6, 32 heads, head_dim 128, bf16" (workloads.gen_agentic seed = rank), with the
+Gradient-Restoration loss at the Qwen3 vocabulary (151,936).  Each rank processes its own tree
+(weak scaling).  `--config batch64k --trees 64` runs config 5 (64 trees x 64K, LPT-partitioned).
+
+value = effective attention FLOPs of the step (14 d Hq A per tree, A = ancestor pairs, i.e.
+only unmasked pairs count) summed over ranks / (max over ranks of the device-timed step time).
+Timing: W untimed warm-up steps, then K steps each bracketed by CUDA events on the launching
+stream, L2 flushed (256 MiB write) between steps outside the events, barrier + synchronize around
+the whole timed loop, max over ranks.
+
+`--impl reference` times the fp64 CPU oracle (oracle/) on the same workload/metric (bounded
+sample per step, extrapolated) — see the cpu_baseline notes in DESIGN.md.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "tree-attn fwd+bwd effective TFLOP/s & % BF16 peak; speedup vs per-branch linear"
+VOCAB = 151936
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return dict(bf16=float(d["bf16_tflops"]), bf16_sustained=float(d.get("bf16_tflops_sustained", d["bf16_tflops"])),
+                    hbm=float(d["hbm_gbs"]), source="measured (MEASURED_PEAKS.json)")
+    return dict(bf16=1590.0, bf16_sustained=1400.0, hbm=6650.0, source="fallback (B200_PROFILING.md)")
+
+
+# ------------------------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for nm, val in zip(names, f[4:8]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------------ workload
+def make_trees(args, rank, world):
+    from workloads import trees
+    if args.config == "batch64k":
+        all_trees = [trees.config_tree("batch64k", s) for s in range(args.trees)]
+        from paper_2511_00413_b200 import tt_pack_plan
+        work = [tt_pack_plan(t.parent, t.length)["n_pairs"] for t in all_trees]
+        # greedy LPT over ranks (descending work, ties by tree id) — deterministic
+        order = sorted(range(len(all_trees)), key=lambda i: (-work[i], i))
+        load = [0] * world
+        assign = [[] for _ in range(world)]
+        for i in order:
+            r = min(range(world), key=lambda x: (load[x], x))
+            assign[r].append(i)
+            load[r] += work[i]
+        mine = sorted(assign[rank])
+        imb = max(load) / (sum(load) / world)
+        return [(i, all_trees[i]) for i in mine], {"lpt_imbalance": round(imb, 4)}
+    seed = rank if args.seed is None else args.seed
+    return [(seed, trees.config_tree(args.config, seed))], {}
+
+
+class TreeJob:
+    """Device-resident inputs + outputs for one tree (allocated once, untimed)."""
+
+    def __init__(self, tid, tree, cfg, vocab, gen, with_loss=True, host_copy=False):
+        import torch
+        import paper_2511_00413_b200 as tt
+        self.tid, self.tree = tid, tree
+        self.hq, self.hkv, self.d = cfg["hq"], cfg["hkv"], cfg["d"]
+        info = tt.tt_pack_plan(tree.parent, tree.length)
+        self.info = info
+        N = self.N = info["n_tokens"]
+        dt = torch.bfloat16
+        dev = "cuda"
+        self.q = torch.randn(N, self.hq, self.d, device=dev, dtype=torch.float32, generator=gen).to(dt)
+        self.k = torch.randn(N, self.hkv, self.d, device=dev, dtype=torch.float32, generator=gen).to(dt)
+        self.v = torch.randn(N, self.hkv, self.d, device=dev, dtype=torch.float32, generator=gen).to(dt)
+        self.g = torch.randn(N, self.hq, self.d, device=dev, dtype=torch.float32, generator=gen).to(dt)
+        self.o = torch.empty_like(self.q)
+        self.lse = torch.empty(self.hq, N, device=dev)
+        self.dq, self.dk, self.dv = torch.empty_like(self.q), torch.empty_like(self.k), torch.empty_like(self.v)
+        self.ws = None
+        self.with_loss = with_loss
+        self.vocab = vocab
+        if with_loss:
+            self.logits = torch.empty(N, vocab, device=dev, dtype=dt)
+            for r0 in range(0, N, 2048):  # chunked to bound the fp32 temporary
+                r1 = min(N, r0 + 2048)
+                self.logits[r0:r1] = (2.0 * torch.randn(r1 - r0, vocab, device=dev, generator=gen)).to(dt)
+            self.tok = torch.randint(0, vocab, (N,), device=dev, dtype=torch.int32, generator=gen)
+            self.dlogits = torch.empty_like(self.logits)
+            self.tok_loss = torch.empty(N, device=dev)
+            self.sums = torch.zeros(2, dtype=torch.float64, device=dev)
+            self.err = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.rec = torch.zeros(5, dtype=torch.float64, device=dev)
+        self.host = None
+        if host_copy:
+            names = ["q", "k", "v", "g"] + (["logits", "tok"] if with_loss else [])
+            self.host = {n: getattr(self, n).cpu().pin_memory() for n in names}
+            self.rec_host = torch.zeros(5, dtype=torch.float64).pin_memory()
+
+    def flops(self):
+        return 14.0 * self.d * self.hq * self.info["n_pairs"]
+
+    def h2d_bytes(self):
+        return sum(t.numel() * t.element_size() for t in self.host.values()) if self.host else 0
+
+
+def run_step(job, ev=None, h2d=False):
+    """One pass of the hot path for one tree.  ev: dict of event pairs for per-op timing."""
+    import torch
+    import paper_2511_00413_b200 as tt
+
+    def mark(name, i):
+        if ev is not None:
+            ev[name][i].record()
+
+    if h2d:
+        for n, t in job.host.items():
+            getattr(job, n).copy_(t, non_blocking=True)
+    mark("pack", 0)
+    pk = tt.tt_pack(job.tree.parent, job.tree.length)                                   # a1
+    mark("pack", 1)
+    mark("fwd", 0)
+    tt.tt_attn_fwd(pk, job.q, job.k, job.v, out=job.o, lse=job.lse)                      # a2
+    mark("fwd", 1)
+    if job.with_loss:
+        mark("loss", 0)
+        tt.tt_restore_loss(pk, job.logits, job.tok, grad_scale=1.0, dlogits=job.dlogits,   # a3
+                           tok_loss=job.tok_loss, sums=job.sums, d_err=job.err)
+        mark("loss", 1)
+    if job.ws is None:
+        job.ws = torch.empty(tt.tt_attn_bwd_workspace(pk, job.hq, job.hkv, job.d, job.q.dtype),
+                             dtype=torch.uint8, device="cuda")
+    mark("bwd", 0)
+    tt.tt_attn_bwd(pk, job.q, job.k, job.v, job.o, job.lse, job.g, restore=True,          # a4 + a5
+                   dq=job.dq, dk=job.dk, dv=job.dv, ws=job.ws)
+    mark("bwd", 1)
+    mark("scal", 0)
+    if job.with_loss:
+        job.rec[0:2].copy_(job.sums)
+    for i, x in enumerate((job.dq, job.dk, job.dv)):                                       # a6
+        tt.tt_grad_sqnorm(x, out=job.rec[2 + i:3 + i])
+    mark("scal", 1)
+    if h2d:
+        job.rec_host.copy_(job.rec, non_blocking=True)
+    return pk
+
+
+def flush_l2(buf):
+    buf.add_(1)  # 256 MiB read+write > 126 MB L2
+
+
+# ------------------------------------------------------------------------------------ linear
+def linear_attention_time(job, reps=5):
+    """Same kernels on the linearised forest (every root-to-leaf trajectory as its own root;
+    untimed gather).  Returns (fwd+bwd ms, linear pairs, linear tokens)."""
+    import torch
+    import oracle  # only for the trajectory paths of the comparison input (untimed setup)
+    import paper_2511_00413_b200 as tt
+    opk = oracle.pack(job.tree.parent, job.tree.length)
+    paths = oracle.paths(opk)
+    idx = torch.as_tensor(np.concatenate(paths).astype(np.int64), device="cuda")
+    lens = [len(p) for p in paths]
+    lq, lk, lv, lg = (x.index_select(0, idx).contiguous() for x in (job.q, job.k, job.v, job.g))
+    pk = tt.tt_pack([-1] * len(lens), lens)
+    o = torch.empty_like(lq)
+    lse = torch.empty(job.hq, pk.n_tokens, device="cuda")
+    dq, dk, dv = torch.empty_like(lq), torch.empty_like(lk), torch.empty_like(lv)
+    ws = torch.empty(tt.tt_attn_bwd_workspace(pk, job.hq, job.hkv, job.d, lq.dtype), dtype=torch.uint8, device="cuda")
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+    ts = []
+    for r in range(reps + 2):
+        flush_l2(flush)
+        a, b = torch.cuda.Event(True), torch.cuda.Event(True)
+        a.record()
+        tt.tt_attn_fwd(pk, lq, lk, lv, out=o, lse=lse)
+        tt.tt_attn_bwd(pk, lq, lk, lv, o, lse, lg, restore=False, dq=dq, dk=dk, dv=dv, ws=ws)
+        b.record()
+        torch.cuda.synchronize()
+        if r >= 2:
+            ts.append(a.elapsed_time(b))
+    return float(np.median(ts)), pk.info["n_pairs"], pk.info["n_tokens"]
+
+
+# ------------------------------------------------------------------------------------ cpu oracle
+def oracle_sample(job_tree, cfg, budget_s=20.0, nthreads=None):
+    """Time the fp64 oracle (as it stands: per-branch linearisation, one std::thread per q head) on
+    a bounded sample of the workload: H = min(Hq, host cores) heads over the first trajectories of
+    the tree, forward + backward.  Returns (seconds measured, the sample's share of the full
+    workload's oracle work = per-branch pairs x heads, trajectories taken, threads used)."""
+    import oracle
+    opk = oracle.pack(job_tree.parent, job_tree.length)
+    paths = oracle.paths(opk)
+    Ls = np.array([len(p) for p in paths], dtype=np.int64)
+    full_work = float((Ls * (Ls + 1) // 2).sum()) * cfg["hq"]
+    d = cfg["d"]
+    heads = max(1, min(cfg["hq"], nthreads or (os.cpu_count() or 1)))
+    cap = budget_s * 3.0e5 * (128.0 / d)  # ~pairs per second per thread (fp64 fwd+bwd, d = 128)
+    take, work = [], 0.0
+    for t, L in enumerate(Ls):
+        w = L * (L + 1) / 2
+        if take and work + w > cap:
+            break
+        take.append(t)
+        work += w
+    sub_idx = np.concatenate([paths[t] for t in take]).astype(np.int32)
+    sub_ptr = np.concatenate([[0], np.cumsum([len(paths[t]) for t in take])]).astype(np.int64)
+    spk = dict(opk)
+    spk["path_ptr"], spk["path_idx"], spk["n_traj"] = sub_ptr, sub_idx, len(take)
+    N = opk["n_tokens"]
+    rng = np.random.default_rng(0)
+    q, k, v, g = (rng.standard_normal((N, heads, d)) for _ in range(4))
+    t0 = time.perf_counter()
+    oracle.attn_fwd(spk, q, k, v, 1 / math.sqrt(d), nthreads=heads)
+    oracle.attn_bwd(spk, q, k, v, g, 1 / math.sqrt(d), nthreads=heads)
+    dt = time.perf_counter() - t0
+    return dt, work * heads / full_work, len(take), heads
+
+
+# ------------------------------------------------------------------------------------ main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="tt", choices=["tt", "reference"])
+    ap.add_argument("--config", default="agentic8k", choices=["agentic8k", "deep32k", "wide", "wide_aligned", "batch64k"])
+    ap.add_argument("--trees", type=int, default=64, help="trees for --config batch64k")
+    ap.add_argument("--seed", type=int, default=None)
+    ap.add_argument("--no-loss", action="store_true")
+    ap.add_argument("--no-linear", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    from workloads import trees as T
+    cfg = T.CONFIGS[args.config]
+
+    if args.impl == "reference":
+        return main_reference(args, rank, world, cfg)
+
+    import torch
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2511_00413_b200 as tt
+    tt.lib()
+
+    my_trees, extra_cfg = make_trees(args, rank, world)
+    gen = torch.Generator(device="cuda").manual_seed(1234 + rank)
+    with_loss = not args.no_loss
+    host_copy = not args.no_e2e
+    jobs = [TreeJob(tid, t, cfg, VOCAB, gen, with_loss=with_loss, host_copy=host_copy) for tid, t in my_trees]
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+    n_total_trees = args.trees if args.config == "batch64k" else world
+    gather = torch.zeros(n_total_trees * 6, dtype=torch.float64, device="cuda") if world > 1 else None
+
+    def do_step(ev=None, h2d=False):
+        recs = []
+        for j in jobs:
+            run_step(j, ev=ev if len(jobs) == 1 else None, h2d=h2d)
+            recs.append(torch.cat([torch.tensor([float(j.tid)], dtype=torch.float64, device="cuda"), j.rec]))
+        if world > 1:
+            # per-tree records [tree id, sum loss, sum Omega, |dQ|^2, |dK|^2, |dV|^2]; fixed-size
+            # per-rank slot so all_gather_into_tensor can be used; summed in tree-id order.
+            per = math.ceil(n_total_trees / world)
+            mine = torch.zeros(per * 6, dtype=torch.float64, device="cuda")
+            mine.fill_(-1.0)
+            if recs:
+                mine[:len(recs) * 6] = torch.cat(recs)
+            out = torch.empty(per * 6 * world, dtype=torch.float64, device="cuda")
+            dist.all_gather_into_tensor(out, mine)
+            return out
+        return torch.cat(recs)
+
+    # warm-up
+    for _ in range(args.warmup):
+        do_step()
+    torch.cuda.synchronize()
+
+    # ---- timed device region ----
+    names = ["pack", "fwd", "loss", "bwd", "scal"]
+    evs = [{n: (torch.cuda.Event(True), torch.cuda.Event(True)) for n in names} for _ in range(args.steps)]
+    step_ev = [(torch.cuda.Event(True), torch.cuda.Event(True)) for _ in range(args.steps)]
+    sampler = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    time.sleep(0.3)
+    tt.tt_launch_count_reset()
+    for s in range(args.steps):
+        flush_l2(flush)
+        step_ev[s][0].record()
+        do_step(ev=evs[s])
+        step_ev[s][1].record()
+    torch.cuda.synchronize()
+    launches = tt.tt_launch_count()
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    step_ms = [a.elapsed_time(b) for a, b in step_ev]
+    my_ms = float(sum(step_ms))
+    per_op = {}
+    if len(jobs) == 1:
+        for n in names:
+            if n == "loss" and not with_loss:
+                continue
+            per_op[n] = float(np.mean([e[n][0].elapsed_time(e[n][1]) for e in evs]))
+    flops_mine = sum(j.flops() for j in jobs) * args.steps
+    t_max = my_ms
+    flops_all = flops_mine
+    if world > 1:
+        tt_ = torch.tensor([my_ms, flops_mine], dtype=torch.float64, device="cuda")
+        allv = [torch.zeros_like(tt_) for _ in range(world)]
+        dist.all_gather(allv, tt_)
+        t_max = max(float(x[0]) for x in allv)
+        flops_all = sum(float(x[1]) for x in allv)
+
+    # ---- e2e: host buffers through the same public API, H2D + D2H inside the timed region ----
+    e2e = None
+    if host_copy:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e_ms = 0.0
+        for s in range(max(2, min(args.steps, 5))):
+            flush_l2(flush)
+            a, b = torch.cuda.Event(True), torch.cuda.Event(True)
+            a.record()
+            do_step(h2d=True)
+            b.record()
+            torch.cuda.synchronize()
+            e_ms += a.elapsed_time(b)
+            n_e = s + 1
+        e_ms /= n_e
+        e_max = e_ms
+        if world > 1:
+            te = torch.tensor([e_ms], dtype=torch.float64, device="cuda")
+            allv = [torch.zeros_like(te) for _ in range(world)]
+            dist.all_gather(allv, te)
+            e_max = max(float(x[0]) for x in allv)
+        e2e = {"value": round(flops_all / args.steps / (e_max * 1e-3) / 1e12, 3), "unit": "TFLOP/s",
+               "ms_per_step": round(e_max, 4), "h2d_bytes_per_step": int(sum(j.h2d_bytes() for j in jobs)),
+               "d2h_bytes_per_step": 8 * 5 * len(jobs)}
+
+    peaks = load_peaks()
+    value = flops_all / (t_max * 1e-3) / 1e12
+    out = None
+    if rank == 0:
+        j0 = jobs[0]
+        info = j0.info
+        result = {
+            "metric": METRIC, "value": round(value, 3), "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(t_max / args.steps, 4), "higher_is_better": True,
+            "scaling": "weak" if args.config != "batch64k" else "strong",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded trees + N(0,1) tensors, random logits)",
+            "config": {"workload": args.config, "trees_per_rank": len(jobs), "n_tokens": int(info["n_tokens"]),
+                       "hq": cfg["hq"], "hkv": cfg["hkv"], "head_dim": cfg["d"], "vocab": VOCAB if with_loss else None,
+                       "ancestor_pairs": int(info["n_pairs"]), "linear_pairs": int(info["n_linear_pairs"]),
+                       "linear_tokens": int(info["n_linear_tokens"]),
+                       "pair_ratio": round(info["n_linear_pairs"] / info["n_pairs"], 4),
+                       "token_ratio": round(info["n_linear_tokens"] / info["n_tokens"], 4),
+                       "l2": "flushed between steps (256 MiB write, outside the step events)",
+                       "parallelism": f"dp{world} (independent trees per rank)", **extra_cfg},
+            "pct_peak": round(100.0 * value / peaks["bf16"], 2),
+            "gpu_launches": int(launches),
+            "clocks": clocks,
+        }
+        if per_op:
+            result["per_op_ms"] = {k: round(v, 4) for k, v in per_op.items()}
+            attn_ms = per_op["fwd"] + per_op["bwd"]
+            result["attn_fwd_bwd_tflops"] = round(j0.flops() / (attn_ms * 1e-3) / 1e12, 2)
+            bwd_fl = 10.0 * j0.d * j0.hq * info["n_pairs"]
+            ach = bwd_fl / (per_op["bwd"] * 1e-3) / 1e12
+            traffic = None
+            prof = os.path.join(ROOT, "profiles", "ncu_bwd_summary.json")
+            if os.path.exists(prof):
+                try:
+                    traffic = json.load(open(prof)).get(args.config, {}).get("dram_bytes_per_launch")
+                except Exception:
+                    traffic = None
+            result["roofline"] = {"bound": "tensor", "kernel": "tt_attn_bwd (bwd_pre + tree_attn_bwd_sm100 + dq_convert)",
+                                  "achieved": round(ach, 2), "peak": peaks["bf16"], "unit": "TFLOP/s",
+                                  "frac": round(ach / peaks["bf16"], 4), "traffic": traffic,
+                                  "peak_source": peaks["source"] + ", dense bf16 burst",
+                                  "frac_of_sustained": round(ach / peaks["bf16_sustained"], 4),
+                                  "algorithmic": "10 d Hq A FLOPs per launch (A = ancestor pairs)"}
+            if with_loss:
+                lb = info["n_tokens"] * (4 * VOCAB + 12)
+                result["loss_hbm"] = {"bound": "hbm", "achieved": round(lb / (per_op["loss"] * 1e-3) / 1e9, 1),
+                                      "peak": peaks["hbm"], "unit": "GB/s",
+                                      "frac": round(lb / (per_op["loss"] * 1e-3) / 1e9 / peaks["hbm"], 4)}
+        if e2e:
+            result["e2e"] = e2e
+        out = result
+    # ---- per-branch linear comparison (same kernels, untimed w.r.t. the step) ----
+    if rank == 0 and not args.no_linear and len(jobs) == 1:
+        tree_ms = per_op["fwd"] + per_op["bwd"]
+        lin_ms, lin_pairs, lin_tokens = linear_attention_time(jobs[0])
+        out["speedup_vs_linear"] = {"attn_fwd_bwd_tree_ms": round(tree_ms, 4), "attn_fwd_bwd_linear_ms": round(lin_ms, 4),
+                                    "speedup": round(lin_ms / tree_ms, 3),
+                                    "pair_ratio": out["config"]["pair_ratio"], "token_ratio": out["config"]["token_ratio"],
+                                    "frac_of_pair_ratio": round(lin_ms / tree_ms / out["config"]["pair_ratio"], 3),
+                                    "frac_of_token_ratio": round(lin_ms / tree_ms / out["config"]["token_ratio"], 3)}
+    if rank == 0 and world == 1 and not args.no_cpu:
+        dt, share, ntraj, cores = oracle_sample(jobs[0].tree, cfg, budget_s=args.cpu_budget)
+        full_s = dt / share
+        out["cpu_baseline"] = {"value": round(jobs[0].flops() / full_s / 1e12, 6), "unit": "TFLOP/s", "cores": cores,
+                               "kind": "oracle",
+                               "sample": f"fp64 oracle fwd+bwd, {cores} of {cfg['hq']} heads (one thread each), first {ntraj} trajectories "
+                                         f"({share * 100:.3f}% of the workload's per-branch pairs x heads), "
+                                         f"{dt:.1f} s measured, extrapolated linearly to the full tree",
+                               "extrapolated_full_step_s": round(full_s, 1)}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main_reference(args, rank, world, cfg):
+    """--impl reference: the fp64 CPU oracle (as it stands) on the same workload and metric."""
+    if rank != 0:
+        return
+    from workloads import trees as T
+    seed = 0 if args.seed is None else args.seed
+    tree = T.config_tree(args.config if args.config != "batch64k" else "batch64k", seed)
+    import paper_2511_00413_b200  # noqa: F401  (pack plan for the FLOP count; host-only)
+    from paper_2511_00413_b200 import tt_pack_plan
+    info = tt_pack_plan(tree.parent, tree.length)
+    flops = 14.0 * cfg["d"] * cfg["hq"] * info["n_pairs"]
+    budget = max(2.0, min(args.cpu_budget, 120.0 / max(1, args.steps + args.warmup)))
+    for _ in range(args.warmup):
+        oracle_sample(tree, cfg, budget_s=budget / 4)
+    ts = []
+    shares = []
+    for _ in range(args.steps):
+        dt, share, ntraj, cores = oracle_sample(tree, cfg, budget_s=budget)
+        ts.append(dt / share)
+        shares.append(share)
+    step_s = float(np.mean(ts))
+    value = flops / step_s / 1e12
+    out = {"impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": "TFLOP/s", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_s * 1e3, 1), "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": args.config, "hq": cfg["hq"], "hkv": cfg["hkv"], "head_dim": cfg["d"],
+                      "ancestor_pairs": int(info["n_pairs"])},
+           "cpu_baseline": {"value": round(value, 6), "unit": "TFLOP/s", "cores": cores, "kind": "oracle",
+                            "sample": f"per step: {cores} of {cfg['hq']} heads (one thread each) over the first trajectories "
+                                      f"(~{100 * float(np.mean(shares)):.3f}% of per-branch pairs x heads), "
+                                      f"extrapolated linearly"},
+           "e2e": {"value": round(value, 6), "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()
