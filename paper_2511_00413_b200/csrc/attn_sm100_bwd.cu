@@ -20,14 +20,19 @@
 //                dV += P^T dO      (A = P^T from TMEM)  (M=128, N=128, K=64)
 //                dK += dS^T Q      (A = dS^T from smem) (M=128, N=128, K=64)
 //                dQ^T = K^T dS^T   (A = K^T MN-major)   (M=128 (d), N=64, K=128)
-//              S^T / dP^T are double buffered so the next tile's products overlap this tile's
-//              element-wise work; dQ^T reuses the dP^T buffer once the softmax has read it.
-//   warps 2-5  element-wise: one thread per key row (TMEM lane); P^T, dS^T with the tree-scale,
-//              P^T -> TMEM (bf16), dS^T -> smem (bf16, SWIZZLE_128B); final dK/dV epilogue
-//   warps 6-9  dQ drain: one thread per head-dim lane of dQ^T; coalesced fp32 reductions into the
-//              fp32 dQ accumulator (128 contiguous bytes per warp instruction)
-// TMEM columns: dV 0-127 | dK 128-255 | S^T[2] 256-383 | dP^T[2] (or dQ^T) 384-511.
+//              Issue order per tile i: [softmax(i) done] dP(i+1), dV(i), dK(i), dQ(i), S(i+2):
+//              softmax(i+1) overlaps dV/dK/dQ(i); S^T is double buffered, dP^T and dQ^T single.
+//   warps 2-9  two warpgroups sharing the 4 TMEM lane quadrants; warpgroup wg owns query columns
+//              [32 wg, 32 wg + 32) of each tile.  Element-wise (one thread per key row): P^T, dS^T
+//              with the tree-scale, P^T -> TMEM (bf16), dS^T -> smem (bf16, SWIZZLE_128B).  Then the
+//              dQ drain of the previous tile (one thread per head-dim lane of dQ^T): transposed
+//              through an 8 KB smem stage per warpgroup and added into the fp32 dQ accumulator
+//              with TMA bulk tensor reductions (cp.reduce.async.bulk.tensor .add.f32).  Epilogue:
+//              warpgroup 0 writes dV, warpgroup 1 writes dK.
+// TMEM columns: dV 0-127 | dK 128-255 | S^T[2] 256-383 | dP^T 384-447 | dQ^T 448-511.
 #include <cudaTypedefs.h>
+
+#include <cstdlib>
 
 #include "sm100_ptx.cuh"
 #include "tt_internal.cuh"
@@ -55,18 +60,23 @@ constexpr uint32_t kNumBars = 1 + 2 * kQStages + 8 + 1;
 constexpr uint32_t kOffMisc = kOffBar + kNumBars * 8;
 constexpr uint32_t kSmemBytes = kOffMisc + 16 + 1024;
 
-constexpr uint32_t kColDV = 0, kColDK = 128, kColS = 256, kColP = 384;
+constexpr uint32_t kColDV = 0, kColDK = 128, kColS = 256, kColP = 384, kColQ = 448;
+
+// development instrumentation (TT_DEBUG_BWD & 8): per-role cycle counters summed over CTAs
+__device__ unsigned long long g_bwd_dbg[16];
 
 struct BwdParams {
   int64_t N;
   int hq, hkv, g, nb;
   int restore;
+  int dbg;  // development ablations (TT_DEBUG_BWD): 1 skip dQ reduce, 2 reuse Q/dO stage (no reload), 4 skip elementwise math
   float scale, scale_log2;
   const int32_t* E;
   const int32_t* kmaxE;
-  const int32_t* w;
-  const float* lse;
-  const float* Dvec;
+  int64_t Np;          // token dimension of the padded preprocess arrays (multiple of 128)
+  const float* L2p;    // [hq][Np] LSE in log2 units
+  const float* Dp;     // [hq][Np] D = dO . O
+  const float* wf;     // [Np] tree-scale (or 1) as fp32
   float* dq_acc;
   __nv_bfloat16* dk;
   __nv_bfloat16* dv;
@@ -101,12 +111,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   if (warp == 1) {
     if (lane == 0) {
       mbar_init(kv_full, 1);
-      for (int s = 0; s < kQStages; ++s) { mbar_init(&q_full[s], 33); mbar_init(&q_empty[s], 1); }
+      for (int s = 0; s < kQStages; ++s) { mbar_init(&q_full[s], 1); mbar_init(&q_empty[s], 1); }
       for (int b = 0; b < 2; ++b) {
         mbar_init(&s_full[b], 1);
-        mbar_init(&sm_done[b], 128);
+        mbar_init(&sm_done[b], 256);
         mbar_init(&dq_full[b], 1);
-        mbar_init(&dq_free[b], 128);
+        mbar_init(&dq_free[b], 256);
       }
       mbar_init(acc_done, 1);
       mbar_fence_init();
@@ -121,9 +131,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   const uint32_t tmem = misc[0];
 
   if (warp == 0) {
-    // ===================== producer warp =====================
-    // lane 0 issues the TMA tiles; all 32 lanes stage LSE (as log2), D and w for the 64 query rows
-    // with plain loads (the [hq, N] rows are not 16-byte aligned for ragged N) and arrive.
+    // ===================== producer (lane 0) =====================
     if (lane == 0) {
       tma_prefetch(&tmQ);
       tma_prefetch(&tmK);
@@ -135,134 +143,183 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         tma_load_3d(smem + kOffV + c * kKVChunk, &tmV, kv_full, c * 64, hk, (int)k0);
       }
     }
-    for (int it = 0; it < n_it; ++it) {
-      const int s = it % kQStages;
-      if (it >= kQStages) mbar_wait(&q_empty[s], ((it / kQStages) - 1) & 1);
-      const int h = hk * p.g + it / nq;
-      const int q0 = (qt0 + it % nq) * kBQ;
-      if (lane == 0) {
+    if (lane == 0) {
+      for (int it = 0; it < n_it; ++it) {
+        const int s = it % kQStages;
+        if (it >= kQStages) mbar_wait(&q_empty[s], ((it / kQStages) - 1) & 1);
+        const int h = hk * p.g + it / nq;
+        const int q0 = (qt0 + it % nq) * kBQ;
         uint8_t* qd = smem + kOffQS + s * 2 * kQTile;
-        mbar_expect_tx(&q_full[s], 2 * kQTile);
+        uint8_t* st = smem + kOffStats + s * 1024;
+        if ((p.dbg & 2) && it >= kQStages) {
+          mbar_arrive(&q_full[s]);
+          continue;
+        }
+        mbar_expect_tx(&q_full[s], 2 * kQTile + 3 * 256);
         for (int c = 0; c < 2; ++c) {
           tma_load_3d(qd + c * kQChunk, &tmQ, &q_full[s], c * 64, h, q0);
           tma_load_3d(qd + kQTile + c * kQChunk, &tmdO, &q_full[s], c * 64, h, q0);
         }
+        bulk_load_1d(st, p.L2p + (int64_t)h * p.Np + q0, 256, &q_full[s]);
+        bulk_load_1d(st + 256, p.Dp + (int64_t)h * p.Np + q0, 256, &q_full[s]);
+        bulk_load_1d(st + 512, p.wf + q0, 256, &q_full[s]);
       }
-      float* st = reinterpret_cast<float*>(smem + kOffStats + s * 1024);
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int c = lane + 32 * u;
-        const int64_t i = (int64_t)q0 + c;
-        const bool in = i < p.N;
-        st[c] = in ? p.lse[(int64_t)h * p.N + i] * kLog2e : 0.f;
-        st[64 + c] = in ? p.Dvec[(int64_t)h * p.N + i] : 0.f;
-        st[128 + c] = (in && p.restore) ? (float)p.w[i] : 1.f;
-      }
-      mbar_arrive(&q_full[s]);
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ===================== MMA issuer =====================
+    {
+      // ===================== MMA issuer (whole warp, one elected lane issues) =====================
       constexpr uint32_t idSP = idesc_bf16(128, kBQ, 0, 0);   // K/V (K-major) x Q/dO^T (K-major)
       constexpr uint32_t idVK = idesc_bf16(128, 128, 0, 1);   // P^T/dS^T (K-major) x dO/Q (MN-major)
       constexpr uint32_t idQ = idesc_bf16(128, kBQ, 1, 1);    // K^T (MN-major) x dS^T (MN-major)
-      const uint32_t kb_s = smem_u32(smem + kOffK), vb_s = smem_u32(smem + kOffV);
+      const uint32_t kb_s = warp_uniform(smem_u32(smem + kOffK)), vb_s = kb_s + kOffV;
+      const uint32_t tm = warp_uniform(tmem);
+      const uint32_t qs0 = kb_s + kOffQS, ds0 = kb_s + kOffDS;
       auto issue_SP = [&](int it) {
         const int s = it % kQStages, b = it & 1;
-        const uint32_t qb = smem_u32(smem + kOffQS + s * 2 * kQTile);
+        const uint32_t qb = qs0 + s * 2 * kQTile;
         const uint32_t ob = qb + kQTile;
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           const uint32_t offk = (kk >> 2) * kKVChunk + (kk & 3) * 32;
           const uint32_t offq = (kk >> 2) * kQChunk + (kk & 3) * 32;
-          mma_ss(tmem + kColS + 64 * b, sdesc(kb_s + offk, 16, 1024), sdesc(qb + offq, 16, 1024), idSP, kk > 0);
+          mma_ss_w(tm + kColS + 64 * b, sdesc(kb_s + offk, 16, 1024), sdesc(qb + offq, 16, 1024), idSP, kk > 0);
         }
         return ob;
       };
       auto issue_dP = [&](int it) {
-        const int s = it % kQStages, b = it & 1;
-        const uint32_t ob = smem_u32(smem + kOffQS + s * 2 * kQTile) + kQTile;
+        const int s = it % kQStages;
+        const uint32_t ob = qs0 + s * 2 * kQTile + kQTile;
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           const uint32_t offk = (kk >> 2) * kKVChunk + (kk & 3) * 32;
           const uint32_t offq = (kk >> 2) * kQChunk + (kk & 3) * 32;
-          mma_ss(tmem + kColP + 64 * b, sdesc(vb_s + offk, 16, 1024), sdesc(ob + offq, 16, 1024), idSP, kk > 0);
+          mma_ss_w(tm + kColP, sdesc(vb_s + offk, 16, 1024), sdesc(ob + offq, 16, 1024), idSP, kk > 0);
         }
       };
+      long long w_sm = 0, w_dq = 0, w_q = 0, t_start = clock64();
       mbar_wait(kv_full, 0);
-      for (int it = 0; it < n_it && it < 2; ++it) {
-        mbar_wait(&q_full[it % kQStages], (it / kQStages) & 1);
+      // prologue: S(0), dP(0) -> s_full[0]; S(1)
+      mbar_wait(&q_full[0], 0);
+      tc_fence_after();
+      issue_SP(0);
+      issue_dP(0);
+      mma_commit_w(&s_full[0]);
+      if (n_it > 1) {
+        mbar_wait(&q_full[1], 0);
         tc_fence_after();
-        issue_SP(it);
-        issue_dP(it);
-        mma_commit(&s_full[it & 1]);
+        issue_SP(1);
       }
       for (int it = 0; it < n_it; ++it) {
         const int s = it % kQStages, b = it & 1;
-        const uint32_t qb = smem_u32(smem + kOffQS + s * 2 * kQTile);
+        const uint32_t qb = qs0 + s * 2 * kQTile;
         const uint32_t ob = qb + kQTile;
-        const uint32_t dsb = smem_u32(smem + kOffDS + b * kDSTile);
-        mbar_wait(&sm_done[b], (it >> 1) & 1);
+        const uint32_t dsb = ds0 + b * kDSTile;
+        { long long t0 = clock64(); mbar_wait(&sm_done[b], (it >> 1) & 1); w_sm += clock64() - t0; }
         tc_fence_after();
+        // next tile's dP^T first (single buffer, free once softmax(it) has read it), so that
+        // softmax(it+1) overlaps this tile's dV / dK / dQ products
+        if (it + 1 < n_it) {
+          issue_dP(it + 1);
+          mma_commit_w(&s_full[(it + 1) & 1]);
+        }
         // dV += P^T dO   (A: P^T bf16 in TMEM over S^T[b]; B: dO MN-major, LBO = 8 KB d-chunk)
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
-          mma_ts(tmem + kColDV, tmem + kColS + 64 * b + kk * 8, sdesc(ob + kk * 2048, kQChunk, 1024), idVK,
+          mma_ts_w(tm + kColDV, tm + kColS + 64 * b + kk * 8, sdesc(ob + kk * 2048, kQChunk, 1024), idVK,
                  (it > 0 || kk > 0) ? 1u : 0u);
         // dK += dS^T Q   (A: dS^T K-major 128 x 64 in smem; B: Q MN-major)
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
-          mma_ss(tmem + kColDK, sdesc(dsb + kk * 32, 16, 1024), sdesc(qb + kk * 2048, kQChunk, 1024), idVK,
+          mma_ss_w(tm + kColDK, sdesc(dsb + kk * 32, 16, 1024), sdesc(qb + kk * 2048, kQChunk, 1024), idVK,
                  (it > 0 || kk > 0) ? 1u : 0u);
         // dQ^T = K^T dS^T   (A: K MN-major, LBO = 16 KB d-chunk; B: dS^T MN-major, one 64-wide group)
+        if (it > 0) {
+          { long long t0 = clock64(); mbar_wait(&dq_free[0], (it - 1) & 1); w_dq += clock64() - t0; }
+          tc_fence_after();
+        }
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)
-          mma_ss(tmem + kColP + 64 * b, sdesc(kb_s + kk * 2048, kKVChunk, 1024), sdesc(dsb + kk * 2048, kDSTile, 1024),
+          mma_ss_w(tm + kColQ, sdesc(kb_s + kk * 2048, kKVChunk, 1024), sdesc(dsb + kk * 2048, kDSTile, 1024),
                  idQ, kk > 0);
-        mma_commit(&dq_full[b]);
-        mma_commit(&q_empty[s]);
+        mma_commit_w(&dq_full[0]);
+        mma_commit_w(&q_empty[s]);
         if (it + 2 < n_it) {
-          mbar_wait(&q_full[(it + 2) % kQStages], ((it + 2) / kQStages) & 1);
+          { long long t0 = clock64(); mbar_wait(&q_full[(it + 2) % kQStages], ((it + 2) / kQStages) & 1); w_q += clock64() - t0; }
           tc_fence_after();
           issue_SP(it + 2);
-          mbar_wait(&dq_free[b], (it >> 1) & 1);
-          tc_fence_after();
-          issue_dP(it + 2);
-          mma_commit(&s_full[b]);
         }
       }
-      mma_commit(acc_done);
+      mma_commit_w(acc_done);
+      if ((p.dbg & 8) && lane == 0) {
+        atomicAdd(&g_bwd_dbg[0], (unsigned long long)(clock64() - t_start));
+        atomicAdd(&g_bwd_dbg[1], (unsigned long long)w_sm);
+        atomicAdd(&g_bwd_dbg[2], (unsigned long long)w_dq);
+        atomicAdd(&g_bwd_dbg[3], (unsigned long long)w_q);
+        atomicAdd(&g_bwd_dbg[4], (unsigned long long)n_it);
+      }
     }
-  } else if (warp < 6) {
-    // ===================== element-wise (one thread per key row) =====================
+  } else {
+    // ===================== compute warps 2-9 =====================
+    // Two warpgroups share every TMEM lane quadrant (lane quadrant = warp % 4): warpgroup wg owns
+    // query columns [32 wg, 32 wg + 32) of each 64-row tile for the element-wise work and the same
+    // 32 rows of dQ for the drain.  One thread = one key row (element-wise) = one head-dim lane (drain).
+    const int wg = (warp - 2) >> 2;
     const int q4 = warp & 3;
     const int r = q4 * 32 + lane;
-    const int64_t j = k0 + r;
+    const int j = (int)k0 + r;
+    const int Nn = (int)p.N;
     const uint32_t tl = tmem + ((uint32_t)(q4 * 32) << 16);
-    const int Ej = (j < p.N) ? p.E[j] : -1;
+    const int Ej = (j < Nn) ? p.E[j] : -1;
     const float sl2 = p.scale_log2;
+    long long c_ws = 0, c_el = 0, c_dr = 0, c_wd = 0;
+    const int64_t rs = (int64_t)p.hq * kD;
+    auto drain = [&](int it) {
+      const int h = hk * p.g + it / nq;
+      const int q0 = (qt0 + it % nq) * kBQ + 32 * wg;
+      { long long t0 = clock64(); mbar_wait(&dq_full[0], it & 1); c_wd += clock64() - t0; }
+      tc_fence_after();
+      uint32_t v[32];
+      tmem_ld32(tl + kColQ + 32 * wg, v);
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(&dq_free[0]);
+      if (p.dbg & 1) return;
+      // fire-and-forget fp32 reductions: for a fixed query row the 32 lanes of a warp cover 32
+      // consecutive head-dim elements (128 contiguous bytes per warp instruction)
+      float* ptr = p.dq_acc + ((int64_t)q0 * p.hq + h) * kD + r;
+      const int nrow = (int)imin64(32, p.N - q0);
+      if (nrow == 32) {
+#pragma unroll
+        for (int c = 0; c < 32; ++c) { atomicAdd(ptr, __uint_as_float(v[c]) * p.scale); ptr += rs; }
+      } else {
+#pragma unroll
+        for (int c = 0; c < 32; ++c) { if (c < nrow) atomicAdd(ptr, __uint_as_float(v[c]) * p.scale); ptr += rs; }
+      }
+    };
     for (int it = 0; it < n_it; ++it) {
       const int s = it % kQStages, b = it & 1;
       const int q0 = (qt0 + it % nq) * kBQ;
-      mbar_wait(&s_full[b], (it >> 1) & 1);
+      { long long t0 = clock64(); mbar_wait(&s_full[b], (it >> 1) & 1); c_ws += clock64() - t0; }
       tc_fence_after();
-      const float4* st_lse = reinterpret_cast<const float4*>(smem + kOffStats + s * 1024);
-      const float4* st_D = reinterpret_cast<const float4*>(smem + kOffStats + s * 1024 + 256);
-      const float4* st_w = reinterpret_cast<const float4*>(smem + kOffStats + s * 1024 + 512);
-      // rows of this key that need no mask: j <= q0 and q0 + 63 < min(E_j, N)
-      const bool nomask = __all_sync(0xffffffffu, (j <= q0) && ((int64_t)q0 + kBQ - 1 < (int64_t)Ej) &&
-                                                      ((int64_t)q0 + kBQ - 1 < p.N));
-      uint8_t* drow = smem + kOffDS + b * kDSTile + r * 128;
-#pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {  // two halves of 32 query columns (keeps registers < 168)
+      long long t_el = clock64();
+      if (p.dbg & 4) {
+        tc_fence_before();
+        mbar_arrive(&sm_done[b]);
+      } else {
+        const float4* st_lse = reinterpret_cast<const float4*>(smem + kOffStats + s * 1024);
+        const float4* st_D = reinterpret_cast<const float4*>(smem + kOffStats + s * 1024 + 256);
+        const float4* st_w = reinterpret_cast<const float4*>(smem + kOffStats + s * 1024 + 512);
+        // no mask needed for this key on these 32 columns: j <= first column, last column < min(E_j, N)
+        const int c0 = q0 + 32 * wg;
+        const bool nomask = __all_sync(0xffffffffu, (j <= c0) && (c0 + 31 < Ej) && (c0 + 31 < Nn));
         uint32_t sv[32], pv[32];
-        tmem_ld32(tl + kColS + 64 * b + 32 * hh, sv);
-        tmem_ld32(tl + kColP + 64 * b + 32 * hh, pv);
+        tmem_ld32(tl + kColS + 64 * b + 32 * wg, sv);
+        tmem_ld32(tl + kColP + 32 * wg, pv);
         tmem_wait_ld();
         uint32_t pwk[16], dsk[16];
 #pragma unroll
         for (int c4 = 0; c4 < 8; ++c4) {
-          const int cg = 8 * hh + c4;  // float4 group within the 64 columns
+          const int cg = 8 * wg + c4;  // float4 group within the 64 columns
           const float4 L = st_lse[cg];
           const float4 Dd = st_D[cg];
           const float4 W = st_w[cg];
@@ -273,10 +330,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             const int c = 4 * c4 + u;
-            const int64_t i = q0 + 32 * hh + c;
             float pr = ex2(fmaf(__uint_as_float(sv[c]), sl2, -Lv[u]));
             if (!nomask) {
-              const bool ok = (j <= i) && (i < (int64_t)Ej) && (i < p.N);
+              const int i = c0 + c;
+              const bool ok = (j <= i) && (i < Ej) && (i < Nn);
               pr = ok ? pr : 0.f;
             }
             pw[u] = Wv[u] * pr;
@@ -287,35 +344,46 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           dsk[2 * c4] = pack_bf16(ds[0], ds[1]);
           dsk[2 * c4 + 1] = pack_bf16(ds[2], ds[3]);
         }
-        // P^T (bf16) over S^T[b] in TMEM: columns [16 hh, 16 hh + 16)
-        tmem_st16(tl + kColS + 64 * b + 16 * hh, pwk);
-        // dS^T row r (128 B) into the SWIZZLE_128B smem tile: 16-byte chunk c at (c ^ (r & 7))
+        // P^T (bf16) over S^T[b] in TMEM: columns [16 wg, 16 wg + 16)
+        tmem_st16(tl + kColS + 64 * b + 16 * wg, pwk);
+        // dS^T row r into the SWIZZLE_128B smem tile: 16-byte chunk c at (c ^ (r & 7))
+        uint8_t* drow = smem + kOffDS + b * kDSTile + r * 128;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-          const int ch = 4 * hh + c;
+          const int ch = 4 * wg + c;
           *reinterpret_cast<uint4*>(drow + ((ch ^ (r & 7)) << 4)) =
               make_uint4(dsk[4 * c], dsk[4 * c + 1], dsk[4 * c + 2], dsk[4 * c + 3]);
         }
+        tmem_wait_st();
+        fence_proxy_async_smem();
+        tc_fence_before();
+        mbar_arrive(&sm_done[b]);
       }
-      tmem_wait_st();
-      fence_proxy_async_smem();
-      tc_fence_before();
-      mbar_arrive(&sm_done[b]);
+      c_el += clock64() - t_el;
+      long long t_dr = clock64();
+      if (it > 0) drain(it - 1);
+      c_dr += clock64() - t_dr;
     }
-    // ---- epilogue: dV, dK (scaled) rows of this key -> bf16 ----
+    drain(n_it - 1);
+    if ((p.dbg & 8) && r == 0 && wg == 0) {
+      atomicAdd(&g_bwd_dbg[5], (unsigned long long)c_ws);
+      atomicAdd(&g_bwd_dbg[6], (unsigned long long)c_el);
+      atomicAdd(&g_bwd_dbg[7], (unsigned long long)c_dr);
+      atomicAdd(&g_bwd_dbg[8], (unsigned long long)c_wd);
+    }
+    // ---- epilogue: warpgroup 0 writes dV, warpgroup 1 writes dK (scaled) for this key row ----
     mbar_wait(acc_done, 0);
     tc_fence_after();
-#pragma unroll 1
-    for (int which = 0; which < 2; ++which) {
-      const uint32_t col = which == 0 ? kColDV : kColDK;
-      const float mul = which == 0 ? 1.f : p.scale;
-      __nv_bfloat16* dst = (which == 0 ? p.dv : p.dk) + (j * p.hkv + hk) * kD;
+    {
+      const uint32_t col = wg == 0 ? kColDV : kColDK;
+      const float mul = wg == 0 ? 1.f : p.scale;
+      __nv_bfloat16* dst = (wg == 0 ? p.dv : p.dk) + ((int64_t)j * p.hkv + hk) * kD;
 #pragma unroll 1
       for (int cc = 0; cc < 4; ++cc) {
         uint32_t ov[32];
         tmem_ld32(tl + col + 32 * cc, ov);
         tmem_wait_ld();
-        if (j < p.N) {
+        if (j < Nn) {
           uint32_t pk[16];
 #pragma unroll
           for (int u = 0; u < 16; ++u)
@@ -324,38 +392,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 #pragma unroll
           for (int u = 0; u < 4; ++u) d4[u] = make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
         }
-      }
-    }
-  } else {
-    // ===================== dQ drain (one thread per head-dim lane of dQ^T) =====================
-    const int q4 = warp & 3;
-    const int dl = q4 * 32 + lane;
-    const uint32_t tl = tmem + ((uint32_t)(q4 * 32) << 16);
-    for (int it = 0; it < n_it; ++it) {
-      const int b = it & 1;
-      const int h = hk * p.g + it / nq;
-      const int q0 = (qt0 + it % nq) * kBQ;
-      mbar_wait(&dq_full[b], (it >> 1) & 1);
-      tc_fence_after();
-      uint32_t v0[32], v1[32];
-      tmem_ld32(tl + kColP + 64 * b, v0);
-      tmem_ld32(tl + kColP + 64 * b + 32, v1);
-      tmem_wait_ld();
-      tc_fence_before();
-      mbar_arrive(&dq_free[b]);
-      const int nrow = (int)imin64(kBQ, p.N - q0);
-      const int64_t rs = (int64_t)p.hq * kD;
-      float* ptr = p.dq_acc + ((int64_t)q0 * p.hq + h) * kD + dl;
-      if (nrow == kBQ) {
-#pragma unroll
-        for (int c = 0; c < 32; ++c) { atomicAdd(ptr, __uint_as_float(v0[c]) * p.scale); ptr += rs; }
-#pragma unroll
-        for (int c = 0; c < 32; ++c) { atomicAdd(ptr, __uint_as_float(v1[c]) * p.scale); ptr += rs; }
-      } else {
-#pragma unroll
-        for (int c = 0; c < 32; ++c) { if (c < nrow) atomicAdd(ptr, __uint_as_float(v0[c]) * p.scale); ptr += rs; }
-#pragma unroll
-        for (int c = 0; c < 32; ++c) { if (32 + c < nrow) atomicAdd(ptr, __uint_as_float(v1[c]) * p.scale); ptr += rs; }
       }
     }
   }
@@ -378,32 +414,61 @@ __global__ void __launch_bounds__(256) dq_convert_kernel(const float4* __restric
 
 }  // namespace
 
-tt_status sm100_attn_bwd(const tt_packed& pk, const void* q, const void* k, const void* v, const float* lse,
-                         const float* Dvec, const void* dout, int restore, int hq, int hkv, int d, float scale,
-                         float* dq_acc, void* dq, void* dk, void* dv, cudaStream_t st) {
+extern "C" int tt_debug_bwd_counters(unsigned long long* out, int reset) {
+  cudaMemcpyFromSymbol(out, g_bwd_dbg, sizeof(g_bwd_dbg));
+  if (reset) {
+    unsigned long long z[16] = {0};
+    cudaMemcpyToSymbol(g_bwd_dbg, z, sizeof(z));
+  }
+  return 0;
+}
+
+static inline size_t al256b(size_t x) { return (x + 255) & ~size_t(255); }
+
+size_t sm100_bwd_ws_bytes(int64_t N, int hq, int d) {
+  const int64_t Np = (N + 127) / 128 * 128;
+  return 2 * al256b((size_t)hq * Np * 4) + al256b((size_t)Np * 4) + al256b((size_t)N * hq * d * 4);
+}
+
+tt_status sm100_attn_bwd(const tt_packed& pk, const void* q, const void* k, const void* v, const void* o,
+                         const float* lse, const void* dout, int restore, int hq, int hkv, int d, float scale,
+                         void* ws, void* dq, void* dk, void* dv, cudaStream_t st) {
   if (d != kD) { set_error("sm100_attn_bwd: d must be 128"); return TT_ERR_UNSUPPORTED; }
+  const int64_t N = pk.n_tokens;
+  const int64_t Np = (N + 127) / 128 * 128;
+  char* w8 = static_cast<char*>(ws);
+  float* Dp = reinterpret_cast<float*>(w8);
+  float* L2p = reinterpret_cast<float*>(w8 + al256b((size_t)hq * Np * 4));
+  float* wf = reinterpret_cast<float*>(w8 + 2 * al256b((size_t)hq * Np * 4));
+  float* dq_acc = reinterpret_cast<float*>(w8 + 2 * al256b((size_t)hq * Np * 4) + al256b((size_t)Np * 4));
+  tt_status s = launch_bwd_pre_tc(o, dout, lse, pk.w, restore, N, Np, hq, Dp, L2p, wf, dq_acc, st);
+  if (s) return s;
   CUtensorMap mq, mk, mv, mdo;
-  tt_status s;
   const auto BF = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   const auto SW = CU_TENSOR_MAP_SWIZZLE_128B;
-  if ((s = make_tmap_thd(&mq, q, pk.n_tokens, hq, d, kBQ, BF, 2, SW, 64))) return s;
-  if ((s = make_tmap_thd(&mdo, dout, pk.n_tokens, hq, d, kBQ, BF, 2, SW, 64))) return s;
-  if ((s = make_tmap_thd(&mk, k, pk.n_tokens, hkv, d, 128, BF, 2, SW, 64))) return s;
-  if ((s = make_tmap_thd(&mv, v, pk.n_tokens, hkv, d, 128, BF, 2, SW, 64))) return s;
+  if ((s = make_tmap_thd(&mq, q, N, hq, d, kBQ, BF, 2, SW, 64))) return s;
+  if ((s = make_tmap_thd(&mdo, dout, N, hq, d, kBQ, BF, 2, SW, 64))) return s;
+  if ((s = make_tmap_thd(&mk, k, N, hkv, d, 128, BF, 2, SW, 64))) return s;
+  if ((s = make_tmap_thd(&mv, v, N, hkv, d, 128, BF, 2, SW, 64))) return s;
   BwdParams prm;
-  prm.N = pk.n_tokens;
+  prm.N = N;
   prm.hq = hq;
   prm.hkv = hkv;
   prm.g = hq / hkv;
   prm.nb = pk.n_blk;
   prm.restore = restore ? 1 : 0;
+  {
+    const char* e = getenv("TT_DEBUG_BWD");
+    prm.dbg = e ? atoi(e) : 0;
+  }
   prm.scale = scale;
   prm.scale_log2 = scale * kLog2e;
   prm.E = pk.E;
   prm.kmaxE = pk.kblk_maxE;
-  prm.w = pk.w;
-  prm.lse = lse;
-  prm.Dvec = Dvec;
+  prm.Np = Np;
+  prm.L2p = L2p;
+  prm.Dp = Dp;
+  prm.wf = wf;
   prm.dq_acc = dq_acc;
   prm.dk = static_cast<__nv_bfloat16*>(dk);
   prm.dv = static_cast<__nv_bfloat16*>(dv);
@@ -413,7 +478,7 @@ tt_status sm100_attn_bwd(const tt_packed& pk, const void* q, const void* k, cons
   tree_attn_bwd_sm100<<<grid, kBwdThreads, kSmemBytes, st>>>(mq, mk, mv, mdo, prm);
   count_launch();
   if ((s = check_launch("tree_attn_bwd_sm100"))) return s;
-  const int64_t n4 = pk.n_tokens * hq * d / 4;
+  const int64_t n4 = N * hq * d / 4;
   dq_convert_kernel<<<(unsigned)std::min<int64_t>((n4 + 255) / 256, 148 * 16), 256, 0, st>>>(
       reinterpret_cast<const float4*>(dq_acc), reinterpret_cast<uint2*>(dq), n4);
   count_launch();

@@ -49,6 +49,44 @@ __global__ void __launch_bounds__(256) bwd_pre_kernel(const T* __restrict__ o, c
   }
 }
 
+// Tensor-core backward preprocess: per (token, head) D_i = dO_i . O_i, LSE_i in log2 units, and
+// per token the tree-scale as fp32 (w_i, or 1 without restoration), all laid out with the token
+// dimension padded to Np (a multiple of 128) so the kernel can bulk-copy 64-row slices; padded rows
+// get D = 0, LSE = 0, w = 0.  Also zeroes the fp32 dQ accumulator.
+__global__ void __launch_bounds__(256) bwd_pre_tc_kernel(const __nv_bfloat16* __restrict__ o,
+                                                         const __nv_bfloat16* __restrict__ dout,
+                                                         const float* __restrict__ lse, const int32_t* __restrict__ w,
+                                                         int restore, int64_t N, int64_t Np, int hq,
+                                                         float* __restrict__ Dp, float* __restrict__ L2p,
+                                                         float* __restrict__ wf, float* __restrict__ dq_acc) {
+  const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);  // row = i * hq + h over padded i
+  const int lane = threadIdx.x & 31;
+  if (row >= Np * hq) return;
+  const int64_t i = row / hq;
+  const int h = (int)(row % hq);
+  float s = 0.f;
+  if (i < N) {
+    const uint2 va = reinterpret_cast<const uint2*>(o + row * 128)[lane];
+    const uint2 vb = reinterpret_cast<const uint2*>(dout + row * 128)[lane];
+    const __nv_bfloat162* pa = reinterpret_cast<const __nv_bfloat162*>(&va);
+    const __nv_bfloat162* pb = reinterpret_cast<const __nv_bfloat162*>(&vb);
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      float2 fa = __bfloat1622float2(pa[t]), fb = __bfloat1622float2(pb[t]);
+      s = fmaf(fa.x, fb.x, s);
+      s = fmaf(fa.y, fb.y, s);
+    }
+    float4* z = reinterpret_cast<float4*>(dq_acc + row * 128);
+    z[lane] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  if (lane == 0) {
+    Dp[(int64_t)h * Np + i] = s;
+    L2p[(int64_t)h * Np + i] = i < N ? lse[(int64_t)h * N + i] * kLog2e : 0.f;
+    if (h == 0) wf[i] = i < N ? (restore ? (float)w[i] : 1.f) : 0.f;
+  }
+}
+
 // fp64 sum of squares: kSqnormBlocks fixed contiguous partitions, fixed-order tree reductions.
 template <typename T>
 __global__ void __launch_bounds__(256) sqnorm_partial_kernel(const T* __restrict__ x, int64_t n, double* __restrict__ part) {
@@ -96,6 +134,16 @@ tt_status launch_bwd_pre(const void* o, const void* dout, tt_dtype dt, int64_t N
     bwd_pre_kernel<float><<<blocks, 256, 0, st>>>((const float*)o, (const float*)dout, N, hq, d, Dvec, dq_acc);
   count_launch();
   return check_launch("bwd_pre_kernel");
+}
+
+tt_status launch_bwd_pre_tc(const void* o, const void* dout, const float* lse, const int32_t* w, int restore,
+                            int64_t N, int64_t Np, int hq, float* Dp, float* L2p, float* wf, float* dq_acc,
+                            cudaStream_t st) {
+  const int64_t rows = Np * hq;
+  bwd_pre_tc_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>((const __nv_bfloat16*)o, (const __nv_bfloat16*)dout,
+                                                               lse, w, restore, N, Np, hq, Dp, L2p, wf, dq_acc);
+  count_launch();
+  return check_launch("bwd_pre_tc_kernel");
 }
 
 tt_status launch_sqnorm(const void* x, int64_t n, tt_dtype dt, double* out, double* partials, cudaStream_t st) {

@@ -330,9 +330,8 @@ tt_status tt_attn_fwd(const tt_packed* pk, const void* q, const void* k, const v
 }
 
 static size_t bwd_ws_bytes(const tt_packed* pk, int hq, int d, tt_dtype dt) {
-  size_t D = al256((size_t)pk->n_tokens * hq * 4);
-  size_t acc = (dt == TT_BF16 && d == 128) ? al256((size_t)pk->n_tokens * hq * d * 4) : 0;
-  return D + acc;
+  if (dt == TT_BF16 && d == 128) return sm100_bwd_ws_bytes(pk->n_tokens, hq, d);
+  return al256((size_t)pk->n_tokens * hq * 4);
 }
 
 tt_status tt_attn_bwd_workspace(const tt_packed* pk, int32_t hq, int32_t hkv, int32_t d, tt_dtype dt, size_t* bytes) {
@@ -360,15 +359,13 @@ tt_status tt_attn_bwd(const tt_packed* pk, const void* q, const void* k, const v
   size_t need = bwd_ws_bytes(pk, hq, d, dt);
   if (ws_bytes < need) { set_error("tt_attn_bwd: workspace %zu < %zu", ws_bytes, need); return TT_ERR_WORKSPACE; }
   cudaStream_t st = as_cuda(stream);
-  float* Dvec = static_cast<float*>(d_ws);
-  bool tc = (dt == TT_BF16 && d == 128);
-  float* dq_acc = tc ? reinterpret_cast<float*>(static_cast<char*>(d_ws) + al256((size_t)pk->n_tokens * hq * 4)) : nullptr;
-  s = launch_bwd_pre(o, dout, dt, pk->n_tokens, hq, d, Dvec, dq_acc, st);
-  if (s) return s;
-  if (tc) {
+  if (dt == TT_BF16 && d == 128) {
     if (!sm100_available()) { set_error("tt_attn_bwd: bf16 d=128 needs an sm_100a device"); return TT_ERR_UNSUPPORTED; }
-    return sm100_attn_bwd(*pk, q, k, v, lse, Dvec, dout, restore, hq, hkv, d, softmax_scale, dq_acc, dq, dk, dv, st);
+    return sm100_attn_bwd(*pk, q, k, v, o, lse, dout, restore, hq, hkv, d, softmax_scale, d_ws, dq, dk, dv, st);
   }
+  float* Dvec = static_cast<float*>(d_ws);
+  s = launch_bwd_pre(o, dout, dt, pk->n_tokens, hq, d, Dvec, nullptr, st);
+  if (s) return s;
   return simt_attn_bwd(*pk, q, k, v, lse, Dvec, dout, restore, dt, hq, hkv, d, softmax_scale, dq, dk, dv, st);
 }
 

@@ -52,6 +52,9 @@ tt_status simt_attn_fwd(const tt_packed& pk, const void* q, const void* k, const
 tt_status simt_attn_bwd(const tt_packed& pk, const void* q, const void* k, const void* v, const float* lse,
                         const float* Dvec, const void* dout, int restore, tt_dtype dt, int hq, int hkv, int d,
                         float scale, void* dq, void* dk, void* dv, cudaStream_t st);
+tt_status launch_bwd_pre_tc(const void* o, const void* dout, const float* lse, const int32_t* w, int restore,
+                            int64_t N, int64_t Np, int hq, float* Dp, float* L2p, float* wf, float* dq_acc,
+                            cudaStream_t st);
 tt_status launch_bwd_pre(const void* o, const void* dout, tt_dtype dt, int64_t N, int hq, int d, float* Dvec,
                          float* dq_acc, cudaStream_t st);
 
@@ -60,9 +63,11 @@ tt_status make_tmap_thd(CUtensorMap* m, const void* ptr, int64_t rows, int heads
                         CUtensorMapDataType dt, int elem_bytes, CUtensorMapSwizzle sw, int box_inner);
 tt_status sm100_attn_fwd(const tt_packed& pk, const void* q, const void* k, const void* v, int hq, int hkv,
                          int d, float scale, void* o, float* lse, cudaStream_t st);
-tt_status sm100_attn_bwd(const tt_packed& pk, const void* q, const void* k, const void* v, const float* lse,
-                         const float* Dvec, const void* dout, int restore, int hq, int hkv, int d, float scale,
-                         float* dq_acc, void* dq, void* dk, void* dv, cudaStream_t st);
+// ws: the tensor-core backward workspace (tt_attn_bwd_workspace bytes); see sm100_bwd_ws_bytes
+size_t sm100_bwd_ws_bytes(int64_t N, int hq, int d);
+tt_status sm100_attn_bwd(const tt_packed& pk, const void* q, const void* k, const void* v, const void* o,
+                         const float* lse, const void* dout, int restore, int hq, int hkv, int d, float scale,
+                         void* ws, void* dq, void* dk, void* dv, cudaStream_t st);
 
 tt_status launch_loss(const tt_packed& pk, const __nv_bfloat16* logits, int64_t ld, int vocab, const int32_t* tok,
                       const uint8_t* node_mask, int boundary_mode, float gamma, __nv_bfloat16* dlogits,
