@@ -87,7 +87,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                         const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
                         const BwdParams p) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned base; pointer arithmetic on smem_raw keeps the shared address space visible to
+  // the compiler (LDS/STS instead of generic LD/ST)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBar);
   uint64_t* kv_full = bars;
   uint64_t* q_full = bars + 1;
@@ -224,9 +226,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         }
         // dV += P^T dO   (A: P^T bf16 in TMEM over S^T[b]; B: dO MN-major, LBO = 8 KB d-chunk)
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-          mma_ts_w(tm + kColDV, tm + kColS + 64 * b + kk * 8, sdesc(ob + kk * 2048, kQChunk, 1024), idVK,
-                 (it > 0 || kk > 0) ? 1u : 0u);
+        for (int kk = 0; kk < 4; ++kk)  // P^T of query columns 16 kk.. lives at S^T[b] + 32 (kk / 2) + 8 (kk % 2)
+          mma_ts_w(tm + kColDV, tm + kColS + 64 * b + 32 * (kk >> 1) + 8 * (kk & 1), sdesc(ob + kk * 2048, kQChunk, 1024),
+                   idVK, (it > 0 || kk > 0) ? 1u : 0u);
         // dK += dS^T Q   (A: dS^T K-major 128 x 64 in smem; B: Q MN-major)
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
@@ -271,8 +273,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const uint32_t tl = tmem + ((uint32_t)(q4 * 32) << 16);
     const int Ej = (j < Nn) ? p.E[j] : -1;
     const float sl2 = p.scale_log2;
-    long long c_ws = 0, c_el = 0, c_dr = 0, c_wd = 0;
-    const int64_t rs = (int64_t)p.hq * kD;
+    long long c_ws = 0, c_el = 0, c_dr = 0, c_wd = 0, c_ld = 0, c_math = 0, c_st = 0;
     auto drain = [&](int it) {
       const int h = hk * p.g + it / nq;
       const int q0 = (qt0 + it % nq) * kBQ + 32 * wg;
@@ -286,6 +287,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       if (p.dbg & 1) return;
       // fire-and-forget fp32 reductions: for a fixed query row the 32 lanes of a warp cover 32
       // consecutive head-dim elements (128 contiguous bytes per warp instruction)
+      const int64_t rs = (int64_t)p.hq * kD;
       float* ptr = p.dq_acc + ((int64_t)q0 * p.hq + h) * kD + r;
       const int nrow = (int)imin64(32, p.N - q0);
       if (nrow == 32) {
@@ -311,11 +313,16 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const float4* st_w = reinterpret_cast<const float4*>(smem + kOffStats + s * 1024 + 512);
         // no mask needed for this key on these 32 columns: j <= first column, last column < min(E_j, N)
         const int c0 = q0 + 32 * wg;
-        const bool nomask = __all_sync(0xffffffffu, (j <= c0) && (c0 + 31 < Ej) && (c0 + 31 < Nn));
+        // allowed query columns of this key form one interval: [max(j, c0), min(E_j, N)) - c0
+        const int lo = max(j - c0, 0), hi = min(min(Ej, Nn) - c0, 32);
+        const uint32_t cmask = (hi <= lo) ? 0u : ((hi >= 32 ? 0xffffffffu : ((1u << hi) - 1u)) & ~((1u << lo) - 1u));
         uint32_t sv[32], pv[32];
+        long long tA = clock64();
         tmem_ld32(tl + kColS + 64 * b + 32 * wg, sv);
         tmem_ld32(tl + kColP + 32 * wg, pv);
         tmem_wait_ld();
+        c_ld += clock64() - tA;
+        tA = clock64();
         uint32_t pwk[16], dsk[16];
 #pragma unroll
         for (int c4 = 0; c4 < 8; ++c4) {
@@ -331,11 +338,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           for (int u = 0; u < 4; ++u) {
             const int c = 4 * c4 + u;
             float pr = ex2(fmaf(__uint_as_float(sv[c]), sl2, -Lv[u]));
-            if (!nomask) {
-              const int i = c0 + c;
-              const bool ok = (j <= i) && (i < Ej) && (i < Nn);
-              pr = ok ? pr : 0.f;
-            }
+            pr = ((cmask >> c) & 1u) ? pr : 0.f;
             pw[u] = Wv[u] * pr;
             ds[u] = pw[u] * (__uint_as_float(pv[c]) - Dv[u]);
           }
@@ -344,8 +347,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           dsk[2 * c4] = pack_bf16(ds[0], ds[1]);
           dsk[2 * c4 + 1] = pack_bf16(ds[2], ds[3]);
         }
-        // P^T (bf16) over S^T[b] in TMEM: columns [16 wg, 16 wg + 16)
-        tmem_st16(tl + kColS + 64 * b + 16 * wg, pwk);
+        c_math += clock64() - tA;
+        tA = clock64();
+        // P^T (bf16) over this warpgroup's own S^T[b] columns: [32 wg, 32 wg + 16) — never over
+        // columns the other warpgroup may still be reading
+        tmem_st16(tl + kColS + 64 * b + 32 * wg, pwk);
         // dS^T row r into the SWIZZLE_128B smem tile: 16-byte chunk c at (c ^ (r & 7))
         uint8_t* drow = smem + kOffDS + b * kDSTile + r * 128;
 #pragma unroll
@@ -358,6 +364,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         fence_proxy_async_smem();
         tc_fence_before();
         mbar_arrive(&sm_done[b]);
+        c_st += clock64() - tA;
       }
       c_el += clock64() - t_el;
       long long t_dr = clock64();
@@ -370,6 +377,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       atomicAdd(&g_bwd_dbg[6], (unsigned long long)c_el);
       atomicAdd(&g_bwd_dbg[7], (unsigned long long)c_dr);
       atomicAdd(&g_bwd_dbg[8], (unsigned long long)c_wd);
+      atomicAdd(&g_bwd_dbg[9], (unsigned long long)c_ld);
+      atomicAdd(&g_bwd_dbg[10], (unsigned long long)c_math);
+      atomicAdd(&g_bwd_dbg[11], (unsigned long long)c_st);
     }
     // ---- epilogue: warpgroup 0 writes dV, warpgroup 1 writes dK (scaled) for this key row ----
     mbar_wait(acc_done, 0);

@@ -172,3 +172,23 @@ def test_unsupported_shapes_fail_loudly(tt):
     k = torch.zeros(64, 2, 128, dtype=torch.bfloat16, device="cuda")
     with pytest.raises(tt.TTError):
         tt.tt_attn_fwd(pk, q, k, k)
+
+
+def test_bwd_dk_dv_bitwise_deterministic(tt):
+    """dK/dV accumulate in TMEM in a fixed order: repeated runs must be bitwise identical
+    (guards the warpgroup hand-off of P^T / dS^T inside the backward kernel)."""
+    import torch
+    t = trees.gen_agentic(3000, root_len=600, seed=7)
+    pk = tt.tt_pack(t.parent, t.length)
+    N = pk.n_tokens
+    q, k, v = (x.cuda() for x in tensors.qkv_tensors(N, 4, 2, 128, "bf16", seed=3))
+    G = tensors.grad_tensor(N, 4, 128, "bf16", seed=4).cuda()
+    o, lse = tt.tt_attn_fwd(pk, q, k, v)
+    ref = [x.clone() for x in tt.tt_attn_bwd(pk, q, k, v, o, lse, G)]
+    for _ in range(10):
+        o2, lse2 = tt.tt_attn_fwd(pk, q, k, v)
+        assert torch.equal(o2, o) and torch.equal(lse2, lse)
+        d = tt.tt_attn_bwd(pk, q, k, v, o, lse, G)
+        assert torch.equal(d[1], ref[1]) and torch.equal(d[2], ref[2])
+        # dQ accumulates with fp32 reductions: order-dependent rounding only
+        assert (d[0].float() - ref[0].float()).abs().max().item() <= 2e-2

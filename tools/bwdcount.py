@@ -16,5 +16,5 @@ for cfg, seed in [("agentic8k", 0), ("deep32k", 1)]:
     tt.tt_attn_bwd(pk, q, k, v, o, lse, G); torch.cuda.synchronize()
     L.tt_debug_bwd_counters(buf, 1)
     b = list(buf); nit = b[4]
-    print(cfg, "iters", nit, "per-iter cycles: mma_total %.0f  wait_sm %.0f  wait_dqfree %.0f  wait_q %.0f | compute(wg0,r0): wait_s %.0f  elem %.0f  drain %.0f (wait dqfull %.0f)" %
-          tuple(x / nit for x in [b[0], b[1], b[2], b[3], b[5], b[6], b[7], b[8]]), flush=True)
+    print(cfg, "iters", nit, "per-iter cycles: mma_total %.0f  wait_sm %.0f  wait_dqfree %.0f  wait_q %.0f | compute(wg0,r0): wait_s %.0f  elem %.0f [ld %.0f math %.0f st %.0f] drain %.0f (wait dqfull %.0f)" %
+          tuple(x / nit for x in [b[0], b[1], b[2], b[3], b[5], b[6], b[9], b[10], b[11], b[7], b[8]]), flush=True)
