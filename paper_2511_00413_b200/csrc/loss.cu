@@ -9,9 +9,10 @@
 //   dlogits_t = gamma (Omega_t softmax(x_t) - sum_k omega_k e_{y_k})
 // Targets (R7): t+1 inside a node; at a node's last token every continuation (succ list).
 //
-// Memory plan per row (V = 151,936 bf16 = 297 KB):  pass 1 streams the row from HBM (16-byte
-// vector loads, online max / sum-exp in the log2 domain), pass 2 re-reads it — it is still in
-// the 126 MB L2 because ~600 rows are in flight — and writes dlogits (may alias logits).  HBM
+// Memory plan per row (V = 151,936 bf16 = 297 KB):  pass 1 streams the row from HBM with 32-byte
+// vector loads marked L2::evict_last (online max / sum-exp in the log2 domain, one max pass and
+// at most one rescale per vector); pass 2 re-reads it from L2 (2 CTAs/SM keep ~300 rows = ~90 MB
+// in flight, under the 126 MB L2) marked evict_first, and writes dlogits (may alias logits).  HBM
 // traffic is therefore ~4 V bytes / row.  Rows with no target (Omega_t = 0, e.g.
 // the last token of every trajectory) skip both reads and only write zeros.
 #include <algorithm>
@@ -24,56 +25,88 @@ namespace {
 constexpr int kLossThreads = 512;
 constexpr int kMaxTargets = 1024;
 
-struct Vec8 { float v[8]; };
+// W bf16 logits per thread-vector: 16 (32-byte .v8.b32 accesses; needs 32-byte aligned rows) or 8.
+template <int W> struct Vec { uint32_t u[W / 2]; };
 
-__device__ __forceinline__ Vec8 load8(const __nv_bfloat16* p) {
-  uint4 u;
-  asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(u.x), "=r"(u.y), "=r"(u.z), "=r"(u.w) : "l"(p));
-  Vec8 r;
-  const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&u);
-#pragma unroll
-  for (int t = 0; t < 4; ++t) {
-    float2 f = __bfloat1622float2(b[t]);
-    r.v[2 * t] = f.x;
-    r.v[2 * t + 1] = f.y;
-  }
+// pass 1: streaming read that asks L2 to keep the line (it is re-read by pass 2)
+template <int W> __device__ __forceinline__ Vec<W> ld_keep(const __nv_bfloat16* p) {
+  Vec<W> r;
+  if constexpr (W == 16)
+    asm volatile("ld.global.nc.L1::no_allocate.L2::evict_last.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r.u[0]), "=r"(r.u[1]), "=r"(r.u[2]), "=r"(r.u[3]), "=r"(r.u[4]), "=r"(r.u[5]), "=r"(r.u[6]),
+                   "=r"(r.u[7])
+                 : "l"(p));
+  else
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.u[0]), "=r"(r.u[1]), "=r"(r.u[2]), "=r"(r.u[3])
+                 : "l"(p));
   return r;
 }
-
-// plain (coherent) load for pass 2: dlogits may alias logits, so the row must not come from the
-// non-coherent path after another thread of this CTA wrote it (it never does: each thread
-// reads then writes only its own chunks), but keep the coherent path to be safe.
-__device__ __forceinline__ Vec8 load8_coherent(const __nv_bfloat16* p) {
-  uint4 u = *reinterpret_cast<const uint4*>(p);
-  Vec8 r;
-  const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&u);
-#pragma unroll
-  for (int t = 0; t < 4; ++t) {
-    float2 f = __bfloat1622float2(b[t]);
-    r.v[2 * t] = f.x;
-    r.v[2 * t + 1] = f.y;
-  }
+// pass 2: coherent read (dlogits may alias logits: each thread reads, then overwrites, its own
+// vectors), last use of the line
+template <int W> __device__ __forceinline__ Vec<W> ld_last(const __nv_bfloat16* p) {
+  Vec<W> r;
+  if constexpr (W == 16)
+    asm volatile("ld.global.L1::no_allocate.L2::evict_first.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r.u[0]), "=r"(r.u[1]), "=r"(r.u[2]), "=r"(r.u[3]), "=r"(r.u[4]), "=r"(r.u[5]), "=r"(r.u[6]),
+                   "=r"(r.u[7])
+                 : "l"(p)
+                 : "memory");
+  else
+    asm volatile("ld.global.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.u[0]), "=r"(r.u[1]), "=r"(r.u[2]), "=r"(r.u[3])
+                 : "l"(p)
+                 : "memory");
   return r;
 }
-
-__device__ __forceinline__ void store8(__nv_bfloat16* p, const float* f) {
-  uint4 u;
-  __nv_bfloat162* b = reinterpret_cast<__nv_bfloat162*>(&u);
+template <int W> __device__ __forceinline__ void st_vec(__nv_bfloat16* p, const Vec<W>& r) {
+  if constexpr (W == 16)
+    asm volatile("st.global.L1::no_allocate.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(r.u[0]), "r"(r.u[1]),
+                 "r"(r.u[2]), "r"(r.u[3]), "r"(r.u[4]), "r"(r.u[5]), "r"(r.u[6]), "r"(r.u[7])
+                 : "memory");
+  else
+    asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(r.u[0]), "r"(r.u[1]),
+                 "r"(r.u[2]), "r"(r.u[3])
+                 : "memory");
+}
+__device__ __forceinline__ float2 bf2f(uint32_t u) {
+  return __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u));
+}
+__device__ __forceinline__ uint32_t f2bf(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+__device__ __forceinline__ float ex2f(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// (m, s) <- (m, s) (+) one vector of logits, log2 domain: one max pass, at most one rescale
+template <int W> __device__ __forceinline__ void accum(float& m, float& s, const Vec<W>& r) {
+  float x[W];
 #pragma unroll
-  for (int t = 0; t < 4; ++t) b[t] = __floats2bfloat162_rn(f[2 * t], f[2 * t + 1]);
-  *reinterpret_cast<uint4*>(p) = u;
-}
-
-__device__ __forceinline__ void online_add(float& m, float& s, float x2) {
-  // x2 in log2 units
-  if (x2 > m) {
-    s = s * exp2f(m - x2) + 1.f;
-    m = x2;
-  } else {
-    s += exp2f(x2 - m);
+  for (int t = 0; t < W / 2; ++t) {
+    const float2 f = bf2f(r.u[t]);
+    x[2 * t] = f.x * kLog2e;
+    x[2 * t + 1] = f.y * kLog2e;
   }
+  float cm = x[0];
+#pragma unroll
+  for (int t = 1; t < W; ++t) cm = fmaxf(cm, x[t]);
+  if (cm > m) {
+    s *= ex2f(m - cm);  // m = -inf -> 0
+    m = cm;
+  }
+  float a = 0.f, b = 0.f;
+#pragma unroll
+  for (int t = 0; t < W; t += 2) {
+    a += ex2f(x[t] - m);
+    b += ex2f(x[t + 1] - m);
+  }
+  s += a + b;
 }
 
+template <int W>
 __global__ void __launch_bounds__(kLossThreads) loss_kernel(
     int64_t N, const __nv_bfloat16* logits, int64_t ld, int V, const int32_t* __restrict__ tok,
     const uint8_t* __restrict__ node_mask, int boundary_mode, float gamma, const int32_t* __restrict__ w,
@@ -87,8 +120,8 @@ __global__ void __launch_bounds__(kLossThreads) loss_kernel(
   __shared__ float s_red[2][kLossThreads / 32];
   __shared__ float s_lse;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int V8 = V & ~7;
-  const float L2E = kLog2e;
+  const int VW = V - V % W;  // vectorised prefix
+  constexpr int STEP = kLossThreads * W;
 
   for (int64_t row = blockIdx.x; row < N; row += gridDim.x) {
     // ---- targets of this row (R7, R17, boundary mode) ----
@@ -112,7 +145,7 @@ __global__ void __launch_bounds__(kLossThreads) loss_kernel(
     }
     __syncthreads();
     const int nt = s_nt;
-    // packed target index -> (token id, weight)
+    // packed target index -> (token id, weight = tree-scale of the target)
     float om_part = 0.f;
     bool bad = false;
     for (int k = tid; k < nt; k += kLossThreads) {
@@ -126,7 +159,6 @@ __global__ void __launch_bounds__(kLossThreads) loss_kernel(
     }
     const __nv_bfloat16* x = logits + row * ld;
     __nv_bfloat16* dx = dlogits + row * ld;
-    // block sum of Omega (fixed order)
     for (int o = 16; o > 0; o >>= 1) om_part += __shfl_xor_sync(0xffffffffu, om_part, o);
     const int bad_any = __syncthreads_or(bad);
     if (lane == 0) s_red[0][warp] = om_part;
@@ -135,10 +167,12 @@ __global__ void __launch_bounds__(kLossThreads) loss_kernel(
     for (int k = 0; k < kLossThreads / 32; ++k) Omega += s_red[0][k];
     __syncthreads();  // s_red is reused below
     if (Omega == 0.f || bad_any) {
-      // no prediction from this row (or invalid target id): zero gradient
-      const float z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-      for (int c = tid * 8; c < V8; c += kLossThreads * 8) store8(dx + c, z);
-      for (int c = V8 + tid; c < V; c += kLossThreads) dx[c] = __float2bfloat16_rn(0.f);
+      // no prediction from this row (or an invalid target id): zero gradient, no logits read
+      Vec<W> z;
+#pragma unroll
+      for (int t = 0; t < W / 2; ++t) z.u[t] = 0u;
+      for (int c = tid * W; c < VW; c += STEP) st_vec<W>(dx + c, z);
+      for (int c = VW + tid; c < V; c += kLossThreads) dx[c] = __float2bfloat16_rn(0.f);
       if (tid == 0) {
         const float lv = bad_any ? __int_as_float(0x7fc00000) : 0.f;
         if (bad_any && d_err) atomicExch(d_err, 1);
@@ -149,42 +183,34 @@ __global__ void __launch_bounds__(kLossThreads) loss_kernel(
       __syncthreads();
       continue;
     }
-    // ---- pass 1: online max / sum-exp (log2 domain), 4 vectors in flight per thread ----
-    float m = -INFINITY, s = 0.f;
-    int c = tid * 8;
-    for (; c + 3 * kLossThreads * 8 < V8; c += 4 * kLossThreads * 8) {
-      Vec8 a = load8(x + c), b = load8(x + c + kLossThreads * 8), d = load8(x + c + 2 * kLossThreads * 8),
-           e = load8(x + c + 3 * kLossThreads * 8);
-#pragma unroll
-      for (int t = 0; t < 8; ++t) {
-        online_add(m, s, a.v[t] * L2E);
-        online_add(m, s, b.v[t] * L2E);
-        online_add(m, s, d.v[t] * L2E);
-        online_add(m, s, e.v[t] * L2E);
-      }
+    // ---- pass 1: online max / sum-exp, two vectors in flight per thread ----
+    float m = -INFINITY, sum = 0.f;
+    int c = tid * W;
+    for (; c + STEP < VW; c += 2 * STEP) {
+      const Vec<W> a = ld_keep<W>(x + c), b = ld_keep<W>(x + c + STEP);
+      accum<W>(m, sum, a);
+      accum<W>(m, sum, b);
     }
-    for (; c < V8; c += kLossThreads * 8) {
-      Vec8 a = load8(x + c);
-#pragma unroll
-      for (int t = 0; t < 8; ++t) online_add(m, s, a.v[t] * L2E);
+    for (; c < VW; c += STEP) accum<W>(m, sum, ld_keep<W>(x + c));
+    for (int cc = VW + tid; cc < V; cc += kLossThreads) {
+      const float x2 = __bfloat162float(x[cc]) * kLog2e;
+      if (x2 > m) { sum = sum * ex2f(m - x2) + 1.f; m = x2; } else { sum += ex2f(x2 - m); }
     }
-    for (int cc = V8 + tid; cc < V; cc += kLossThreads) online_add(m, s, __bfloat162float(x[cc]) * L2E);
-    // warp + block combine of (m, s)
     for (int o = 16; o > 0; o >>= 1) {
       const float m2 = __shfl_xor_sync(0xffffffffu, m, o);
-      const float s2 = __shfl_xor_sync(0xffffffffu, s, o);
+      const float s2 = __shfl_xor_sync(0xffffffffu, sum, o);
       const float mm = fmaxf(m, m2);
-      s = (mm == -INFINITY) ? 0.f : s * exp2f(m - mm) + s2 * exp2f(m2 - mm);
+      sum = (mm == -INFINITY) ? 0.f : sum * ex2f(m - mm) + s2 * ex2f(m2 - mm);
       m = mm;
     }
-    if (lane == 0) { s_red[0][warp] = m; s_red[1][warp] = s; }
+    if (lane == 0) { s_red[0][warp] = m; s_red[1][warp] = sum; }
     __syncthreads();
     if (tid == 0) {
       float M = -INFINITY, S = 0.f;
       for (int k = 0; k < kLossThreads / 32; ++k) {
         const float m2 = s_red[0][k], s2 = s_red[1][k];
         const float mm = fmaxf(M, m2);
-        S = (mm == -INFINITY) ? 0.f : S * exp2f(M - mm) + s2 * exp2f(m2 - mm);
+        S = (mm == -INFINITY) ? 0.f : S * ex2f(M - mm) + s2 * ex2f(m2 - mm);
         M = mm;
       }
       s_lse = M + log2f(S);  // log2 units
@@ -204,15 +230,18 @@ __global__ void __launch_bounds__(kLossThreads) loss_kernel(
     __syncthreads();
     // ---- pass 2: dlogits = gamma * Omega * softmax (target entries fixed up below) ----
     const float gO = gamma * Omega;
-    for (c = tid * 8; c < V8; c += kLossThreads * 8) {
-      Vec8 a = load8_coherent(x + c);
-      float f[8];
+    for (c = tid * W; c < VW; c += STEP) {
+      const Vec<W> a = ld_last<W>(x + c);
+      Vec<W> o;
 #pragma unroll
-      for (int t = 0; t < 8; ++t) f[t] = gO * exp2f(fmaf(a.v[t], L2E, -lse2));
-      store8(dx + c, f);
+      for (int t = 0; t < W / 2; ++t) {
+        const float2 f = bf2f(a.u[t]);
+        o.u[t] = f2bf(gO * ex2f(fmaf(f.x, kLog2e, -lse2)), gO * ex2f(fmaf(f.y, kLog2e, -lse2)));
+      }
+      st_vec<W>(dx + c, o);
     }
-    for (int cc = V8 + tid; cc < V; cc += kLossThreads)
-      dx[cc] = __float2bfloat16_rn(gO * exp2f(fmaf(__bfloat162float(x[cc]), L2E, -lse2)));
+    for (int cc = VW + tid; cc < V; cc += kLossThreads)
+      dx[cc] = __float2bfloat16_rn(gO * ex2f(fmaf(__bfloat162float(x[cc]), kLog2e, -lse2)));
     __syncthreads();
     // ---- fix-up: dlogits[y] = gamma (Omega p_y - sum_{k: y_k = y} omega_k), once per distinct y ----
     for (int k = tid; k < nt; k += kLossThreads) {
@@ -226,7 +255,7 @@ __global__ void __launch_bounds__(kLossThreads) loss_kernel(
         }
       }
       if (first) {
-        const float py = exp2f(fmaf(s_xy[k], L2E, -lse2));
+        const float py = ex2f(fmaf(s_xy[k], kLog2e, -lse2));
         dx[y] = __float2bfloat16_rn(gamma * (Omega * py - om_y));
       }
     }
@@ -267,10 +296,19 @@ tt_status launch_loss(const tt_packed& pk, const __nv_bfloat16* logits, int64_t 
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t grid = imin64(pk.n_tokens, (int64_t)sms * 4);
-  loss_kernel<<<(unsigned)grid, kLossThreads, 0, st>>>(pk.n_tokens, logits, ld, vocab, tok, node_mask, boundary_mode,
-                                                      gamma, pk.w, pk.node, pk.node_start, pk.node_len, pk.succ_ptr,
-                                                      pk.succ_tok, dlogits, tok_loss, ws_loss, ws_omega, d_err);
+  // 2 CTAs per SM: ~300 rows (~90 MB at V = 151,936) in flight, so pass 2 re-reads from L2
+  const int64_t grid = std::min<int64_t>(pk.n_tokens, (int64_t)sms * 2);
+  const bool v16 = (ld % 16 == 0) && ((reinterpret_cast<uintptr_t>(logits) | reinterpret_cast<uintptr_t>(dlogits)) % 32 == 0);
+  if (v16)
+    loss_kernel<16><<<(unsigned)grid, kLossThreads, 0, st>>>(pk.n_tokens, logits, ld, vocab, tok, node_mask, boundary_mode,
+                                                             gamma, pk.w, pk.node, pk.node_start, pk.node_len,
+                                                             pk.succ_ptr, pk.succ_tok, dlogits, tok_loss, ws_loss,
+                                                             ws_omega, d_err);
+  else
+    loss_kernel<8><<<(unsigned)grid, kLossThreads, 0, st>>>(pk.n_tokens, logits, ld, vocab, tok, node_mask, boundary_mode,
+                                                            gamma, pk.w, pk.node, pk.node_start, pk.node_len,
+                                                            pk.succ_ptr, pk.succ_tok, dlogits, tok_loss, ws_loss,
+                                                            ws_omega, d_err);
   count_launch();
   tt_status s = check_launch("loss_kernel");
   if (s) return s;

@@ -87,17 +87,44 @@ __global__ void __launch_bounds__(256) bwd_pre_tc_kernel(const __nv_bfloat16* __
   }
 }
 
-// fp64 sum of squares: kSqnormBlocks fixed contiguous partitions, fixed-order tree reductions.
+// fp64 sum of squares: kSqnormBlocks fixed contiguous partitions (16-byte aligned), 16-byte vector
+// loads (4 in flight per thread), squares accumulated in fp64, fixed-order tree reductions.
 template <typename T>
 __global__ void __launch_bounds__(256) sqnorm_partial_kernel(const T* __restrict__ x, int64_t n, double* __restrict__ part) {
-  const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+  constexpr int E = 16 / sizeof(T);  // elements per 16-byte vector
+  const int64_t nv = n / E;          // whole vectors (the tail is added by block 0)
+  const int64_t per = (nv + gridDim.x - 1) / gridDim.x;
   const int64_t b0 = (int64_t)blockIdx.x * per;
-  const int64_t b1 = imin64(n, b0 + per);
+  const int64_t b1 = imin64(nv, b0 + per);
+  const uint4* xv = reinterpret_cast<const uint4*>(x);
   double s = 0.0;
-  for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
-    const double v = (double)ld_f(x + i);
-    s = fma(v, v, s);
+  auto add = [&](const uint4& u) {
+    if constexpr (sizeof(T) == 2) {
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const float2 f = __bfloat1622float2(h[t]);
+        s = fma((double)f.x, (double)f.x, s);
+        s = fma((double)f.y, (double)f.y, s);
+      }
+    } else {
+      const float* f = reinterpret_cast<const float*>(&u);
+#pragma unroll
+      for (int t = 0; t < 4; ++t) s = fma((double)f[t], (double)f[t], s);
+    }
+  };
+  int64_t i = b0 + threadIdx.x;
+  for (; i + 3 * blockDim.x < b1; i += 4 * blockDim.x) {
+    const uint4 u0 = __ldg(xv + i), u1 = __ldg(xv + i + blockDim.x), u2 = __ldg(xv + i + 2 * blockDim.x),
+                u3 = __ldg(xv + i + 3 * blockDim.x);
+    add(u0); add(u1); add(u2); add(u3);
   }
+  for (; i < b1; i += blockDim.x) add(__ldg(xv + i));
+  if (blockIdx.x == 0)
+    for (int64_t t = nv * E + threadIdx.x; t < n; t += blockDim.x) {
+      const double v = (double)ld_f(x + t);
+      s = fma(v, v, s);
+    }
   __shared__ double sh[256];
   sh[threadIdx.x] = s;
   __syncthreads();

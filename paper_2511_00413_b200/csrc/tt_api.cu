@@ -401,6 +401,7 @@ tt_status tt_grad_sqnorm(const void* x, int64_t n, tt_dtype dt, double* out, voi
                          tt_stream_t stream) {
   clear_error();
   if (!x || !out || !d_ws || n < 0) { set_error("tt_grad_sqnorm: bad argument"); return TT_ERR_INVALID_ARGUMENT; }
+  if (!aligned16(x)) { set_error("tt_grad_sqnorm: x must be 16-byte aligned"); return TT_ERR_ALIGNMENT; }
   if (dt != TT_BF16 && dt != TT_FP32) { set_error("tt_grad_sqnorm: bad dtype"); return TT_ERR_INVALID_ARGUMENT; }
   if (ws_bytes < tt_grad_sqnorm_workspace(n)) { set_error("tt_grad_sqnorm: workspace too small"); return TT_ERR_WORKSPACE; }
   return launch_sqnorm(x, n, dt, out, static_cast<double*>(d_ws), as_cuda(stream));
