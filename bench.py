@@ -103,20 +103,11 @@ class ClockSampler:
 def make_trees(args, rank, world):
     from workloads import trees
     if args.config == "batch64k":
+        from paper_2511_00413_b200 import sharding, tt_pack_plan
         all_trees = [trees.config_tree("batch64k", s) for s in range(args.trees)]
-        from paper_2511_00413_b200 import tt_pack_plan
         work = [tt_pack_plan(t.parent, t.length)["n_pairs"] for t in all_trees]
-        # greedy LPT over ranks (descending work, ties by tree id) — deterministic
-        order = sorted(range(len(all_trees)), key=lambda i: (-work[i], i))
-        load = [0] * world
-        assign = [[] for _ in range(world)]
-        for i in order:
-            r = min(range(world), key=lambda x: (load[x], x))
-            assign[r].append(i)
-            load[r] += work[i]
-        mine = sorted(assign[rank])
-        imb = max(load) / (sum(load) / world)
-        return [(i, all_trees[i]) for i in mine], {"lpt_imbalance": round(imb, 4)}
+        assign, imb = sharding.lpt_partition(work, world)   # greedy LPT, deterministic
+        return [(i, all_trees[i]) for i in assign[rank]], {"lpt_imbalance": round(imb, 4)}
     seed = rank if args.seed is None else args.seed
     return [(seed, trees.config_tree(args.config, seed))], {}
 
@@ -324,25 +315,19 @@ def main():
     jobs = [TreeJob(tid, t, cfg, VOCAB, gen, with_loss=with_loss, host_copy=host_copy) for tid, t in my_trees]
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
     n_total_trees = args.trees if args.config == "batch64k" else world
-    gather = torch.zeros(n_total_trees * 6, dtype=torch.float64, device="cuda") if world > 1 else None
+
+    from paper_2511_00413_b200 import sharding
 
     def do_step(ev=None, h2d=False):
-        recs = []
         for j in jobs:
             run_step(j, ev=ev if len(jobs) == 1 else None, h2d=h2d)
-            recs.append(torch.cat([torch.tensor([float(j.tid)], dtype=torch.float64, device="cuda"), j.rec]))
         if world > 1:
-            # per-tree records [tree id, sum loss, sum Omega, |dQ|^2, |dK|^2, |dV|^2]; fixed-size
-            # per-rank slot so all_gather_into_tensor can be used; summed in tree-id order.
-            per = math.ceil(n_total_trees / world)
-            mine = torch.zeros(per * 6, dtype=torch.float64, device="cuda")
-            mine.fill_(-1.0)
-            if recs:
-                mine[:len(recs) * 6] = torch.cat(recs)
-            out = torch.empty(per * 6 * world, dtype=torch.float64, device="cuda")
-            dist.all_gather_into_tensor(out, mine)
-            return out
-        return torch.cat(recs)
+            # a6: one NCCL all_gather of the fixed-size per-tree fp64 records; every rank then
+            # sums them in tree-id order (identical totals at every world size)
+            recs = [(j.tid, j.rec) for j in jobs]
+            slot = sharding.pack_records(recs, n_total_trees, world, device="cuda")
+            return sharding.gather_records(slot, dist, world)
+        return None
 
     # warm-up
     for _ in range(args.warmup):
