@@ -11,8 +11,9 @@
 //
 // Memory plan per row (V = 151,936 bf16 = 297 KB):  pass 1 streams the row from HBM with 32-byte
 // vector loads marked L2::evict_last (online max / sum-exp in the log2 domain, one max pass and
-// at most one rescale per vector); pass 2 re-reads it from L2 (2 CTAs/SM keep ~300 rows = ~90 MB
-// in flight, under the 126 MB L2) marked evict_first, and writes dlogits (may alias logits).  HBM
+// at most one rescale per vector); pass 2 re-reads it from L2 (one 1024-thread CTA per SM keeps
+// 148 rows = 44 MB in flight, well under the 126 MB L2) marked evict_first, and writes dlogits
+// (evict_first; may alias logits).  HBM
 // traffic is therefore ~4 V bytes / row.  Rows with no target (Omega_t = 0, e.g.
 // the last token of every trajectory) skip both reads and only write zeros.
 #include <algorithm>
@@ -22,7 +23,7 @@
 namespace tt {
 namespace {
 
-constexpr int kLossThreads = 512;
+constexpr int kLossThreads = 1024;
 constexpr int kMaxTargets = 1024;
 
 // W bf16 logits per thread-vector: 16 (32-byte .v8.b32 accesses; needs 32-byte aligned rows) or 8.
@@ -61,7 +62,7 @@ template <int W> __device__ __forceinline__ Vec<W> ld_last(const __nv_bfloat16* 
 }
 template <int W> __device__ __forceinline__ void st_vec(__nv_bfloat16* p, const Vec<W>& r) {
   if constexpr (W == 16)
-    asm volatile("st.global.L1::no_allocate.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(r.u[0]), "r"(r.u[1]),
+    asm volatile("st.global.L1::no_allocate.L2::evict_first.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(r.u[0]), "r"(r.u[1]),
                  "r"(r.u[2]), "r"(r.u[3]), "r"(r.u[4]), "r"(r.u[5]), "r"(r.u[6]), "r"(r.u[7])
                  : "memory");
   else
@@ -270,6 +271,240 @@ __global__ void __launch_bounds__(kLossThreads) loss_kernel(
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Pipelined variant (V % 16 == 0, 32-byte aligned rows): warp 0 streams every row in 32 KB chunks
+// into a 4-slot shared-memory ring with TMA bulk copies (L2 evict_last policy, so pass 2 finds the
+// row in L2); 16 compute warps run pass 1 out of shared memory, then pass 2 re-reads the row from
+// L2 and writes dlogits while the producer is already prefetching the next row.
+// ---------------------------------------------------------------------------------------------
+constexpr int kPipeCompute = 512;                 // compute threads
+constexpr int kPipeThreads = kPipeCompute + 32;   // + producer warp
+constexpr int kChunkElems = 16384;                // 32 KB of bf16
+constexpr int kRing = 4;
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init_(uint64_t* b, uint32_t c) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(c) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_(uint64_t* b, uint32_t ph) {
+  asm volatile("{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra W_%=;\n}\n" ::"r"(
+                   smem_addr(b)),
+               "r"(ph)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(b)), "r"(bytes) : "memory");
+}
+
+__global__ void __launch_bounds__(kPipeThreads, 1) loss_pipe_kernel(
+    int64_t N, const __nv_bfloat16* logits, int64_t ld, int V, const int32_t* __restrict__ tok,
+    const uint8_t* __restrict__ node_mask, int boundary_mode, float gamma, const int32_t* __restrict__ w,
+    const int32_t* __restrict__ node, const int32_t* __restrict__ node_start, const int32_t* __restrict__ node_len,
+    const int32_t* __restrict__ succ_ptr, const int32_t* __restrict__ succ_tok, __nv_bfloat16* dlogits,
+    float* __restrict__ tok_loss, float* __restrict__ ws_loss, float* __restrict__ ws_omega, int32_t* d_err) {
+  extern __shared__ __align__(128) uint8_t lsm[];
+  __nv_bfloat16* ring = reinterpret_cast<__nv_bfloat16*>(lsm);            // kRing x 32 KB
+  uint64_t* full = reinterpret_cast<uint64_t*>(lsm + kRing * kChunkElems * 2);
+  uint64_t* empty = full + kRing;
+  __shared__ int s_y[kMaxTargets];
+  __shared__ float s_om[kMaxTargets];
+  __shared__ float s_xy[kMaxTargets];
+  __shared__ int s_nt;
+  __shared__ float s_red[2][kPipeCompute / 32];
+  __shared__ float s_lse;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nchunk = (V + kChunkElems - 1) / kChunkElems;
+  if (tid == 0) {
+    for (int k = 0; k < kRing; ++k) { mbar_init_(&full[k], 1); mbar_init_(&empty[k], kPipeCompute / 32); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == kPipeCompute / 32) {
+    // ============ producer warp: stream every row of this CTA, chunk by chunk ============
+    if (lane == 0) {
+      uint64_t pol;
+      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+      int g = 0;  // global chunk counter (ring slot = g % kRing)
+      for (int64_t row = blockIdx.x; row < N; row += gridDim.x) {
+        const __nv_bfloat16* x = logits + row * ld;
+        for (int c = 0; c < nchunk; ++c, ++g) {
+          const int slot = g % kRing;
+          if (g >= kRing) mbar_wait_(&empty[slot], ((g / kRing) - 1) & 1);
+          const int n = min(kChunkElems, V - c * kChunkElems);
+          mbar_expect_(&full[slot], (uint32_t)n * 2);
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+                  smem_addr(ring + slot * kChunkElems)),
+              "l"(x + (int64_t)c * kChunkElems), "r"(n * 2), "r"(smem_addr(&full[slot])), "l"(pol)
+              : "memory");
+        }
+      }
+    }
+    return;
+  }
+  // ============ compute warps ============
+  int g = 0;
+  auto bar_c = [&]() { asm volatile("bar.sync 1, %0;" ::"n"(kPipeCompute) : "memory"); };
+  for (int64_t row = blockIdx.x; row < N; row += gridDim.x) {
+    if (tid == 0) {
+      const int32_t u = node[row];
+      const bool last = row == (int64_t)node_start[u] + node_len[u] - 1;
+      int nt = 0;
+      if (!last) {
+        const int64_t tg = row + 1;
+        if (!node_mask || node_mask[node[tg]]) { s_y[0] = (int)tg; nt = 1; }
+      } else {
+        const int b = succ_ptr[u], e = succ_ptr[u + 1];
+        if (!(boundary_mode == 1 && e - b > 1)) {
+          for (int k = b; k < e; ++k) {
+            const int tg = succ_tok[k];
+            if (!node_mask || node_mask[node[tg]]) s_y[nt++] = tg;
+          }
+        }
+      }
+      s_nt = nt;
+    }
+    bar_c();
+    const int nt = s_nt;
+    float om_part = 0.f;
+    int bad = 0;
+    for (int k = tid; k < nt; k += kPipeCompute) {
+      const int tg = s_y[k];
+      const int y = tok[tg];
+      const float om = (float)w[tg];
+      bad |= (y < 0 || y >= V);
+      s_y[k] = y;
+      s_om[k] = om;
+      om_part += om;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      om_part += __shfl_xor_sync(0xffffffffu, om_part, o);
+      bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+    }
+    if (lane == 0) { s_red[0][warp] = om_part; s_red[1][warp] = (float)bad; }
+    bar_c();
+    float Omega = 0.f, badf = 0.f;
+    for (int k = 0; k < kPipeCompute / 32; ++k) { Omega += s_red[0][k]; badf += s_red[1][k]; }
+    const bool bad_any = badf != 0.f;
+    bar_c();  // s_red reused below
+    const __nv_bfloat16* x = logits + row * ld;
+    __nv_bfloat16* dx = dlogits + row * ld;
+    // ---- pass 1 from the shared-memory ring ----
+    float m = -INFINITY, sum = 0.f;
+    for (int c = 0; c < nchunk; ++c, ++g) {
+      const int slot = g % kRing;
+      mbar_wait_(&full[slot], (g / kRing) & 1);
+      const int n = min(kChunkElems, V - c * kChunkElems);
+      const uint4* src = reinterpret_cast<const uint4*>(ring + slot * kChunkElems);
+      if (Omega != 0.f && !bad_any) {
+        for (int v = tid; v < n / 16; v += kPipeCompute) {  // 16 elements = 2 x uint4 per step
+          Vec<16> r;
+          const uint4 a = src[2 * v], b = src[2 * v + 1];
+          r.u[0] = a.x; r.u[1] = a.y; r.u[2] = a.z; r.u[3] = a.w;
+          r.u[4] = b.x; r.u[5] = b.y; r.u[6] = b.z; r.u[7] = b.w;
+          accum<16>(m, sum, r);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive_(&empty[slot]);
+    }
+    if (Omega == 0.f || bad_any) {
+      Vec<16> z;
+#pragma unroll
+      for (int t = 0; t < 8; ++t) z.u[t] = 0u;
+      for (int c = tid * 16; c < V; c += kPipeCompute * 16) st_vec<16>(dx + c, z);
+      if (tid == 0) {
+        const float lv = bad_any ? __int_as_float(0x7fc00000) : 0.f;
+        if (bad_any && d_err) atomicExch(d_err, 1);
+        ws_loss[row] = lv;
+        ws_omega[row] = bad_any ? 0.f : Omega;
+        if (tok_loss) tok_loss[row] = lv;
+      }
+      continue;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const float m2 = __shfl_xor_sync(0xffffffffu, m, o);
+      const float s2 = __shfl_xor_sync(0xffffffffu, sum, o);
+      const float mm = fmaxf(m, m2);
+      sum = (mm == -INFINITY) ? 0.f : sum * ex2f(m - mm) + s2 * ex2f(m2 - mm);
+      m = mm;
+    }
+    if (lane == 0) { s_red[0][warp] = m; s_red[1][warp] = sum; }
+    bar_c();
+    if (tid == 0) {
+      float M = -INFINITY, S = 0.f;
+      for (int k = 0; k < kPipeCompute / 32; ++k) {
+        const float m2 = s_red[0][k], s2 = s_red[1][k];
+        const float mm = fmaxf(M, m2);
+        S = (mm == -INFINITY) ? 0.f : S * ex2f(M - mm) + s2 * ex2f(m2 - mm);
+        M = mm;
+      }
+      s_lse = M + log2f(S);
+    }
+    bar_c();
+    const float lse2 = s_lse;
+    float lpart = 0.f;
+    for (int k = tid; k < nt; k += kPipeCompute) {
+      const float xy = __bfloat162float(x[s_y[k]]);
+      s_xy[k] = xy;
+      lpart += s_om[k] * (lse2 * kLn2 - xy);
+    }
+    for (int o = 16; o > 0; o >>= 1) lpart += __shfl_xor_sync(0xffffffffu, lpart, o);
+    bar_c();
+    if (lane == 0) s_red[1][warp] = lpart;
+    // ---- pass 2: re-read from L2, write dlogits ----
+    const float gO = gamma * Omega;
+    auto softmax16 = [&](const Vec<16>& a, __nv_bfloat16* dst) {
+      Vec<16> o;
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const float2 f = bf2f(a.u[t]);
+        o.u[t] = f2bf(gO * ex2f(fmaf(f.x, kLog2e, -lse2)), gO * ex2f(fmaf(f.y, kLog2e, -lse2)));
+      }
+      st_vec<16>(dst, o);
+    };
+    constexpr int S2 = kPipeCompute * 16;
+    int c = tid * 16;
+    for (; c + 3 * S2 < V; c += 4 * S2) {  // four independent 32-byte loads in flight per thread
+      const Vec<16> a0 = ld_last<16>(x + c), a1 = ld_last<16>(x + c + S2), a2 = ld_last<16>(x + c + 2 * S2),
+                    a3 = ld_last<16>(x + c + 3 * S2);
+      softmax16(a0, dx + c);
+      softmax16(a1, dx + c + S2);
+      softmax16(a2, dx + c + 2 * S2);
+      softmax16(a3, dx + c + 3 * S2);
+    }
+    for (; c < V; c += S2) softmax16(ld_last<16>(x + c), dx + c);
+    bar_c();
+    for (int k = tid; k < nt; k += kPipeCompute) {
+      const int y = s_y[k];
+      bool first = true;
+      float om_y = 0.f;
+      for (int k2 = 0; k2 < nt; ++k2) {
+        if (s_y[k2] == y) {
+          if (k2 < k) first = false;
+          om_y += s_om[k2];
+        }
+      }
+      if (first) {
+        const float py = ex2f(fmaf(s_xy[k], kLog2e, -lse2));
+        dx[y] = __float2bfloat16_rn(gamma * (Omega * py - om_y));
+      }
+    }
+    if (tid == 0) {
+      float L = 0.f;
+      for (int k = 0; k < kPipeCompute / 32; ++k) L += s_red[1][k];
+      ws_loss[row] = L;
+      ws_omega[row] = Omega;
+      if (tok_loss) tok_loss[row] = L;
+    }
+    bar_c();
+  }
+}
+
 // fixed-order fp64 reduction of the per-row loss / Omega into sums[0..1]
 __global__ void __launch_bounds__(1024) loss_sum_kernel(int64_t N, const float* __restrict__ ws_loss,
                                                         const float* __restrict__ ws_omega, double* __restrict__ sums) {
@@ -296,19 +531,21 @@ tt_status launch_loss(const tt_packed& pk, const __nv_bfloat16* logits, int64_t 
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  // 2 CTAs per SM: ~300 rows (~90 MB at V = 151,936) in flight, so pass 2 re-reads from L2
-  const int64_t grid = std::min<int64_t>(pk.n_tokens, (int64_t)sms * 2);
+  // 1 CTA (1024 threads) per SM: 148 rows (~44 MB at V = 151,936) in flight, so pass 2 re-reads from L2
+  const int64_t grid = std::min<int64_t>(pk.n_tokens, (int64_t)sms);
   const bool v16 = (ld % 16 == 0) && ((reinterpret_cast<uintptr_t>(logits) | reinterpret_cast<uintptr_t>(dlogits)) % 32 == 0);
-  if (v16)
-    loss_kernel<16><<<(unsigned)grid, kLossThreads, 0, st>>>(pk.n_tokens, logits, ld, vocab, tok, node_mask, boundary_mode,
-                                                             gamma, pk.w, pk.node, pk.node_start, pk.node_len,
-                                                             pk.succ_ptr, pk.succ_tok, dlogits, tok_loss, ws_loss,
-                                                             ws_omega, d_err);
-  else
+  if (v16) {
+    const size_t smem = (size_t)kRing * kChunkElems * 2 + 2 * kRing * 8;
+    cudaFuncSetAttribute(loss_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    loss_pipe_kernel<<<(unsigned)std::min<int64_t>(pk.n_tokens, sms), kPipeThreads, smem, st>>>(
+        pk.n_tokens, logits, ld, vocab, tok, node_mask, boundary_mode, gamma, pk.w, pk.node, pk.node_start,
+        pk.node_len, pk.succ_ptr, pk.succ_tok, dlogits, tok_loss, ws_loss, ws_omega, d_err);
+  } else {
     loss_kernel<8><<<(unsigned)grid, kLossThreads, 0, st>>>(pk.n_tokens, logits, ld, vocab, tok, node_mask, boundary_mode,
                                                             gamma, pk.w, pk.node, pk.node_start, pk.node_len,
                                                             pk.succ_ptr, pk.succ_tok, dlogits, tok_loss, ws_loss,
                                                             ws_omega, d_err);
+  }
   count_launch();
   tt_status s = check_launch("loss_kernel");
   if (s) return s;
