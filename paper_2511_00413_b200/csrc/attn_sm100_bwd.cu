@@ -52,13 +52,19 @@ constexpr uint32_t kQChunk = kBQ * 64 * 2;     // 8 KB
 constexpr uint32_t kOffK = 0;
 constexpr uint32_t kOffV = kKVTile;
 constexpr uint32_t kOffQS = 2 * kKVTile;                     // stage s: Q at +s*32K, dO at +s*32K+16K
-constexpr uint32_t kOffStats = kOffQS + kQStages * 2 * kQTile;  // stage s: lse | D | w (256 B each)
-constexpr uint32_t kOffDS = ((kOffStats + kQStages * 1024 + 1023) / 1024) * 1024;  // dS^T[2], 16 KB each
 constexpr uint32_t kDSTile = 128 * kBQ * 2;
-constexpr uint32_t kOffBar = kOffDS + 2 * kDSTile;
+constexpr uint32_t kOffDS = kOffQS + kQStages * 2 * kQTile;      // dS^T[2], 16 KB each (1024-aligned)
+constexpr uint32_t kOffDQ = kOffDS + 2 * kDSTile;                 // dQ staging: 2 warpgroups x 32 rows x 128 fp32
+constexpr uint32_t kDQStage = 32 * kD * 4;
+constexpr uint32_t kStatBytes = 768;                              // per stage: -LSE2 | -D | w (256 B each)
+constexpr uint32_t kOffStats = kOffDQ + 2 * kDQStage;
+constexpr uint32_t kOffBar = kOffStats + kQStages * kStatBytes;
 constexpr uint32_t kNumBars = 1 + 2 * kQStages + 8 + 1;
 constexpr uint32_t kOffMisc = kOffBar + kNumBars * 8;
-constexpr uint32_t kSmemBytes = kOffMisc + 16 + 1024;
+// The dynamic shared-memory window is 1024-byte aligned on sm_100 (checked at run time; the kernel
+// traps otherwise), so no alignment slack is reserved.
+constexpr uint32_t kSmemBytes = kOffMisc + 16;
+static_assert(kSmemBytes <= 232448, "backward kernel exceeds 227 KB of shared memory");
 
 constexpr uint32_t kColDV = 0, kColDK = 128, kColS = 256, kColP = 384, kColQ = 448;
 
@@ -85,11 +91,12 @@ struct BwdParams {
 __global__ void __launch_bounds__(kBwdThreads, 1)
     tree_attn_bwd_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                         const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
-                        const BwdParams p) {
+                        const __grid_constant__ CUtensorMap tmdQ, const BwdParams p) {
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte aligned base; pointer arithmetic on smem_raw keeps the shared address space visible to
   // the compiler (LDS/STS instead of generic LD/ST)
-  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* smem = smem_raw;
+  if (smem_u32(smem_raw) & 1023u) __trap();
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBar);
   uint64_t* kv_full = bars;
   uint64_t* q_full = bars + 1;
@@ -152,7 +159,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const int h = hk * p.g + it / nq;
         const int q0 = (qt0 + it % nq) * kBQ;
         uint8_t* qd = smem + kOffQS + s * 2 * kQTile;
-        uint8_t* st = smem + kOffStats + s * 1024;
+        uint8_t* st = smem + kOffStats + s * kStatBytes;
         if ((p.dbg & 2) && it >= kQStages) {
           mbar_arrive(&q_full[s]);
           continue;
@@ -285,17 +292,19 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       tc_fence_before();
       mbar_arrive(&dq_free[0]);
       if (p.dbg & 1) return;
-      // fire-and-forget fp32 reductions: for a fixed query row the 32 lanes of a warp cover 32
-      // consecutive head-dim elements (128 contiguous bytes per warp instruction)
-      const int64_t rs = (int64_t)p.hq * kD;
-      float* ptr = p.dq_acc + ((int64_t)q0 * p.hq + h) * kD + r;
-      const int nrow = (int)imin64(32, p.N - q0);
-      if (nrow == 32) {
+      // stage the warpgroup's 32 query rows x 128 dims (scaled, fp32, [row][dim]) in its own smem
+      // buffer and add them into the fp32 accumulator with one TMA bulk tensor reduction; the
+      // buffer is reused one tile later, so the reduction runs asynchronously for a whole tile
+      float* stg = reinterpret_cast<float*>(smem + kOffDQ + wg * kDQStage);
+      if (r == 0) bulk_wait_read<0>();  // the previous reduction of this warpgroup has read the buffer
+      named_bar_sync(1 + wg, 128);
 #pragma unroll
-        for (int c = 0; c < 32; ++c) { atomicAdd(ptr, __uint_as_float(v[c]) * p.scale); ptr += rs; }
-      } else {
-#pragma unroll
-        for (int c = 0; c < 32; ++c) { if (c < nrow) atomicAdd(ptr, __uint_as_float(v[c]) * p.scale); ptr += rs; }
+      for (int c = 0; c < 32; ++c) stg[c * kD + r] = __uint_as_float(v[c]) * p.scale;
+      fence_proxy_async_smem();
+      named_bar_sync(1 + wg, 128);
+      if (r == 0) {
+        tma_reduce_add_3d(&tmdQ, stg, 0, h, q0);
+        bulk_commit();
       }
     };
     for (int it = 0; it < n_it; ++it) {
@@ -308,9 +317,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         tc_fence_before();
         mbar_arrive(&sm_done[b]);
       } else {
-        const float4* st_lse = reinterpret_cast<const float4*>(smem + kOffStats + s * 1024);
-        const float4* st_D = reinterpret_cast<const float4*>(smem + kOffStats + s * 1024 + 256);
-        const float4* st_w = reinterpret_cast<const float4*>(smem + kOffStats + s * 1024 + 512);
+        const float4* st_lse = reinterpret_cast<const float4*>(smem + kOffStats + s * kStatBytes);
+        const float4* st_D = reinterpret_cast<const float4*>(smem + kOffStats + s * kStatBytes + 256);
+        const float4* st_w = reinterpret_cast<const float4*>(smem + kOffStats + s * kStatBytes + 512);
         // no mask needed for this key on these 32 columns: j <= first column, last column < min(E_j, N)
         const int c0 = q0 + 32 * wg;
         // allowed query columns of this key form one interval: [max(j, c0), min(E_j, N)) - c0
@@ -324,28 +333,34 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         c_ld += clock64() - tA;
         tA = clock64();
         uint32_t pwk[16], dsk[16];
+        const bool all_in = __all_sync(0xffffffffu, cmask == 0xffffffffu);
+        const float2 SL = make_float2(sl2, sl2);
 #pragma unroll
         for (int c4 = 0; c4 < 8; ++c4) {
           const int cg = 8 * wg + c4;  // float4 group within the 64 columns
-          const float4 L = st_lse[cg];
-          const float4 Dd = st_D[cg];
+          const float4 NL = st_lse[cg];  // -LSE * log2e
+          const float4 ND = st_D[cg];    // -D
           const float4 W = st_w[cg];
-          const float Lv[4] = {L.x, L.y, L.z, L.w};
-          const float Dv[4] = {Dd.x, Dd.y, Dd.z, Dd.w};
-          const float Wv[4] = {W.x, W.y, W.z, W.w};
-          float pw[4], ds[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int c = 4 * c4 + u;
-            float pr = ex2(fmaf(__uint_as_float(sv[c]), sl2, -Lv[u]));
-            pr = ((cmask >> c) & 1u) ? pr : 0.f;
-            pw[u] = Wv[u] * pr;
-            ds[u] = pw[u] * (__uint_as_float(pv[c]) - Dv[u]);
+          const int c = 4 * c4;
+          // P = 2^(s * scale * log2e - LSE2): columns c, c+1 on the MUFU, c+2, c+3 on the FMA pipe
+          const float2 a01 = ffma2(make_float2(__uint_as_float(sv[c]), __uint_as_float(sv[c + 1])), SL, make_float2(NL.x, NL.y));
+          const float2 a23 = ffma2(make_float2(__uint_as_float(sv[c + 2]), __uint_as_float(sv[c + 3])), SL, make_float2(NL.z, NL.w));
+          float2 p01 = make_float2(ex2(a01.x), ex2(a01.y));
+          float2 p23 = exp2_poly2(a23);
+          if (!all_in) {
+            p01.x = ((cmask >> c) & 1u) ? p01.x : 0.f;
+            p01.y = ((cmask >> (c + 1)) & 1u) ? p01.y : 0.f;
+            p23.x = ((cmask >> (c + 2)) & 1u) ? p23.x : 0.f;
+            p23.y = ((cmask >> (c + 3)) & 1u) ? p23.y : 0.f;
           }
-          pwk[2 * c4] = pack_bf16(pw[0], pw[1]);
-          pwk[2 * c4 + 1] = pack_bf16(pw[2], pw[3]);
-          dsk[2 * c4] = pack_bf16(ds[0], ds[1]);
-          dsk[2 * c4 + 1] = pack_bf16(ds[2], ds[3]);
+          const float2 pw01 = fmul2(p01, make_float2(W.x, W.y));
+          const float2 pw23 = fmul2(p23, make_float2(W.z, W.w));
+          const float2 ds01 = fmul2(pw01, fadd2(make_float2(__uint_as_float(pv[c]), __uint_as_float(pv[c + 1])), make_float2(ND.x, ND.y)));
+          const float2 ds23 = fmul2(pw23, fadd2(make_float2(__uint_as_float(pv[c + 2]), __uint_as_float(pv[c + 3])), make_float2(ND.z, ND.w)));
+          pwk[2 * c4] = pack_bf16(pw01.x, pw01.y);
+          pwk[2 * c4 + 1] = pack_bf16(pw23.x, pw23.y);
+          dsk[2 * c4] = pack_bf16(ds01.x, ds01.y);
+          dsk[2 * c4 + 1] = pack_bf16(ds23.x, ds23.y);
         }
         c_math += clock64() - tA;
         tA = clock64();
@@ -372,6 +387,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       c_dr += clock64() - t_dr;
     }
     drain(n_it - 1);
+    if (r == 0) bulk_wait<0>();
     if ((p.dbg & 8) && r == 0 && wg == 0) {
       atomicAdd(&g_bwd_dbg[5], (unsigned long long)c_ws);
       atomicAdd(&g_bwd_dbg[6], (unsigned long long)c_el);
@@ -453,13 +469,15 @@ tt_status sm100_attn_bwd(const tt_packed& pk, const void* q, const void* k, cons
   float* dq_acc = reinterpret_cast<float*>(w8 + 2 * al256b((size_t)hq * Np * 4) + al256b((size_t)Np * 4));
   tt_status s = launch_bwd_pre_tc(o, dout, lse, pk.w, restore, N, Np, hq, Dp, L2p, wf, dq_acc, st);
   if (s) return s;
-  CUtensorMap mq, mk, mv, mdo;
+  CUtensorMap mq, mk, mv, mdo, mdq;
   const auto BF = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   const auto SW = CU_TENSOR_MAP_SWIZZLE_128B;
   if ((s = make_tmap_thd(&mq, q, N, hq, d, kBQ, BF, 2, SW, 64))) return s;
   if ((s = make_tmap_thd(&mdo, dout, N, hq, d, kBQ, BF, 2, SW, 64))) return s;
   if ((s = make_tmap_thd(&mk, k, N, hkv, d, 128, BF, 2, SW, 64))) return s;
   if ((s = make_tmap_thd(&mv, v, N, hkv, d, 128, BF, 2, SW, 64))) return s;
+  if ((s = make_tmap_thd(&mdq, dq_acc, N, hq, d, 32, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, CU_TENSOR_MAP_SWIZZLE_NONE, kD)))
+    return s;
   BwdParams prm;
   prm.N = N;
   prm.hq = hq;
@@ -485,7 +503,7 @@ tt_status sm100_attn_bwd(const tt_packed& pk, const void* q, const void* k, cons
   cudaError_t e = cudaFuncSetAttribute(tree_attn_bwd_sm100, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
   if (e != cudaSuccess) { set_error("sm100_attn_bwd: smem attribute: %s", cudaGetErrorString(e)); return TT_ERR_CUDA; }
   const unsigned grid = (unsigned)pk.n_blk * hkv;
-  tree_attn_bwd_sm100<<<grid, kBwdThreads, kSmemBytes, st>>>(mq, mk, mv, mdo, prm);
+  tree_attn_bwd_sm100<<<grid, kBwdThreads, kSmemBytes, st>>>(mq, mk, mv, mdo, mdq, prm);
   count_launch();
   if ((s = check_launch("tree_attn_bwd_sm100"))) return s;
   const int64_t n4 = N * hq * d / 4;

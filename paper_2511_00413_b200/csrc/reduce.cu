@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(256) bwd_pre_kernel(const T* __restrict__ o, c
   }
 }
 
-// Tensor-core backward preprocess: per (token, head) D_i = dO_i . O_i, LSE_i in log2 units, and
+// Tensor-core backward preprocess: per (token, head) -D_i = -dO_i . O_i, -LSE_i in log2 units, and
 // per token the tree-scale as fp32 (w_i, or 1 without restoration), all laid out with the token
 // dimension padded to Np (a multiple of 128) so the kernel can bulk-copy 64-row slices; padded rows
 // get D = 0, LSE = 0, w = 0.  Also zeroes the fp32 dQ accumulator.
@@ -81,8 +81,8 @@ __global__ void __launch_bounds__(256) bwd_pre_tc_kernel(const __nv_bfloat16* __
   }
   for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
   if (lane == 0) {
-    Dp[(int64_t)h * Np + i] = s;
-    L2p[(int64_t)h * Np + i] = i < N ? lse[(int64_t)h * N + i] * kLog2e : 0.f;
+    Dp[(int64_t)h * Np + i] = -s;                                              // stored negated
+    L2p[(int64_t)h * Np + i] = i < N ? -lse[(int64_t)h * N + i] * kLog2e : 0.f;  // stored negated
     if (h == 0) wf[i] = i < N ? (restore ? (float)w[i] : 1.f) : 0.f;
   }
 }
