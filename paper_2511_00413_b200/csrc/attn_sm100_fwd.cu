@@ -21,6 +21,8 @@
 // O (bf16) and LSE (fp32, natural log).
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
+
 #include "sm100_ptx.cuh"
 #include "tt_internal.cuh"
 
@@ -42,10 +44,13 @@ constexpr uint32_t kOffMisc = kOffBar + kNumBars * 8;
 constexpr uint32_t kOffTiles = kOffMisc + 16;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 
+__device__ unsigned long long g_fwd_dbg[16];  // development instrumentation (TT_DEBUG_FWD & 8)
+
 struct FwdParams {
   int64_t N;
   int hq, hkv, nb, npairs;
   float scale_log2;
+  int dbg;
   const int32_t* E;
   const int32_t* fwd_cnt;
   const int32_t* fwd_list;
@@ -144,8 +149,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         for (int c = 0; c < 2; ++c)
           tma_load_3d(kd + kTileBytes + c * kChunkBytes, &tmV, &full[s], c * 64, hk, kb * 128);
       }
-    } else if (warp == 1 && lane == 0) {
-      // ===================== MMA issuer =====================
+    } else if (warp == 1) {
+      // ===================== MMA issuer (whole warp converged, one elected lane issues) ==========
       constexpr uint32_t idS = idesc_bf16(128, 128, 0, 0);  // Q (K-major) x K^T (K-major)
       constexpr uint32_t idO = idesc_bf16(128, 128, 0, 1);  // P (TMEM, K-major) x V (MN-major)
       int last[2] = {-1, -1};
@@ -153,19 +158,21 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         if (tile_cls(tiles[t], 0)) last[0] = t;
         if (tile_cls(tiles[t], 1)) last[1] = t;
       }
-      const uint32_t qbase = smem_u32(smem + kOffQ);
+      const uint32_t qbase = warp_uniform(smem_u32(smem + kOffQ));
+      const uint32_t tm = warp_uniform(tmem);
       auto issue_S = [&](int i, int t) {
-        const uint32_t kbase = smem_u32(smem + kOffKV + (t % kStages) * 2 * kTileBytes);
+        const uint32_t kbase = qbase + kOffKV + (t % kStages) * 2 * kTileBytes;
         const uint32_t qb = qbase + i * kTileBytes;
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           const uint32_t off = (kk >> 2) * kChunkBytes + (kk & 3) * 32;
-          mma_ss(tmem + 128 * i, sdesc(qb + off, 16, 1024), sdesc(kbase + off, 16, 1024), idS, kk > 0);
+          mma_ss_w(tm + 128 * i, sdesc(qb + off, 16, 1024), sdesc(kbase + off, 16, 1024), idS, kk > 0);
         }
-        mma_commit(&s_full[i]);
+        mma_commit_w(&s_full[i]);
       };
       uint32_t pph[2] = {0, 0};
       bool first[2] = {true, true};
+      long long w_p = 0, w_kv = 0, t_beg = clock64();
       mbar_wait(bar_q, 0);
       if (T > 0) {
         mbar_wait(&full[0], 0);
@@ -176,31 +183,37 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       }
       for (int t = 0; t < T; ++t) {
         const int s = t % kStages;
-        const uint32_t vbase = smem_u32(smem + kOffKV + s * 2 * kTileBytes + kTileBytes);
+        const uint32_t vbase = qbase + kOffKV + s * 2 * kTileBytes + kTileBytes;
         bool waited = false;
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
           if (tile_cls(tiles[t], i)) {
-            mbar_wait(&p_full[i], pph[i]);
+            { long long t0 = clock64(); mbar_wait(&p_full[i], pph[i]); w_p += clock64() - t0; }
             pph[i] ^= 1;
             tc_fence_after();
 #pragma unroll
             for (int kk = 0; kk < 8; ++kk)
-              mma_ts(tmem + 256 + 128 * i, tmem + 128 * i + kk * 8, sdesc(vbase + kk * 2048, kChunkBytes, 1024), idO,
+              mma_ts_w(tm + 256 + 128 * i, tm + 128 * i + kk * 8, sdesc(vbase + kk * 2048, kChunkBytes, 1024), idO,
                      (!first[i] || kk > 0) ? 1u : 0u);
             first[i] = false;
-            if (t == last[i]) mma_commit(&o_full[i]);
+            if (t == last[i]) mma_commit_w(&o_full[i]);
           }
           if (t + 1 < T && tile_cls(tiles[t + 1], i)) {
             if (!waited) {
-              mbar_wait(&full[(t + 1) % kStages], ((t + 1) / kStages) & 1);
+              { long long t0 = clock64(); mbar_wait(&full[(t + 1) % kStages], ((t + 1) / kStages) & 1); w_kv += clock64() - t0; }
               tc_fence_after();
               waited = true;
             }
             issue_S(i, t + 1);
           }
         }
-        mma_commit(&empty[s]);
+        mma_commit_w(&empty[s]);
+      }
+      if ((p.dbg & 8) && lane == 0) {
+        atomicAdd(&g_fwd_dbg[0], (unsigned long long)(clock64() - t_beg));
+        atomicAdd(&g_fwd_dbg[1], (unsigned long long)w_p);
+        atomicAdd(&g_fwd_dbg[2], (unsigned long long)w_kv);
+        atomicAdd(&g_fwd_dbg[3], (unsigned long long)T);
       }
     }
   } else {
@@ -216,6 +229,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     float m = -INFINITY, l = 0.f;
     uint32_t sph = 0;
     bool first = true;
+    long long c_ws = 0, c_cmp = 0, c_n = 0, c_ld = 0, c_math = 0, c_stt = 0;
     if (i == 0 || has1) {
       for (int t = 0; t < T; ++t) {
         const int32_t e = tiles[t];
@@ -223,7 +237,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         if (!cls) continue;
         const int kb = e & kKbMask;
         const int64_t j0 = (int64_t)kb * 128;
-        mbar_wait(&s_full[i], sph);
+        { long long t0 = clock64(); mbar_wait(&s_full[i], sph); c_ws += clock64() - t0; }
+        long long t_cmp = clock64();
         sph ^= 1;
         tc_fence_after();
         uint32_t s[128];
@@ -232,6 +247,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         tmem_ld32(tS + 64, *reinterpret_cast<uint32_t(*)[32]>(&s[64]));
         tmem_ld32(tS + 96, *reinterpret_cast<uint32_t(*)[32]>(&s[96]));
         tmem_wait_ld();
+        c_ld += clock64() - t_cmp;
+        long long t_m = clock64();
         // ---- mask (partial tiles, and key columns past N on the ragged last block) ----
         if (cls == kClsPartial) {
           const int4* Es = reinterpret_cast<const int4*>(smem + kOffE + (t % kStages) * 512);
@@ -253,25 +270,53 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           for (int c = 0; c < 128; ++c)
             if (c >= jmax) s[c] = __float_as_uint(-INFINITY);
         }
-        // ---- row max (log2 units) ----
-        float mx = -INFINITY;
+        // ---- row max (log2 units): 8 independent partial maxima, then a tree ----
+        float pm[8];
 #pragma unroll
-        for (int c = 0; c < 128; ++c) mx = fmaxf(mx, __uint_as_float(s[c]));
+        for (int u = 0; u < 8; ++u) pm[u] = __uint_as_float(s[u]);
+#pragma unroll
+        for (int c = 8; c < 128; c += 8)
+#pragma unroll
+          for (int u = 0; u < 8; ++u) pm[u] = fmaxf(pm[u], __uint_as_float(s[c + u]));
+        const float mx = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])), fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7])));
         const float m_new = fmaxf(m, mx * sl2);
         const bool resc = (m == -INFINITY) ? (m_new != -INFINITY) : (m_new > m + kRescaleThreshold);
         const float m_use = resc ? m_new : m;
         const float corr = (m == -INFINITY) ? 0.f : ex2(m - m_use);
         const float mb = (m_use == -INFINITY) ? 0.f : m_use;
         // ---- P = exp2(s * scale_log2 - m), packed bf16 in place (s[0..63]) ----
-        float lsum0 = 0.f, lsum1 = 0.f;
+        // packed f32x2 FMAs; on tiles without any mask half of the exponentials run as a
+        // polynomial on the FMA pipe (FA4-style) to relieve the MUFU unit
+        const float2 SL = make_float2(sl2, sl2), NM = make_float2(-mb, -mb);
+        float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f), acc2 = make_float2(0.f, 0.f),
+               acc3 = make_float2(0.f, 0.f);
+        if (cls == kClsFull && j0 + 128 <= p.N) {
 #pragma unroll
-        for (int c = 0; c < 128; c += 2) {
-          const float p0 = ex2(fmaf(__uint_as_float(s[c]), sl2, -mb));
-          const float p1 = ex2(fmaf(__uint_as_float(s[c + 1]), sl2, -mb));
-          lsum0 += p0;
-          lsum1 += p1;
-          s[c >> 1] = pack_bf16(p0, p1);
+          for (int c = 0; c < 128; c += 4) {
+            const float2 a01 = ffma2(make_float2(__uint_as_float(s[c]), __uint_as_float(s[c + 1])), SL, NM);
+            const float2 a23 = ffma2(make_float2(__uint_as_float(s[c + 2]), __uint_as_float(s[c + 3])), SL, NM);
+            const float2 p01 = make_float2(ex2(a01.x), ex2(a01.y));
+            const float2 p23 = exp2_poly2(a23);
+            if (c & 4) { acc2 = fadd2(acc2, p01); acc3 = fadd2(acc3, p23); }
+            else { acc0 = fadd2(acc0, p01); acc1 = fadd2(acc1, p23); }
+            s[c >> 1] = pack_bf16(p01.x, p01.y);
+            s[(c >> 1) + 1] = pack_bf16(p23.x, p23.y);
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < 128; c += 4) {
+            const float2 a01 = ffma2(make_float2(__uint_as_float(s[c]), __uint_as_float(s[c + 1])), SL, NM);
+            const float2 a23 = ffma2(make_float2(__uint_as_float(s[c + 2]), __uint_as_float(s[c + 3])), SL, NM);
+            const float2 p01 = make_float2(ex2(a01.x), ex2(a01.y));
+            const float2 p23 = make_float2(ex2(a23.x), ex2(a23.y));
+            if (c & 4) { acc2 = fadd2(acc2, p01); acc3 = fadd2(acc3, p23); }
+            else { acc0 = fadd2(acc0, p01); acc1 = fadd2(acc1, p23); }
+            s[c >> 1] = pack_bf16(p01.x, p01.y);
+            s[(c >> 1) + 1] = pack_bf16(p23.x, p23.y);
+          }
         }
+        const float2 accs = fadd2(fadd2(acc0, acc1), fadd2(acc2, acc3));
+        const float lsum0 = accs.x, lsum1 = accs.y;
         l = l * corr + (lsum0 + lsum1);
         m = m_use;
         // ---- lazy rescale of the O accumulator (PV of the previous tile has completed: its
@@ -287,11 +332,16 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             tmem_st32(tO + 32 * cc, ov);
           }
         }
+        c_math += clock64() - t_m;
+        long long t_st = clock64();
         tmem_st32(tS + 0, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
         tmem_st32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
         tmem_wait_st();
         tc_fence_before();
         mbar_arrive(&p_full[i]);
+        c_stt += clock64() - t_st;
+        c_cmp += clock64() - t_cmp;
+        ++c_n;
         first = false;
       }
       // ---- epilogue: O / l -> bf16, LSE ----
@@ -315,6 +365,14 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         }
       }
       if (row < p.N) p.lse[(int64_t)h * p.N + row] = (m + __log2f(l)) * kLn2;
+      if ((p.dbg & 8) && r == 0 && i == 0) {
+        atomicAdd(&g_fwd_dbg[4], (unsigned long long)c_ws);
+        atomicAdd(&g_fwd_dbg[5], (unsigned long long)c_cmp);
+        atomicAdd(&g_fwd_dbg[6], (unsigned long long)c_n);
+        atomicAdd(&g_fwd_dbg[7], (unsigned long long)c_ld);
+        atomicAdd(&g_fwd_dbg[8], (unsigned long long)c_math);
+        atomicAdd(&g_fwd_dbg[9], (unsigned long long)c_stt);
+      }
     }
   }
   tc_fence_before();
@@ -355,6 +413,15 @@ tt_status make_tmap_thd(CUtensorMap* m, const void* ptr, int64_t rows, int heads
   return TT_OK;
 }
 
+extern "C" int tt_debug_fwd_counters(unsigned long long* out, int reset) {
+  cudaMemcpyFromSymbol(out, g_fwd_dbg, sizeof(g_fwd_dbg));
+  if (reset) {
+    unsigned long long z[16] = {0};
+    cudaMemcpyToSymbol(g_fwd_dbg, z, sizeof(z));
+  }
+  return 0;
+}
+
 size_t sm100_fwd_smem_bytes(int nb) {
   return 1024 + kOffTiles + (size_t)(2 * nb + 4) * 4 + 2 * (size_t)(nb + 4) + 16;
 }
@@ -377,6 +444,10 @@ tt_status sm100_attn_fwd(const tt_packed& pk, const void* q, const void* k, cons
   prm.nb = nb;
   prm.npairs = (nb + 1) / 2;
   prm.scale_log2 = scale * kLog2e;
+  {
+    const char* e = getenv("TT_DEBUG_FWD");
+    prm.dbg = e ? atoi(e) : 0;
+  }
   prm.E = pk.E;
   prm.fwd_cnt = pk.fwd_cnt;
   prm.fwd_list = pk.fwd_list;

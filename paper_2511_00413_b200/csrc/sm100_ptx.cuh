@@ -250,10 +250,11 @@ __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
 }
 // 2^x on the FMA pipe (offloads the MUFU unit, FA4-style): x = n + f with n = round(x) obtained by
 // the 1.5*2^23 trick, 2^f on [-1/2, 1/2] by a degree-3 polynomial (max rel. error 7.5e-5, below
-// the bf16 rounding of P and dS), and 2^n added into the exponent bits.  x is clamped at -127.
+// the bf16 rounding of P and dS), and 2^n added into the exponent bits.  x is clamped at -125 so the
+// result stays a normal number (inputs below -125 return ~2^-125 instead of 0: < 3e-38 absolute).
 __device__ __forceinline__ float2 exp2_poly2(float2 x) {
-  x.x = fmaxf(x.x, -127.f);
-  x.y = fmaxf(x.y, -127.f);
+  x.x = fmaxf(x.x, -125.f);
+  x.y = fmaxf(x.y, -125.f);
   const float2 M = make_float2(12582912.f, 12582912.f);
   const float2 t = fadd2(x, M);
   const float2 r = fadd2(t, make_float2(-12582912.f, -12582912.f));

@@ -1,0 +1,17 @@
+import ctypes, os, sys, torch
+sys.path.insert(0, '/root/repo')
+os.environ["TT_DEBUG_FWD"] = "8"
+import paper_2511_00413_b200 as tt
+from workloads import trees, tensors
+L = tt.lib()
+for cfg, seed in [("agentic8k", 0), ("deep32k", 1)]:
+    t = trees.config_tree(cfg, seed); c = trees.CONFIGS[cfg]
+    pk = tt.tt_pack(t.parent, t.length); N = pk.n_tokens; hq, hkv, d = c["hq"], c["hkv"], c["d"]
+    q, k, v = (x.cuda() for x in tensors.qkv_tensors(N, hq, hkv, d, "bf16", seed=0))
+    buf = (ctypes.c_ulonglong * 16)()
+    tt.tt_attn_fwd(pk, q, k, v); torch.cuda.synchronize(); L.tt_debug_fwd_counters(buf, 1)
+    tt.tt_attn_fwd(pk, q, k, v); torch.cuda.synchronize(); L.tt_debug_fwd_counters(buf, 1)
+    b = list(buf); T = b[3]; n = b[6]
+    n = max(n, 1)
+    print(cfg, "merged tiles", T, "per-tile cycles: mma_total %.0f wait_p %.0f wait_kv %.0f | softmax(wg0,r0) tiles %d: wait_s %.0f compute %.0f [ld %.0f math %.0f st %.0f]" %
+          (b[0] / T, b[1] / T, b[2] / T, n, b[4] / n, b[5] / n, b[7] / n, b[8] / n, b[9] / n), flush=True)
