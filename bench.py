@@ -180,7 +180,7 @@ def run_step(job, ev=None, h2d=False):
     if job.with_loss:
         mark("loss", 0)
         tt.tt_restore_loss(pk, job.logits, job.tok, grad_scale=1.0, dlogits=job.dlogits,   # a3
-                           tok_loss=job.tok_loss, sums=job.sums, d_err=job.err)
+                           tok_loss=job.tok_loss, sums=job.rec[0:2], d_err=job.err)
         mark("loss", 1)
     if job.ws is None:
         job.ws = torch.empty(tt.tt_attn_bwd_workspace(pk, job.hq, job.hkv, job.d, job.q.dtype),
@@ -190,10 +190,7 @@ def run_step(job, ev=None, h2d=False):
                    dq=job.dq, dk=job.dk, dv=job.dv, ws=job.ws)
     mark("bwd", 1)
     mark("scal", 0)
-    if job.with_loss:
-        job.rec[0:2].copy_(job.sums)
-    for i, x in enumerate((job.dq, job.dk, job.dv)):                                       # a6
-        tt.tt_grad_sqnorm(x, out=job.rec[2 + i:3 + i])
+    tt.tt_grad_sqnorm3(job.dq, job.dk, job.dv, out=job.rec[2:5])                          # a6
     mark("scal", 1)
     if h2d:
         job.rec_host.copy_(job.rec, non_blocking=True)

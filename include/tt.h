@@ -197,11 +197,18 @@ tt_status tt_restore_loss(const tt_packed* pk, const void* logits, int64_t ld, i
                           float* tok_loss, double* sums, int32_t* d_err, void* d_ws, size_t ws_bytes,
                           tt_stream_t stream);
 
-/* Deterministic fp64 sum of squares of n elements of x (dtype dt) into *out (device).
+/* Deterministic sum of squares of n elements of x (dtype dt) into *out (device, fp64): the squares
+ * of each 16-byte vector are summed in fp32 (exact squares for bf16; <= 2^-21 relative for the
+ * 8-term sum), vectors are accumulated in fp64 over a fixed partition and reduced in a fixed order,
+ * so the result is bitwise reproducible.  x must be 16-byte aligned.
  * ws >= tt_grad_sqnorm_workspace(n) bytes. */
 size_t tt_grad_sqnorm_workspace(int64_t n);
 tt_status tt_grad_sqnorm(const void* x, int64_t n, tt_dtype dt, double* out, void* d_ws, size_t ws_bytes,
                          tt_stream_t stream);
+/* The per-tree gradient-norm scalars of §8(a) a6 in one launch: out[k] = sum of squares of tensor k
+ * (e.g. dQ, dK, dV).  Same numerics as tt_grad_sqnorm; ws >= tt_grad_sqnorm_workspace(0). */
+tt_status tt_grad_sqnorm3(const void* x0, int64_t n0, const void* x1, int64_t n1, const void* x2, int64_t n2,
+                          tt_dtype dt, double* out, void* d_ws, size_t ws_bytes, tt_stream_t stream);
 
 /* Kernel-level launch counters (for bench.py's gpu_launches claim): number of kernels this
  * thread has launched through the library since the last reset. */

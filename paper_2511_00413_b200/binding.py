@@ -84,12 +84,13 @@ def lib():
             L.tt_grad_sqnorm_workspace.restype = C.c_size_t
             L.tt_grad_sqnorm_workspace.argtypes = [C.c_int64]
             L.tt_grad_sqnorm.argtypes = [vp, C.c_int64, C.c_int, vp, vp, sz, st]
+            L.tt_grad_sqnorm3.argtypes = [vp, C.c_int64, vp, C.c_int64, vp, C.c_int64, C.c_int, vp, vp, sz, st]
             L.tt_launch_count.restype = C.c_int64
             L.tt_launch_count.argtypes = []
             L.tt_launch_count_reset.argtypes = []
             L.tt_launch_count_reset.restype = None
             for fn in ("tt_pack_plan", "tt_pack", "tt_attn_fwd", "tt_attn_bwd_workspace", "tt_attn_bwd",
-                       "tt_restore_loss", "tt_grad_sqnorm"):
+                       "tt_restore_loss", "tt_grad_sqnorm", "tt_grad_sqnorm3"):
                 getattr(L, fn).restype = C.c_int
             _lib = L
     return _lib
@@ -287,4 +288,18 @@ def tt_grad_sqnorm(x, out=None, ws=None, stream=None):
         ws = torch.empty(need, dtype=torch.uint8, device=x.device)
     _check("tt_grad_sqnorm", L.tt_grad_sqnorm(_p(x), int(x.numel()), _dt(x), _p(out), _p(ws), int(ws.numel()),
                                               _stream(stream)))
+    return out
+
+
+def tt_grad_sqnorm3(x0, x1, x2, out=None, ws=None, stream=None):
+    """Sums of squares of three tensors (same dtype) in one launch -> out [3] fp64 (device)."""
+    import torch
+    out = torch.zeros(3, dtype=torch.float64, device=x0.device) if out is None else out
+    L = lib()
+    need = int(L.tt_grad_sqnorm_workspace(0))
+    if ws is None or ws.numel() < need:
+        ws = torch.empty(need, dtype=torch.uint8, device=x0.device)
+    _check("tt_grad_sqnorm3", L.tt_grad_sqnorm3(_p(x0), int(x0.numel()), _p(x1), int(x1.numel()), _p(x2),
+                                                int(x2.numel()), _dt(x0), _p(out), _p(ws), int(ws.numel()),
+                                                _stream(stream)))
     return out

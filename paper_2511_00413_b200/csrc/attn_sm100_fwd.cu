@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   const int h = (int)(blockIdx.x % p.hq);
   const int hk = h / (p.hq / p.hkv);
   const int qa = 2 * pair;
-  const bool has1 = qa + 1 < p.nb;
+  const bool has1 = qa + 1 < p.nb && !(p.dbg & 16);  // dbg 16: development ablation, drop query tile 1
   const int kb_end = has1 ? qa + 2 : qa + 1;
 
   // ---- merged tile list of the two query blocks: kb | cls0 << 28 | cls1 << 30 ----

@@ -87,39 +87,55 @@ __global__ void __launch_bounds__(256) bwd_pre_tc_kernel(const __nv_bfloat16* __
   }
 }
 
-// fp64 sum of squares: kSqnormBlocks fixed contiguous partitions (16-byte aligned), 16-byte vector
-// loads (4 in flight per thread), squares accumulated in fp64, fixed-order tree reductions.
+// Sum of squares over up to 3 tensors in one launch: kSqnormBlocks fixed contiguous partitions per
+// tensor (blockIdx.y = tensor), 16-byte vector loads (4 in flight per thread).  The squares of one
+// vector are summed in fp32 (squares of bf16 values are exact in fp32; the 8-term fp32 sum has
+// relative error <= 2^-21), vectors are accumulated in fp64, then fixed-order tree reductions —
+// bitwise reproducible.
+struct SqArgs {
+  const void* x[3];
+  int64_t n[3];
+};
+
 template <typename T>
-__global__ void __launch_bounds__(256) sqnorm_partial_kernel(const T* __restrict__ x, int64_t n, double* __restrict__ part) {
-  constexpr int E = 16 / sizeof(T);  // elements per 16-byte vector
-  const int64_t nv = n / E;          // whole vectors (the tail is added by block 0)
+__global__ void __launch_bounds__(256) sqnorm_partial_kernel(SqArgs a, double* __restrict__ part) {
+  constexpr int E = 16 / sizeof(T);
+  const int tsr = blockIdx.y;
+  const T* x = static_cast<const T*>(a.x[tsr]);
+  const int64_t n = a.n[tsr];
+  const int64_t nv = n / E;
   const int64_t per = (nv + gridDim.x - 1) / gridDim.x;
   const int64_t b0 = (int64_t)blockIdx.x * per;
   const int64_t b1 = imin64(nv, b0 + per);
   const uint4* xv = reinterpret_cast<const uint4*>(x);
   double s = 0.0;
-  auto add = [&](const uint4& u) {
+  auto vsq = [&](const uint4& u) -> float {
+    float r = 0.f;
     if constexpr (sizeof(T) == 2) {
       const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
         const float2 f = __bfloat1622float2(h[t]);
-        s = fma((double)f.x, (double)f.x, s);
-        s = fma((double)f.y, (double)f.y, s);
+        r = fmaf(f.x, f.x, r);
+        r = fmaf(f.y, f.y, r);
       }
     } else {
       const float* f = reinterpret_cast<const float*>(&u);
 #pragma unroll
-      for (int t = 0; t < 4; ++t) s = fma((double)f[t], (double)f[t], s);
+      for (int t = 0; t < 4; ++t) r = fmaf(f[t], f[t], r);
     }
+    return r;
   };
   int64_t i = b0 + threadIdx.x;
   for (; i + 3 * blockDim.x < b1; i += 4 * blockDim.x) {
     const uint4 u0 = __ldg(xv + i), u1 = __ldg(xv + i + blockDim.x), u2 = __ldg(xv + i + 2 * blockDim.x),
                 u3 = __ldg(xv + i + 3 * blockDim.x);
-    add(u0); add(u1); add(u2); add(u3);
+    s += (double)vsq(u0);
+    s += (double)vsq(u1);
+    s += (double)vsq(u2);
+    s += (double)vsq(u3);
   }
-  for (; i < b1; i += blockDim.x) add(__ldg(xv + i));
+  for (; i < b1; i += blockDim.x) s += (double)vsq(__ldg(xv + i));
   if (blockIdx.x == 0)
     for (int64_t t = nv * E + threadIdx.x; t < n; t += blockDim.x) {
       const double v = (double)ld_f(x + t);
@@ -132,10 +148,12 @@ __global__ void __launch_bounds__(256) sqnorm_partial_kernel(const T* __restrict
     if ((int)threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
     __syncthreads();
   }
-  if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
+  if (threadIdx.x == 0) part[(int64_t)tsr * gridDim.x + blockIdx.x] = sh[0];
 }
 
 __global__ void __launch_bounds__(256) sum_partials_kernel(const double* __restrict__ part, int n, double* __restrict__ out) {
+  part += (int64_t)blockIdx.x * n;
+  out += blockIdx.x;
   double s = 0.0;
   for (int i = threadIdx.x; i < n; i += blockDim.x) s += part[i];
   __shared__ double sh[256];
@@ -173,15 +191,19 @@ tt_status launch_bwd_pre_tc(const void* o, const void* dout, const float* lse, c
   return check_launch("bwd_pre_tc_kernel");
 }
 
-tt_status launch_sqnorm(const void* x, int64_t n, tt_dtype dt, double* out, double* partials, cudaStream_t st) {
+tt_status launch_sqnorm(const void* const* xs, const int64_t* ns, int count, tt_dtype dt, double* out,
+                        double* partials, cudaStream_t st) {
+  SqArgs a{};
+  for (int k = 0; k < count; ++k) { a.x[k] = xs[k]; a.n[k] = ns[k]; }
+  const dim3 grid(kSqnormBlocks, count);
   if (dt == TT_BF16)
-    sqnorm_partial_kernel<__nv_bfloat16><<<kSqnormBlocks, 256, 0, st>>>((const __nv_bfloat16*)x, n, partials);
+    sqnorm_partial_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(a, partials);
   else
-    sqnorm_partial_kernel<float><<<kSqnormBlocks, 256, 0, st>>>((const float*)x, n, partials);
+    sqnorm_partial_kernel<float><<<grid, 256, 0, st>>>(a, partials);
   count_launch();
   tt_status s = check_launch("sqnorm_partial_kernel");
   if (s) return s;
-  sum_partials_kernel<<<1, 256, 0, st>>>(partials, kSqnormBlocks, out);
+  sum_partials_kernel<<<count, 256, 0, st>>>(partials, kSqnormBlocks, out);
   count_launch();
   return check_launch("sum_partials_kernel");
 }

@@ -395,7 +395,7 @@ tt_status tt_restore_loss(const tt_packed* pk, const void* logits, int64_t ld, i
                      as_cuda(stream));
 }
 
-size_t tt_grad_sqnorm_workspace(int64_t n) { (void)n; return al256(kSqnormBlocks * sizeof(double)); }
+size_t tt_grad_sqnorm_workspace(int64_t n) { (void)n; return al256(3 * kSqnormBlocks * sizeof(double)); }
 
 tt_status tt_grad_sqnorm(const void* x, int64_t n, tt_dtype dt, double* out, void* d_ws, size_t ws_bytes,
                          tt_stream_t stream) {
@@ -404,7 +404,24 @@ tt_status tt_grad_sqnorm(const void* x, int64_t n, tt_dtype dt, double* out, voi
   if (!aligned16(x)) { set_error("tt_grad_sqnorm: x must be 16-byte aligned"); return TT_ERR_ALIGNMENT; }
   if (dt != TT_BF16 && dt != TT_FP32) { set_error("tt_grad_sqnorm: bad dtype"); return TT_ERR_INVALID_ARGUMENT; }
   if (ws_bytes < tt_grad_sqnorm_workspace(n)) { set_error("tt_grad_sqnorm: workspace too small"); return TT_ERR_WORKSPACE; }
-  return launch_sqnorm(x, n, dt, out, static_cast<double*>(d_ws), as_cuda(stream));
+  const void* xs[1] = {x};
+  const int64_t ns[1] = {n};
+  return launch_sqnorm(xs, ns, 1, dt, out, static_cast<double*>(d_ws), as_cuda(stream));
+}
+
+tt_status tt_grad_sqnorm3(const void* x0, int64_t n0, const void* x1, int64_t n1, const void* x2, int64_t n2,
+                          tt_dtype dt, double* out, void* d_ws, size_t ws_bytes, tt_stream_t stream) {
+  clear_error();
+  const void* xs[3] = {x0, x1, x2};
+  const int64_t ns[3] = {n0, n1, n2};
+  for (int k = 0; k < 3; ++k) {
+    if (!xs[k] || ns[k] < 0) { set_error("tt_grad_sqnorm3: bad tensor %d", k); return TT_ERR_INVALID_ARGUMENT; }
+    if (!aligned16(xs[k])) { set_error("tt_grad_sqnorm3: tensor %d must be 16-byte aligned", k); return TT_ERR_ALIGNMENT; }
+  }
+  if (!out || !d_ws) { set_error("tt_grad_sqnorm3: bad argument"); return TT_ERR_INVALID_ARGUMENT; }
+  if (dt != TT_BF16 && dt != TT_FP32) { set_error("tt_grad_sqnorm3: bad dtype"); return TT_ERR_INVALID_ARGUMENT; }
+  if (ws_bytes < tt_grad_sqnorm_workspace(0)) { set_error("tt_grad_sqnorm3: workspace too small"); return TT_ERR_WORKSPACE; }
+  return launch_sqnorm(xs, ns, 3, dt, out, static_cast<double*>(d_ws), as_cuda(stream));
 }
 
 }  // extern "C"

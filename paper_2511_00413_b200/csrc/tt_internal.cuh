@@ -73,7 +73,8 @@ tt_status launch_loss(const tt_packed& pk, const __nv_bfloat16* logits, int64_t 
                       const uint8_t* node_mask, int boundary_mode, float gamma, __nv_bfloat16* dlogits,
                       float* tok_loss, double* sums, int32_t* d_err, float* ws_loss, float* ws_omega,
                       cudaStream_t st);
-tt_status launch_sqnorm(const void* x, int64_t n, tt_dtype dt, double* out, double* partials, cudaStream_t st);
+tt_status launch_sqnorm(const void* const* xs, const int64_t* ns, int count, tt_dtype dt, double* out,
+                        double* partials, cudaStream_t st);
 
 constexpr int kSqnormBlocks = 296;
 

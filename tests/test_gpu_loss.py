@@ -109,7 +109,19 @@ def test_sqnorm(tt):
         out = tt.tt_grad_sqnorm(x.cuda())
         torch.cuda.synchronize()
         ref = float((to64(x) ** 2).sum())
-        assert abs(out.item() - ref) <= 1e-12 * max(ref, 1.0)
+        # fp32 sums of 8 exact squares per vector, fp64 across vectors (include/tt.h)
+        assert abs(out.item() - ref) <= 1e-6 * max(ref, 1.0)
         out2 = tt.tt_grad_sqnorm(x.cuda())
         torch.cuda.synchronize()
         assert out2.item() == out.item()  # deterministic
+
+
+def test_sqnorm3_matches_single(tt):
+    import torch
+    xs = [torch.randn(n, generator=torch.Generator().manual_seed(n)).to(torch.bfloat16).cuda()
+          for n in (4096 * 128, 333 * 128, 17)]
+    out = tt.tt_grad_sqnorm3(*xs)
+    singles = [tt.tt_grad_sqnorm(x) for x in xs]
+    torch.cuda.synchronize()
+    for k in range(3):
+        assert out[k].item() == singles[k].item()
