@@ -26,6 +26,8 @@ SO = os.path.join(HERE, "libtt.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-Xptxas", "-warn-spills", "-I", os.path.join(ROOT, "include")]
+if os.environ.get("TT_PROFILE_COUNTERS"):
+    FLAGS += ["-DTT_PROFILE_COUNTERS"]  # development cycle counters in the tensor-core kernels
 
 
 def nvcc() -> str:

@@ -35,6 +35,15 @@
 #include <cstdlib>
 
 #include "sm100_ptx.cuh"
+
+// Development cycle counters (per-role wait / compute time, read back with tt_debug_*_counters):
+// compiled in only with -DTT_PROFILE_COUNTERS; otherwise TT_CLK() is a constant and the bookkeeping
+// folds away.
+#ifdef TT_PROFILE_COUNTERS
+#define TT_CLK() clock64()
+#else
+#define TT_CLK() 0ll
+#endif
 #include "tt_internal.cuh"
 
 namespace tt {
@@ -109,6 +118,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   uint32_t* misc = reinterpret_cast<uint32_t*>(smem + kOffMisc);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long t_kernel0 = TT_CLK();
   const int kb = (int)(blockIdx.x / p.hkv);
   const int hk = (int)(blockIdx.x % p.hkv);
   const int64_t k0 = (int64_t)kb * 128;
@@ -205,7 +215,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           mma_ss_w(tm + kColP, sdesc(vb_s + offk, 16, 1024), sdesc(ob + offq, 16, 1024), idSP, kk > 0);
         }
       };
-      long long w_sm = 0, w_dq = 0, w_q = 0, t_start = clock64();
+      long long w_sm = 0, w_dq = 0, w_q = 0, t_start = TT_CLK();
       mbar_wait(kv_full, 0);
       // prologue: S(0), dP(0) -> s_full[0]; S(1)
       mbar_wait(&q_full[0], 0);
@@ -223,7 +233,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const uint32_t qb = qs0 + s * 2 * kQTile;
         const uint32_t ob = qb + kQTile;
         const uint32_t dsb = ds0 + b * kDSTile;
-        { long long t0 = clock64(); mbar_wait(&sm_done[b], (it >> 1) & 1); w_sm += clock64() - t0; }
+        { long long t0 = TT_CLK(); mbar_wait(&sm_done[b], (it >> 1) & 1); w_sm += TT_CLK() - t0; }
         tc_fence_after();
         // next tile's dP^T first (single buffer, free once softmax(it) has read it), so that
         // softmax(it+1) overlaps this tile's dV / dK / dQ products
@@ -243,7 +253,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                  (it > 0 || kk > 0) ? 1u : 0u);
         // dQ^T = K^T dS^T   (A: K MN-major, LBO = 16 KB d-chunk; B: dS^T MN-major, one 64-wide group)
         if (it > 0) {
-          { long long t0 = clock64(); mbar_wait(&dq_free[0], (it - 1) & 1); w_dq += clock64() - t0; }
+          { long long t0 = TT_CLK(); mbar_wait(&dq_free[0], (it - 1) & 1); w_dq += TT_CLK() - t0; }
           tc_fence_after();
         }
 #pragma unroll
@@ -253,14 +263,14 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         mma_commit_w(&dq_full[0]);
         mma_commit_w(&q_empty[s]);
         if (it + 2 < n_it) {
-          { long long t0 = clock64(); mbar_wait(&q_full[(it + 2) % kQStages], ((it + 2) / kQStages) & 1); w_q += clock64() - t0; }
+          { long long t0 = TT_CLK(); mbar_wait(&q_full[(it + 2) % kQStages], ((it + 2) / kQStages) & 1); w_q += TT_CLK() - t0; }
           tc_fence_after();
           issue_SP(it + 2);
         }
       }
       mma_commit_w(acc_done);
       if ((p.dbg & 8) && lane == 0) {
-        atomicAdd(&g_bwd_dbg[0], (unsigned long long)(clock64() - t_start));
+        atomicAdd(&g_bwd_dbg[0], (unsigned long long)(TT_CLK() - t_start));
         atomicAdd(&g_bwd_dbg[1], (unsigned long long)w_sm);
         atomicAdd(&g_bwd_dbg[2], (unsigned long long)w_dq);
         atomicAdd(&g_bwd_dbg[3], (unsigned long long)w_q);
@@ -284,7 +294,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     auto drain = [&](int it) {
       const int h = hk * p.g + it / nq;
       const int q0 = (qt0 + it % nq) * kBQ + 32 * wg;
-      { long long t0 = clock64(); mbar_wait(&dq_full[0], it & 1); c_wd += clock64() - t0; }
+      { long long t0 = TT_CLK(); mbar_wait(&dq_full[0], it & 1); c_wd += TT_CLK() - t0; }
       tc_fence_after();
       uint32_t v[32];
       tmem_ld32(tl + kColQ + 32 * wg, v);
@@ -310,9 +320,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     for (int it = 0; it < n_it; ++it) {
       const int s = it % kQStages, b = it & 1;
       const int q0 = (qt0 + it % nq) * kBQ;
-      { long long t0 = clock64(); mbar_wait(&s_full[b], (it >> 1) & 1); c_ws += clock64() - t0; }
+      { long long t0 = TT_CLK(); mbar_wait(&s_full[b], (it >> 1) & 1); c_ws += TT_CLK() - t0; }
       tc_fence_after();
-      long long t_el = clock64();
+      long long t_el = TT_CLK();
       if (p.dbg & 4) {
         tc_fence_before();
         mbar_arrive(&sm_done[b]);
@@ -326,12 +336,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const int lo = max(j - c0, 0), hi = min(min(Ej, Nn) - c0, 32);
         const uint32_t cmask = (hi <= lo) ? 0u : ((hi >= 32 ? 0xffffffffu : ((1u << hi) - 1u)) & ~((1u << lo) - 1u));
         uint32_t sv[32], pv[32];
-        long long tA = clock64();
+        long long tA = TT_CLK();
         tmem_ld32(tl + kColS + 64 * b + 32 * wg, sv);
         tmem_ld32(tl + kColP + 32 * wg, pv);
         tmem_wait_ld();
-        c_ld += clock64() - tA;
-        tA = clock64();
+        c_ld += TT_CLK() - tA;
+        tA = TT_CLK();
         uint32_t pwk[16], dsk[16];
         const bool all_in = __all_sync(0xffffffffu, cmask == 0xffffffffu);
         const float2 SL = make_float2(sl2, sl2);
@@ -362,8 +372,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           dsk[2 * c4] = pack_bf16(ds01.x, ds01.y);
           dsk[2 * c4 + 1] = pack_bf16(ds23.x, ds23.y);
         }
-        c_math += clock64() - tA;
-        tA = clock64();
+        c_math += TT_CLK() - tA;
+        tA = TT_CLK();
         // P^T (bf16) over this warpgroup's own S^T[b] columns: [32 wg, 32 wg + 16) — never over
         // columns the other warpgroup may still be reading
         tmem_st16(tl + kColS + 64 * b + 32 * wg, pwk);
@@ -379,12 +389,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         fence_proxy_async_smem();
         tc_fence_before();
         mbar_arrive(&sm_done[b]);
-        c_st += clock64() - tA;
+        c_st += TT_CLK() - tA;
       }
-      c_el += clock64() - t_el;
-      long long t_dr = clock64();
+      c_el += TT_CLK() - t_el;
+      long long t_dr = TT_CLK();
       if (it > 0) drain(it - 1);
-      c_dr += clock64() - t_dr;
+      c_dr += TT_CLK() - t_dr;
     }
     drain(n_it - 1);
     if (r == 0) bulk_wait<0>();
@@ -426,6 +436,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
+  }
+  if ((p.dbg & 8) && threadIdx.x == 0) {
+    atomicAdd(&g_bwd_dbg[12], (unsigned long long)(TT_CLK() - t_kernel0));
+    atomicAdd(&g_bwd_dbg[13], 1ull);
   }
 }
 

@@ -24,6 +24,15 @@
 #include <cstdlib>
 
 #include "sm100_ptx.cuh"
+
+// Development cycle counters (per-role wait / compute time, read back with tt_debug_*_counters):
+// compiled in only with -DTT_PROFILE_COUNTERS; otherwise TT_CLK() is a constant and the bookkeeping
+// folds away.
+#ifdef TT_PROFILE_COUNTERS
+#define TT_CLK() clock64()
+#else
+#define TT_CLK() 0ll
+#endif
 #include "tt_internal.cuh"
 
 namespace tt {
@@ -172,7 +181,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       };
       uint32_t pph[2] = {0, 0};
       bool first[2] = {true, true};
-      long long w_p = 0, w_kv = 0, t_beg = clock64();
+      long long w_p = 0, w_kv = 0, t_beg = TT_CLK();
       mbar_wait(bar_q, 0);
       if (T > 0) {
         mbar_wait(&full[0], 0);
@@ -188,7 +197,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
           if (tile_cls(tiles[t], i)) {
-            { long long t0 = clock64(); mbar_wait(&p_full[i], pph[i]); w_p += clock64() - t0; }
+            { long long t0 = TT_CLK(); mbar_wait(&p_full[i], pph[i]); w_p += TT_CLK() - t0; }
             pph[i] ^= 1;
             tc_fence_after();
 #pragma unroll
@@ -200,7 +209,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           }
           if (t + 1 < T && tile_cls(tiles[t + 1], i)) {
             if (!waited) {
-              { long long t0 = clock64(); mbar_wait(&full[(t + 1) % kStages], ((t + 1) / kStages) & 1); w_kv += clock64() - t0; }
+              { long long t0 = TT_CLK(); mbar_wait(&full[(t + 1) % kStages], ((t + 1) / kStages) & 1); w_kv += TT_CLK() - t0; }
               tc_fence_after();
               waited = true;
             }
@@ -210,7 +219,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         mma_commit_w(&empty[s]);
       }
       if ((p.dbg & 8) && lane == 0) {
-        atomicAdd(&g_fwd_dbg[0], (unsigned long long)(clock64() - t_beg));
+        atomicAdd(&g_fwd_dbg[0], (unsigned long long)(TT_CLK() - t_beg));
         atomicAdd(&g_fwd_dbg[1], (unsigned long long)w_p);
         atomicAdd(&g_fwd_dbg[2], (unsigned long long)w_kv);
         atomicAdd(&g_fwd_dbg[3], (unsigned long long)T);
@@ -237,8 +246,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         if (!cls) continue;
         const int kb = e & kKbMask;
         const int64_t j0 = (int64_t)kb * 128;
-        { long long t0 = clock64(); mbar_wait(&s_full[i], sph); c_ws += clock64() - t0; }
-        long long t_cmp = clock64();
+        { long long t0 = TT_CLK(); mbar_wait(&s_full[i], sph); c_ws += TT_CLK() - t0; }
+        long long t_cmp = TT_CLK();
         sph ^= 1;
         tc_fence_after();
         uint32_t s[128];
@@ -247,12 +256,14 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         tmem_ld32(tS + 64, *reinterpret_cast<uint32_t(*)[32]>(&s[64]));
         tmem_ld32(tS + 96, *reinterpret_cast<uint32_t(*)[32]>(&s[96]));
         tmem_wait_ld();
-        c_ld += clock64() - t_cmp;
-        long long t_m = clock64();
+        c_ld += TT_CLK() - t_cmp;
+        long long t_m = TT_CLK();
         // ---- mask (partial tiles, and key columns past N on the ragged last block) ----
         if (cls == kClsPartial) {
+          // int32 index math (N < 2^31): key c is allowed iff c <= row - j0, c < N - j0, row < E_c
           const int4* Es = reinterpret_cast<const int4*>(smem + kOffE + (t % kStages) * 512);
-          const int64_t jmax = p.N - j0;  // keys c >= jmax do not exist
+          const int cmax = min((int)(row - j0), (int)(p.N - j0) - 1);  // last allowed column by position
+          const int irow = (int)row;
 #pragma unroll
           for (int c4 = 0; c4 < 32; ++c4) {
             const int4 ev = Es[c4];
@@ -260,12 +271,12 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
               const int c = 4 * c4 + u;
-              const bool ok = (c < jmax) && (j0 + c <= row) && (row < (int64_t)ee[u]);
+              const bool ok = (c <= cmax) && (irow < ee[u]);
               if (!ok) s[c] = __float_as_uint(-INFINITY);
             }
           }
         } else if (j0 + 128 > p.N) {
-          const int64_t jmax = p.N - j0;
+          const int jmax = (int)(p.N - j0);
 #pragma unroll
           for (int c = 0; c < 128; ++c)
             if (c >= jmax) s[c] = __float_as_uint(-INFINITY);
@@ -332,15 +343,15 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             tmem_st32(tO + 32 * cc, ov);
           }
         }
-        c_math += clock64() - t_m;
-        long long t_st = clock64();
+        c_math += TT_CLK() - t_m;
+        long long t_st = TT_CLK();
         tmem_st32(tS + 0, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
         tmem_st32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
         tmem_wait_st();
         tc_fence_before();
         mbar_arrive(&p_full[i]);
-        c_stt += clock64() - t_st;
-        c_cmp += clock64() - t_cmp;
+        c_stt += TT_CLK() - t_st;
+        c_cmp += TT_CLK() - t_cmp;
         ++c_n;
         first = false;
       }
