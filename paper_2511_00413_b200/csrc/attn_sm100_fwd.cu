@@ -12,9 +12,9 @@
 //   warp 1      TMEM allocator (512 columns: S0 | S1 | O0 | O1) and MMA issuer (one thread):
 //               S_i = Q_i K^T (SS, M=N=128, K=128) into TMEM, then O_i += P_i V with P_i read from
 //               TMEM (TS) — FA4-style order PV_0, S_0', PV_1, S_1'
-//   warps 2-5   softmax of query tile 0 (one thread per row: tcgen05.ld 32x32b gives each thread
-//   warps 6-9   softmax of query tile 1  its row, so row max / row sum are thread-local; the TMEM
-//               lane quadrant of a warp is warp % 4)
+//   warps 2-17  softmax: 2 query tiles x 2 column halves x 4 warps.  One thread per (row, half):
+//               tcgen05.ld 32x32b gives each thread its row (TMEM lane quadrant = warp % 4), so row
+//               max / sum are thread-local within a half; the halves exchange maxima through smem.
 // Softmax keeps the running max in log2 units and only rescales the O accumulator in TMEM when
 // the max grows by more than 2^8 (stale-max trick; exact after the final 1/l).  P (bf16) is
 // written back over S in TMEM and consumed by the TS MMA; the epilogue divides by l and stores
@@ -41,7 +41,7 @@ using namespace sm100;
 
 constexpr int kD = 128;
 constexpr int kStages = 2;
-constexpr int kFwdThreads = 320;  // 10 warps: producer, MMA, 2 x 4 softmax warps
+constexpr int kFwdThreads = 576;  // 18 warps: producer, MMA, 2 query tiles x 2 column halves x 4 softmax warps
 constexpr uint32_t kTileBytes = 128 * kD * 2;  // 32 KB: two 16 KB SWIZZLE_128B chunks (d 0-63 | 64-127)
 constexpr uint32_t kChunkBytes = 128 * 64 * 2;
 constexpr uint32_t kOffQ = 0;                       // Q0, Q1
@@ -50,7 +50,8 @@ constexpr uint32_t kOffE = kOffKV + kStages * 2 * kTileBytes;  // E of the stage
 constexpr uint32_t kOffBar = kOffE + kStages * 512;
 constexpr uint32_t kNumBars = 1 + 2 * kStages + 6;
 constexpr uint32_t kOffMisc = kOffBar + kNumBars * 8;
-constexpr uint32_t kOffTiles = kOffMisc + 16;
+constexpr uint32_t kOffX = kOffMisc + 16;           // row-max exchange [2 parity][2 tiles][2 halves][128] + l [2][2][128]
+constexpr uint32_t kOffTiles = kOffX + (2 * 2 * 2 * 128 + 2 * 2 * 128) * 4;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 
 __device__ unsigned long long g_fwd_dbg[16];  // development instrumentation (TT_DEBUG_FWD & 8)
@@ -124,7 +125,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     if (lane == 0) {
       mbar_init(bar_q, 1);
       for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-      for (int i = 0; i < 2; ++i) { mbar_init(&s_full[i], 1); mbar_init(&p_full[i], 128); mbar_init(&o_full[i], 1); }
+      for (int i = 0; i < 2; ++i) { mbar_init(&s_full[i], 1); mbar_init(&p_full[i], 256); mbar_init(&o_full[i], 1); }
       mbar_fence_init();
     }
     __syncwarp();
@@ -202,7 +203,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             tc_fence_after();
 #pragma unroll
             for (int kk = 0; kk < 8; ++kk)
-              mma_ts_w(tm + 256 + 128 * i, tm + 128 * i + kk * 8, sdesc(vbase + kk * 2048, kChunkBytes, 1024), idO,
+              // P of keys [16 kk, 16 kk + 16): packed by column half kk / 4 at S column 64 (kk / 4) + 8 (kk % 4)
+              mma_ts_w(tm + 256 + 128 * i, tm + 128 * i + 8 * kk + ((kk >> 2) << 5), sdesc(vbase + kk * 2048, kChunkBytes, 1024), idO,
                      (!first[i] || kk > 0) ? 1u : 0u);
             first[i] = false;
             if (t == last[i]) mma_commit_w(&o_full[i]);
@@ -226,144 +228,144 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       }
     }
   } else {
-    // ===================== softmax warpgroups =====================
-    const int i = (warp - 2) >> 2;  // query tile
-    const int q = warp & 3;         // TMEM lane quadrant
+    // ===================== softmax: 2 query tiles x 2 column halves =====================
+    // Warpgroup (i, hf) owns rows of query tile i (one thread per row: its TMEM lane) and key columns
+    // [64 hf, 64 hf + 64) of every k-tile.  The two halves exchange their row maxima through shared
+    // memory (one named barrier per tile), keep separate partial row sums (same running max), rescale
+    // their own half of O, and pack P (bf16) over their OWN S columns so neither half can overwrite
+    // scores the other has not read yet.
+    const int i = (warp - 2) >> 3;           // query tile
+    const int hf = ((warp - 2) >> 2) & 1;    // column half
+    const int q = warp & 3;                  // TMEM lane quadrant
     const int r = q * 32 + lane;
     const int64_t row = (int64_t)(qa + i) * 128 + r;
     const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
-    const uint32_t tS = tl + 128 * i;
-    const uint32_t tO = tl + 256 + 128 * i;
+    const uint32_t tSh = tl + 128 * i + 64 * hf;        // this half's S columns (P packed at [tSh, tSh + 32))
+    const uint32_t tOh = tl + 256 + 128 * i + 64 * hf;  // this half's O columns
+    float* xmax = reinterpret_cast<float*>(smem + kOffX);  // [parity][tile][half][row]
+    float* xl = xmax + 2 * 2 * 2 * 128;                    // [tile][half][row]
     const float sl2 = p.scale_log2;
     float m = -INFINITY, l = 0.f;
-    uint32_t sph = 0;
+    uint32_t sph = 0, par = 0;
     bool first = true;
-    long long c_ws = 0, c_cmp = 0, c_n = 0, c_ld = 0, c_math = 0, c_stt = 0;
     if (i == 0 || has1) {
       for (int t = 0; t < T; ++t) {
         const int32_t e = tiles[t];
         const int cls = tile_cls(e, i);
         if (!cls) continue;
         const int kb = e & kKbMask;
-        const int64_t j0 = (int64_t)kb * 128;
-        { long long t0 = TT_CLK(); mbar_wait(&s_full[i], sph); c_ws += TT_CLK() - t0; }
-        long long t_cmp = TT_CLK();
+        const int64_t j0 = (int64_t)kb * 128 + 64 * hf;  // first key of this half
+        mbar_wait(&s_full[i], sph);
         sph ^= 1;
         tc_fence_after();
-        uint32_t s[128];
-        tmem_ld32(tS + 0, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
-        tmem_ld32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
-        tmem_ld32(tS + 64, *reinterpret_cast<uint32_t(*)[32]>(&s[64]));
-        tmem_ld32(tS + 96, *reinterpret_cast<uint32_t(*)[32]>(&s[96]));
+        uint32_t s[64];
+        tmem_ld32(tSh, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
+        tmem_ld32(tSh + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
         tmem_wait_ld();
-        c_ld += TT_CLK() - t_cmp;
-        long long t_m = TT_CLK();
-        // ---- mask (partial tiles, and key columns past N on the ragged last block) ----
+        // ---- mask (partial tiles; key columns past N on the ragged last block) ----
+        const bool ragged = j0 + 64 > p.N;
         if (cls == kClsPartial) {
-          // int32 index math (N < 2^31): key c is allowed iff c <= row - j0, c < N - j0, row < E_c
-          const int4* Es = reinterpret_cast<const int4*>(smem + kOffE + (t % kStages) * 512);
-          const int cmax = min((int)(row - j0), (int)(p.N - j0) - 1);  // last allowed column by position
+          // int32 index math (N < 2^31): key c allowed iff c <= row - j0, c < N - j0, row < E_c
+          const int4* Es = reinterpret_cast<const int4*>(smem + kOffE + (t % kStages) * 512) + 16 * hf;
+          const int cmax = min((int)(row - j0), (int)(p.N - j0) - 1);
           const int irow = (int)row;
 #pragma unroll
-          for (int c4 = 0; c4 < 32; ++c4) {
+          for (int c4 = 0; c4 < 16; ++c4) {
             const int4 ev = Es[c4];
             const int ee[4] = {ev.x, ev.y, ev.z, ev.w};
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
               const int c = 4 * c4 + u;
-              const bool ok = (c <= cmax) && (irow < ee[u]);
-              if (!ok) s[c] = __float_as_uint(-INFINITY);
+              if (!((c <= cmax) && (irow < ee[u]))) s[c] = __float_as_uint(-INFINITY);
             }
           }
-        } else if (j0 + 128 > p.N) {
+        } else if (ragged) {
           const int jmax = (int)(p.N - j0);
 #pragma unroll
-          for (int c = 0; c < 128; ++c)
+          for (int c = 0; c < 64; ++c)
             if (c >= jmax) s[c] = __float_as_uint(-INFINITY);
         }
-        // ---- row max (log2 units): 8 independent partial maxima, then a tree ----
-        float pm[8];
+        // ---- row max: 4 partial maxima, exchange with the other half ----
+        float pm[4];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) pm[u] = __uint_as_float(s[u]);
+        for (int u = 0; u < 4; ++u) pm[u] = __uint_as_float(s[u]);
 #pragma unroll
-        for (int c = 8; c < 128; c += 8)
+        for (int c = 4; c < 64; c += 4)
 #pragma unroll
-          for (int u = 0; u < 8; ++u) pm[u] = fmaxf(pm[u], __uint_as_float(s[c + u]));
-        const float mx = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])), fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7])));
+          for (int u = 0; u < 4; ++u) pm[u] = fmaxf(pm[u], __uint_as_float(s[c + u]));
+        const float hmax = fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3]));
+        xmax[((par * 2 + i) * 2 + hf) * 128 + r] = hmax;
+        named_bar_sync(1 + i, 256);
+        const float mx = fmaxf(hmax, xmax[((par * 2 + i) * 2 + (hf ^ 1)) * 128 + r]);
+        par ^= 1;
         const float m_new = fmaxf(m, mx * sl2);
         const bool resc = (m == -INFINITY) ? (m_new != -INFINITY) : (m_new > m + kRescaleThreshold);
         const float m_use = resc ? m_new : m;
         const float corr = (m == -INFINITY) ? 0.f : ex2(m - m_use);
         const float mb = (m_use == -INFINITY) ? 0.f : m_use;
-        // ---- P = exp2(s * scale_log2 - m), packed bf16 in place (s[0..63]) ----
-        // packed f32x2 FMAs; on tiles without any mask half of the exponentials run as a
-        // polynomial on the FMA pipe (FA4-style) to relieve the MUFU unit
+        // ---- P = exp2(s * scale_log2 - m): packed f32x2 FMAs; on unmasked tiles half of the
+        //      exponentials run as a polynomial on the FMA pipe (FA4-style) ----
         const float2 SL = make_float2(sl2, sl2), NM = make_float2(-mb, -mb);
-        float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f), acc2 = make_float2(0.f, 0.f),
-               acc3 = make_float2(0.f, 0.f);
-        if (cls == kClsFull && j0 + 128 <= p.N) {
+        float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
+        if (cls == kClsFull && !ragged) {
 #pragma unroll
-          for (int c = 0; c < 128; c += 4) {
+          for (int c = 0; c < 64; c += 4) {
             const float2 a01 = ffma2(make_float2(__uint_as_float(s[c]), __uint_as_float(s[c + 1])), SL, NM);
             const float2 a23 = ffma2(make_float2(__uint_as_float(s[c + 2]), __uint_as_float(s[c + 3])), SL, NM);
             const float2 p01 = make_float2(ex2(a01.x), ex2(a01.y));
             const float2 p23 = exp2_poly2(a23);
-            if (c & 4) { acc2 = fadd2(acc2, p01); acc3 = fadd2(acc3, p23); }
-            else { acc0 = fadd2(acc0, p01); acc1 = fadd2(acc1, p23); }
+            acc0 = fadd2(acc0, p01);
+            acc1 = fadd2(acc1, p23);
             s[c >> 1] = pack_bf16(p01.x, p01.y);
             s[(c >> 1) + 1] = pack_bf16(p23.x, p23.y);
           }
         } else {
 #pragma unroll
-          for (int c = 0; c < 128; c += 4) {
+          for (int c = 0; c < 64; c += 4) {
             const float2 a01 = ffma2(make_float2(__uint_as_float(s[c]), __uint_as_float(s[c + 1])), SL, NM);
             const float2 a23 = ffma2(make_float2(__uint_as_float(s[c + 2]), __uint_as_float(s[c + 3])), SL, NM);
             const float2 p01 = make_float2(ex2(a01.x), ex2(a01.y));
             const float2 p23 = make_float2(ex2(a23.x), ex2(a23.y));
-            if (c & 4) { acc2 = fadd2(acc2, p01); acc3 = fadd2(acc3, p23); }
-            else { acc0 = fadd2(acc0, p01); acc1 = fadd2(acc1, p23); }
+            acc0 = fadd2(acc0, p01);
+            acc1 = fadd2(acc1, p23);
             s[c >> 1] = pack_bf16(p01.x, p01.y);
             s[(c >> 1) + 1] = pack_bf16(p23.x, p23.y);
           }
         }
-        const float2 accs = fadd2(fadd2(acc0, acc1), fadd2(acc2, acc3));
-        const float lsum0 = accs.x, lsum1 = accs.y;
-        l = l * corr + (lsum0 + lsum1);
+        const float2 accs = fadd2(acc0, acc1);
+        l = l * corr + (accs.x + accs.y);
         m = m_use;
-        // ---- lazy rescale of the O accumulator (PV of the previous tile has completed: its
-        //      commit precedes the s_full arrival we waited on) ----
+        // ---- lazy rescale of this half of O (PV of the previous tile has completed: its commit
+        //      precedes the s_full arrival we waited on) ----
         if (!first && __any_sync(0xffffffffu, resc)) {
 #pragma unroll 1
-          for (int cc = 0; cc < 4; ++cc) {
+          for (int cc = 0; cc < 2; ++cc) {
             uint32_t ov[32];
-            tmem_ld32(tO + 32 * cc, ov);
+            tmem_ld32(tOh + 32 * cc, ov);
             tmem_wait_ld();
 #pragma unroll
             for (int u = 0; u < 32; ++u) ov[u] = __float_as_uint(__uint_as_float(ov[u]) * corr);
-            tmem_st32(tO + 32 * cc, ov);
+            tmem_st32(tOh + 32 * cc, ov);
           }
         }
-        c_math += TT_CLK() - t_m;
-        long long t_st = TT_CLK();
-        tmem_st32(tS + 0, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
-        tmem_st32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
+        tmem_st32(tSh, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
         tmem_wait_st();
         tc_fence_before();
         mbar_arrive(&p_full[i]);
-        c_stt += TT_CLK() - t_st;
-        c_cmp += TT_CLK() - t_cmp;
-        ++c_n;
         first = false;
       }
-      // ---- epilogue: O / l -> bf16, LSE ----
+      // ---- epilogue: O / l -> bf16 (this half's 64 columns), LSE (half 0) ----
       mbar_wait(&o_full[i], 0);
       tc_fence_after();
-      const float inv = (l > 0.f) ? 1.f / l : 0.f;
-      __nv_bfloat16* orow = p.o + (row * p.hq + h) * kD;
+      xl[(i * 2 + hf) * 128 + r] = l;
+      named_bar_sync(1 + i, 256);
+      const float lt = xl[(i * 2) * 128 + r] + xl[(i * 2 + 1) * 128 + r];
+      const float inv = (lt > 0.f) ? 1.f / lt : 0.f;
+      __nv_bfloat16* orow = p.o + (row * p.hq + h) * kD + 64 * hf;
 #pragma unroll 1
-      for (int cc = 0; cc < 4; ++cc) {
+      for (int cc = 0; cc < 2; ++cc) {
         uint32_t ov[32];
-        tmem_ld32(tO + 32 * cc, ov);
+        tmem_ld32(tOh + 32 * cc, ov);
         tmem_wait_ld();
         if (row < p.N) {
           uint32_t pk[16];
@@ -375,15 +377,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           for (int u = 0; u < 4; ++u) dst[u] = make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
         }
       }
-      if (row < p.N) p.lse[(int64_t)h * p.N + row] = (m + __log2f(l)) * kLn2;
-      if ((p.dbg & 8) && r == 0 && i == 0) {
-        atomicAdd(&g_fwd_dbg[4], (unsigned long long)c_ws);
-        atomicAdd(&g_fwd_dbg[5], (unsigned long long)c_cmp);
-        atomicAdd(&g_fwd_dbg[6], (unsigned long long)c_n);
-        atomicAdd(&g_fwd_dbg[7], (unsigned long long)c_ld);
-        atomicAdd(&g_fwd_dbg[8], (unsigned long long)c_math);
-        atomicAdd(&g_fwd_dbg[9], (unsigned long long)c_stt);
-      }
+      if (hf == 0 && row < p.N) p.lse[(int64_t)h * p.N + row] = (m + __log2f(lt)) * kLn2;
     }
   }
   tc_fence_before();
