@@ -356,7 +356,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           const float2 a01 = ffma2(make_float2(__uint_as_float(sv[c]), __uint_as_float(sv[c + 1])), SL, make_float2(NL.x, NL.y));
           const float2 a23 = ffma2(make_float2(__uint_as_float(sv[c + 2]), __uint_as_float(sv[c + 3])), SL, make_float2(NL.z, NL.w));
           float2 p01 = make_float2(ex2(a01.x), ex2(a01.y));
-          float2 p23 = exp2_poly2(a23);
+#ifndef TT_BWD_POLY
+#define TT_BWD_POLY 1
+#endif
+          // 2 x TT_BWD_POLY of every 8 exponentials run on the FMA pipe
+          float2 p23 = (TT_BWD_POLY == 2 || (TT_BWD_POLY == 1 && (c4 & 1))) ? exp2_poly2(a23)
+                                                                           : make_float2(ex2(a23.x), ex2(a23.y));
           if (!all_in) {
             p01.x = ((cmask >> c) & 1u) ? p01.x : 0.f;
             p01.y = ((cmask >> (c + 1)) & 1u) ? p01.y : 0.f;

@@ -248,6 +248,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     float m = -INFINITY, l = 0.f;
     uint32_t sph = 0, par = 0;
     bool first = true;
+    long long c_ws = 0, c_cmp = 0, c_n = 0, c_bar = 0;
     if (i == 0 || has1) {
       for (int t = 0; t < T; ++t) {
         const int32_t e = tiles[t];
@@ -255,9 +256,15 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         if (!cls) continue;
         const int kb = e & kKbMask;
         const int64_t j0 = (int64_t)kb * 128 + 64 * hf;  // first key of this half
-        mbar_wait(&s_full[i], sph);
+        { const long long t0 = TT_CLK(); mbar_wait(&s_full[i], sph); c_ws += TT_CLK() - t0; }
+        const long long t_cmp = TT_CLK();
         sph ^= 1;
         tc_fence_after();
+        if (p.dbg & 32) {  // development ablation: no softmax work (MMA pipeline alone)
+          tc_fence_before();
+          mbar_arrive(&p_full[i]);
+          continue;
+        }
         uint32_t s[64];
         tmem_ld32(tSh, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
         tmem_ld32(tSh + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
@@ -295,7 +302,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           for (int u = 0; u < 4; ++u) pm[u] = fmaxf(pm[u], __uint_as_float(s[c + u]));
         const float hmax = fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3]));
         xmax[((par * 2 + i) * 2 + hf) * 128 + r] = hmax;
-        named_bar_sync(1 + i, 256);
+        { const long long tb = TT_CLK(); named_bar_sync(1 + i, 256); c_bar += TT_CLK() - tb; }
         const float mx = fmaxf(hmax, xmax[((par * 2 + i) * 2 + (hf ^ 1)) * 128 + r]);
         par ^= 1;
         const float m_new = fmaxf(m, mx * sl2);
@@ -313,7 +320,13 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             const float2 a01 = ffma2(make_float2(__uint_as_float(s[c]), __uint_as_float(s[c + 1])), SL, NM);
             const float2 a23 = ffma2(make_float2(__uint_as_float(s[c + 2]), __uint_as_float(s[c + 3])), SL, NM);
             const float2 p01 = make_float2(ex2(a01.x), ex2(a01.y));
-            const float2 p23 = exp2_poly2(a23);
+#ifndef TT_FWD_POLY
+#define TT_FWD_POLY 1
+#endif
+            // 2 x TT_FWD_POLY of every 8 exponentials run on the FMA pipe (measured best: 1, i.e. 25%;
+            // the polynomial costs ~8 FMA-pipe cycles per element vs 8 MUFU cycles per exp)
+            const float2 p23 = (TT_FWD_POLY == 2 || (TT_FWD_POLY == 1 && (c & 4))) ? exp2_poly2(a23)
+                                                                                   : make_float2(ex2(a23.x), ex2(a23.y));
             acc0 = fadd2(acc0, p01);
             acc1 = fadd2(acc1, p23);
             s[c >> 1] = pack_bf16(p01.x, p01.y);
@@ -352,6 +365,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         tmem_wait_st();
         tc_fence_before();
         mbar_arrive(&p_full[i]);
+        c_cmp += TT_CLK() - t_cmp;
+        ++c_n;
         first = false;
       }
       // ---- epilogue: O / l -> bf16 (this half's 64 columns), LSE (half 0) ----
@@ -378,6 +393,12 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         }
       }
       if (hf == 0 && row < p.N) p.lse[(int64_t)h * p.N + row] = (m + __log2f(lt)) * kLn2;
+      if ((p.dbg & 8) && r == 0 && i == 0 && hf == 0) {
+        atomicAdd(&g_fwd_dbg[4], (unsigned long long)c_ws);
+        atomicAdd(&g_fwd_dbg[5], (unsigned long long)c_cmp);
+        atomicAdd(&g_fwd_dbg[6], (unsigned long long)c_n);
+        atomicAdd(&g_fwd_dbg[7], (unsigned long long)c_bar);
+      }
     }
   }
   tc_fence_before();

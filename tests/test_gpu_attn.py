@@ -130,7 +130,7 @@ def test_branch_invariance_on_gpu(tt):
     assert max_abs(lsel.cpu(), lse[:, ii]) <= 1e-3
 
 
-@pytest.mark.parametrize("cfg,seed", [("agentic8k", 0), ("wide", None)])
+@pytest.mark.parametrize("cfg,seed", [("agentic8k", 0), ("wide", None), ("deep32k", 1), ("batch64k", 0)])
 def test_full_size_sampled_rows(tt, cfg, seed):
     """BASELINE configs at full size and the bench launch configuration; the oracle evaluates a
     sample of query rows (O, LSE, dQ) and of keys (dK, dV) one by one."""
@@ -142,14 +142,15 @@ def test_full_size_sampled_rows(tt, cfg, seed):
     opk = oracle.pack(t.parent, t.length)
     N = opk["n_tokens"]
     rng = np.random.default_rng(0)
+    big = N > 20000
     want = np.zeros(N, np.uint8)
-    want[rng.choice(N, 48, replace=False)] = 1
+    want[rng.choice(N, 24 if big else 48, replace=False)] = 1
     want[[0, N - 1]] = 1
-    # keys: leaf-level keys have short query ranges; plus a few random keys if cheap
+    # keys: leaf-level keys have short query ranges (cheap for the per-branch oracle)
     span = opk["E"] - np.arange(N)
-    cand = np.flatnonzero(span <= 400)
+    cand = np.flatnonzero(span <= (160 if big else 400))
     wk = np.zeros(N, np.uint8)
-    wk[rng.choice(cand, min(24, len(cand)), replace=False)] = 1
+    wk[rng.choice(cand, min(8 if big else 24, len(cand)), replace=False)] = 1
     oo, olse = oracle.attn_fwd(opk, q, k, v, scale, want=want, check_invariant=False)
     m = want.astype(bool)
     assert max_abs(o[m], oo[m]) <= TOL_O_BF16

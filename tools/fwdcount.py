@@ -13,5 +13,5 @@ for cfg, seed in [("agentic8k", 0), ("deep32k", 1)]:
     tt.tt_attn_fwd(pk, q, k, v); torch.cuda.synchronize(); L.tt_debug_fwd_counters(buf, 1)
     b = list(buf); T = b[3]; n = b[6]
     n = max(n, 1)
-    print(cfg, "merged tiles", T, "per-tile cycles: mma_total %.0f wait_p %.0f wait_kv %.0f | softmax(wg0,r0) tiles %d: wait_s %.0f compute %.0f [ld %.0f math %.0f st %.0f]" %
-          (b[0] / T, b[1] / T, b[2] / T, n, b[4] / n, b[5] / n, b[7] / n, b[8] / n, b[9] / n), flush=True)
+    print(cfg, "merged tiles", T, "per-tile cycles: mma_total %.0f wait_p %.0f wait_kv %.0f | softmax(tile0,half0,r0) tiles %d: wait_s %.0f compute %.0f (of which max-exchange barrier %.0f)" %
+          (b[0] / T, b[1] / T, b[2] / T, n, b[4] / n, b[5] / n, b[7] / n), flush=True)

@@ -14,7 +14,9 @@ KEYS = {
     "dram_write": "dram__bytes_write.sum",
     "dram_pct": "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
     "tensor_pipe_pct": "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
-    "bf16_mma_ops_pct": "sm__ops_path_tensor_op_hmma_src_bf16_dst_fp32_sparsity_off.avg.pct_of_peak_sustained_elapsed",
+    "bf16_mma_ops_pct": "sm__ops_path_tensor_op_utchmma_src_bf16_dst_fp32_sparsity_off.avg.pct_of_peak_sustained_elapsed",
+    "mem_tensor_pct": "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+    "l1tex_throughput_pct": "l1tex__throughput.avg.pct_of_peak_sustained_elapsed",
     "xu_pipe_pct_active": "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
     "sm_throughput_pct": "sm__throughput.avg.pct_of_peak_sustained_elapsed",
     "shared_pipe_pct": "sm__pipe_shared_cycles_active.avg.pct_of_peak_sustained_active",
