@@ -210,6 +210,37 @@ tt_status tt_grad_sqnorm(const void* x, int64_t n, tt_dtype dt, double* out, voi
 tt_status tt_grad_sqnorm3(const void* x0, int64_t n0, const void* x1, int64_t n1, const void* x2, int64_t n2,
                           tt_dtype dt, double* out, void* d_ws, size_t ws_bytes, tt_stream_t stream);
 
+/* --------------------------------------------------------------------------------------
+ * Capacity-constrained Tree Packing.  HOST only, synchronous.
+ *
+ * Splits the trajectories of a tree/forest (same parent/len/term input as tt_pack) into traversals
+ * (training steps) whose induced sub-forest holds at most `capacity` tokens (Eq. 3
+ * generalised to multi-path traversals), with the heuristic of P:303-306 (reading R19 in DESIGN.md:
+ * DFS with children in descending order of their deepest trajectory end, a new traversal whenever
+ * the next trajectory's uncovered tokens would exceed the capacity).
+ * Trajectories are numbered in canonical order: DFS pre-order (roots / children ascending id) of
+ * their end nodes, term(u) consecutive copies.  traversal_of_traj [n_traj] (nullable for sizing)
+ * receives each trajectory's traversal id.  TT_ERR_TOO_LARGE if one trajectory exceeds capacity.
+ * tt_traversal_forest writes the sub-forest induced by one traversal (node ids keep their relative
+ * order; out_term counts the traversal's trajectories ending at each node, so tt_pack on it yields
+ * the in-traversal tree-scale) into caller arrays of n_nodes entries; out_node maps new ids
+ * to original ids.
+ * -------------------------------------------------------------------------------------- */
+typedef struct {
+  int32_t n_traj;
+  int32_t n_traversals;
+  int64_t capacity;
+  int64_t linear_tokens;  /* sum over trajectories of their path length (per-branch packing)   */
+  int64_t tree_tokens;    /* tokens on at least one trajectory (whole tree in one step)        */
+  int64_t planned_tokens; /* sum over traversals of their induced sub-forest tokens            */
+} tt_plan_info;
+
+tt_status tt_plan_traversals(const int32_t* parent, const int32_t* len, const int32_t* term, int32_t n_nodes,
+                             int64_t capacity, int32_t* traversal_of_traj, tt_plan_info* info);
+tt_status tt_traversal_forest(const int32_t* parent, const int32_t* len, const int32_t* term, int32_t n_nodes,
+                              const int32_t* traversal_of_traj, int32_t traversal, int32_t* out_parent,
+                              int32_t* out_len, int32_t* out_term, int32_t* out_node, int32_t* n_out);
+
 /* Kernel-level launch counters (for bench.py's gpu_launches claim): number of kernels this
  * thread has launched through the library since the last reset. */
 int64_t tt_launch_count(void);

@@ -41,6 +41,11 @@ _PTR_FIELDS = ["pos", "w", "E", "node", "node_start", "node_len", "node_sub_end"
                "succ_ptr", "succ_tok", "kblk_minE", "kblk_maxE", "fwd_cnt", "fwd_list"]
 
 
+class TTPlanInfo(C.Structure):
+    _fields_ = [("n_traj", C.c_int32), ("n_traversals", C.c_int32), ("capacity", C.c_int64),
+                ("linear_tokens", C.c_int64), ("tree_tokens", C.c_int64), ("planned_tokens", C.c_int64)]
+
+
 class TTPacked(C.Structure):
     _fields_ = [(f, C.c_void_p) for f in _PTR_FIELDS] + [
         ("n_tokens", C.c_int64), ("n_nodes", C.c_int32), ("n_blk", C.c_int32), ("n_succ", C.c_int32),
@@ -85,12 +90,15 @@ def lib():
             L.tt_grad_sqnorm_workspace.argtypes = [C.c_int64]
             L.tt_grad_sqnorm.argtypes = [vp, C.c_int64, C.c_int, vp, vp, sz, st]
             L.tt_grad_sqnorm3.argtypes = [vp, C.c_int64, vp, C.c_int64, vp, C.c_int64, C.c_int, vp, vp, sz, st]
+            L.tt_plan_traversals.argtypes = [i32p, i32p, i32p, C.c_int32, C.c_int64, i32p, C.POINTER(TTPlanInfo)]
+            L.tt_traversal_forest.argtypes = [i32p, i32p, i32p, C.c_int32, i32p, C.c_int32, i32p, i32p, i32p, i32p, i32p]
             L.tt_launch_count.restype = C.c_int64
             L.tt_launch_count.argtypes = []
             L.tt_launch_count_reset.argtypes = []
             L.tt_launch_count_reset.restype = None
             for fn in ("tt_pack_plan", "tt_pack", "tt_attn_fwd", "tt_attn_bwd_workspace", "tt_attn_bwd",
-                       "tt_restore_loss", "tt_grad_sqnorm", "tt_grad_sqnorm3"):
+                       "tt_restore_loss", "tt_grad_sqnorm", "tt_grad_sqnorm3", "tt_plan_traversals",
+                       "tt_traversal_forest"):
                 getattr(L, fn).restype = C.c_int
             _lib = L
     return _lib
@@ -303,3 +311,34 @@ def tt_grad_sqnorm3(x0, x1, x2, out=None, ws=None, stream=None):
                                                 int(x2.numel()), _dt(x0), _p(out), _p(ws), int(ws.numel()),
                                                 _stream(stream)))
     return out
+
+
+def tt_plan_traversals(parent, length, capacity, term=None):
+    """Capacity-constrained Tree Packing (host).  Returns (traversal id per canonical trajectory
+    [n_traj] int32 numpy, info dict)."""
+    par, pp = _host_i32(parent)
+    ln, lp = _host_i32(length)
+    tm, tp = _host_i32(term)
+    info = TTPlanInfo()
+    L = lib()
+    _check("tt_plan_traversals", L.tt_plan_traversals(pp, lp, tp, int(par.shape[0]), int(capacity), None, C.byref(info)))
+    out = np.zeros(max(info.n_traj, 1), np.int32)
+    _check("tt_plan_traversals", L.tt_plan_traversals(pp, lp, tp, int(par.shape[0]), int(capacity),
+                                                      out.ctypes.data_as(C.POINTER(C.c_int32)), C.byref(info)))
+    return out[:info.n_traj], {f: getattr(info, f) for f, _ in TTPlanInfo._fields_}
+
+
+def tt_traversal_forest(parent, length, traversal_of_traj, traversal, term=None):
+    """Sub-forest induced by one traversal -> (parent, len, term, original node ids) numpy int32."""
+    par, pp = _host_i32(parent)
+    ln, lp = _host_i32(length)
+    tm, tp = _host_i32(term)
+    tv, tvp = _host_i32(traversal_of_traj)
+    n = int(par.shape[0])
+    op, ol, ot, on = (np.zeros(n, np.int32) for _ in range(4))
+    m = C.c_int32()
+    ptr = lambda a: a.ctypes.data_as(C.POINTER(C.c_int32))
+    _check("tt_traversal_forest", lib().tt_traversal_forest(pp, lp, tp, n, tvp, int(traversal), ptr(op), ptr(ol),
+                                                            ptr(ot), ptr(on), C.byref(m)))
+    k = m.value
+    return op[:k], ol[:k], ot[:k], on[:k]
