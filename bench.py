@@ -197,6 +197,20 @@ def run_step(job, ev=None, h2d=False):
     return pk
 
 
+def _longest_paths(tree):
+    """Token length of every root-to-node path that ends a trajectory (plain parent walk)."""
+    par, ln = tree.parent, tree.length
+    has_child = np.zeros(len(par), bool)
+    has_child[par[par >= 0]] = True
+    ends = np.flatnonzero(~has_child) if tree.term is None else np.flatnonzero(tree.term > 0)
+    for v in ends:
+        s, u = 0, int(v)
+        while u >= 0:
+            s += int(ln[u])
+            u = int(par[u])
+        yield s
+
+
 def flush_l2(buf):
     buf.add_(1)  # 256 MiB read+write > 126 MB L2
 
@@ -456,6 +470,24 @@ def main():
                                     "pair_ratio": out["config"]["pair_ratio"], "token_ratio": out["config"]["token_ratio"],
                                     "frac_of_pair_ratio": round(lin_ms / tree_ms / out["config"]["pair_ratio"], 3),
                                     "frac_of_token_ratio": round(lin_ms / tree_ms / out["config"]["token_ratio"], 3)}
+    if rank == 0:
+        # NEXT-f1: capacity-constrained Tree Packing of this rank's tree at a budget forcing a split
+        # (C = max(longest trajectory, tree tokens / 2)); host planner timing + effective reuse
+        t_ = jobs[0].tree
+        lens = tt.tt_plan_traversals(t_.parent, t_.length, 1 << 40)[1]
+        longest = max(int(x) for x in _longest_paths(t_))
+        C = max(longest, lens["tree_tokens"] // 2)
+        reps = 20
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            a, pinfo = tt.tt_plan_traversals(t_.parent, t_.length, C)
+        plan_ms = (time.perf_counter() - t0) / reps * 1e3
+        out["next_f1_planner"] = {"capacity": int(C), "n_traversals": pinfo["n_traversals"],
+                                  "planned_tokens": pinfo["planned_tokens"], "tree_tokens": pinfo["tree_tokens"],
+                                  "linear_tokens": pinfo["linear_tokens"],
+                                  "ERR": round(1 - pinfo["planned_tokens"] / pinfo["linear_tokens"], 4),
+                                  "POR": round(1 - pinfo["tree_tokens"] / pinfo["linear_tokens"], 4),
+                                  "host_plan_ms": round(plan_ms, 4)}
     if rank == 0 and world == 1 and not args.no_cpu:
         dt, share, ntraj, cores = oracle_sample(jobs[0].tree, cfg, budget_s=args.cpu_budget)
         full_s = dt / share
