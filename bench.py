@@ -112,10 +112,44 @@ def make_trees(args, rank, world):
     return [(seed, trees.config_tree(args.config, seed))], {}
 
 
-class TreeJob:
-    """Device-resident inputs + outputs for one tree (allocated once, untimed)."""
+class Scratch:
+    """Per-rank buffers shared by the trees a rank processes one after another (allocated once at
+    the largest tree, untimed): outputs, logits / dlogits, the bwd workspace, pinned host sources."""
 
-    def __init__(self, tid, tree, cfg, vocab, gen, with_loss=True, host_copy=False):
+    def __init__(self, maxN, cfg, vocab, gen, with_loss, host_copy):
+        import torch
+        dev, dt = "cuda", torch.bfloat16
+        hq, hkv, d = cfg["hq"], cfg["hkv"], cfg["d"]
+        self.o = torch.empty(maxN, hq, d, device=dev, dtype=dt)
+        self.lse = torch.empty(hq * maxN, device=dev)
+        self.dq = torch.empty(maxN, hq, d, device=dev, dtype=dt)
+        self.dk = torch.empty(maxN, hkv, d, device=dev, dtype=dt)
+        self.dv = torch.empty(maxN, hkv, d, device=dev, dtype=dt)
+        self.ws = None
+        if with_loss:
+            self.logits = torch.empty(maxN, vocab, device=dev, dtype=dt)
+            for r0 in range(0, maxN, 2048):  # chunked to bound the fp32 temporary
+                r1 = min(maxN, r0 + 2048)
+                self.logits[r0:r1] = (2.0 * torch.randn(r1 - r0, vocab, device=dev, generator=gen)).to(dt)
+            self.dlogits = torch.empty_like(self.logits)
+            self.tok_loss = torch.empty(maxN, device=dev)
+        self.host = None
+        if host_copy:
+            # pinned host sources of one tree's step inputs (re-used for every tree of the rank:
+            # the bytes each tree copies are its own N rows)
+            hg = torch.Generator().manual_seed(99)
+            self.host = {n: torch.randn(maxN, h, d, generator=hg).to(dt).pin_memory()
+                         for n, h in (("q", hq), ("k", hkv), ("v", hkv), ("g", hq))}
+            if with_loss:
+                self.host["logits"] = self.logits.cpu().pin_memory()
+                self.host["tok"] = torch.randint(0, vocab, (maxN,), generator=hg, dtype=torch.int32).pin_memory()
+
+
+class TreeJob:
+    """Device-resident inputs for one tree (allocated once, untimed); outputs live in the rank's
+    shared Scratch (trees of a rank run one after another)."""
+
+    def __init__(self, tid, tree, cfg, vocab, gen, scratch, with_loss=True, host_copy=False):
         import torch
         import paper_2511_00413_b200 as tt
         self.tid, self.tree = tid, tree
@@ -129,28 +163,28 @@ class TreeJob:
         self.k = torch.randn(N, self.hkv, self.d, device=dev, dtype=torch.float32, generator=gen).to(dt)
         self.v = torch.randn(N, self.hkv, self.d, device=dev, dtype=torch.float32, generator=gen).to(dt)
         self.g = torch.randn(N, self.hq, self.d, device=dev, dtype=torch.float32, generator=gen).to(dt)
-        self.o = torch.empty_like(self.q)
-        self.lse = torch.empty(self.hq, N, device=dev)
-        self.dq, self.dk, self.dv = torch.empty_like(self.q), torch.empty_like(self.k), torch.empty_like(self.v)
-        self.ws = None
+        S = self.scratch = scratch
+        self.o, self.dq, self.dk, self.dv = S.o[:N], S.dq[:N], S.dk[:N], S.dv[:N]
+        self.lse = S.lse[:self.hq * N].view(self.hq, N)
         self.with_loss = with_loss
         self.vocab = vocab
         if with_loss:
-            self.logits = torch.empty(N, vocab, device=dev, dtype=dt)
-            for r0 in range(0, N, 2048):  # chunked to bound the fp32 temporary
-                r1 = min(N, r0 + 2048)
-                self.logits[r0:r1] = (2.0 * torch.randn(r1 - r0, vocab, device=dev, generator=gen)).to(dt)
+            self.logits, self.dlogits, self.tok_loss = S.logits[:N], S.dlogits[:N], S.tok_loss[:N]
             self.tok = torch.randint(0, vocab, (N,), device=dev, dtype=torch.int32, generator=gen)
-            self.dlogits = torch.empty_like(self.logits)
-            self.tok_loss = torch.empty(N, device=dev)
-            self.sums = torch.zeros(2, dtype=torch.float64, device=dev)
             self.err = torch.zeros(1, dtype=torch.int32, device=dev)
         self.rec = torch.zeros(5, dtype=torch.float64, device=dev)
         self.host = None
         if host_copy:
-            names = ["q", "k", "v", "g"] + (["logits", "tok"] if with_loss else [])
-            self.host = {n: getattr(self, n).cpu().pin_memory() for n in names}
+            self.host = {n: t[:N] for n, t in S.host.items()}
             self.rec_host = torch.zeros(5, dtype=torch.float64).pin_memory()
+
+    @property
+    def ws(self):
+        return self.scratch.ws
+
+    @ws.setter
+    def ws(self, value):
+        self.scratch.ws = value
 
     def flops(self):
         return 14.0 * self.d * self.hq * self.info["n_pairs"]
@@ -182,9 +216,9 @@ def run_step(job, ev=None, h2d=False):
         tt.tt_restore_loss(pk, job.logits, job.tok, grad_scale=1.0, dlogits=job.dlogits,   # a3
                            tok_loss=job.tok_loss, sums=job.rec[0:2], d_err=job.err)
         mark("loss", 1)
-    if job.ws is None:
-        job.ws = torch.empty(tt.tt_attn_bwd_workspace(pk, job.hq, job.hkv, job.d, job.q.dtype),
-                             dtype=torch.uint8, device="cuda")
+    need = tt.tt_attn_bwd_workspace(pk, job.hq, job.hkv, job.d, job.q.dtype)
+    if job.ws is None or job.ws.numel() < need:
+        job.ws = torch.empty(need, dtype=torch.uint8, device="cuda")
     mark("bwd", 0)
     tt.tt_attn_bwd(pk, job.q, job.k, job.v, job.o, job.lse, job.g, restore=True,          # a4 + a5
                    dq=job.dq, dk=job.dk, dv=job.dv, ws=job.ws)
@@ -323,7 +357,9 @@ def main():
     gen = torch.Generator(device="cuda").manual_seed(1234 + rank)
     with_loss = not args.no_loss
     host_copy = not args.no_e2e
-    jobs = [TreeJob(tid, t, cfg, VOCAB, gen, with_loss=with_loss, host_copy=host_copy) for tid, t in my_trees]
+    maxN = max(int(tt.tt_pack_plan(t.parent, t.length)["n_tokens"]) for _, t in my_trees)
+    scratch = Scratch(maxN, cfg, VOCAB, gen, with_loss, host_copy)
+    jobs = [TreeJob(tid, t, cfg, VOCAB, gen, scratch, with_loss=with_loss, host_copy=host_copy) for tid, t in my_trees]
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
     n_total_trees = args.trees if args.config == "batch64k" else world
 

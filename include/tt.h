@@ -128,6 +128,9 @@ typedef struct {
   const int32_t* kblk_maxE;    /* [n_blk]  */
   const int32_t* fwd_cnt;      /* [n_blk]  */
   const int32_t* fwd_list;     /* [n_blk * (n_blk + 1) / 2] */
+  const float* wr;             /* [n_blk * 128] real-valued tree-scale W (NEXT-f4), NULL after tt_pack;
+                                  set by tt_pack_weights.  When non-NULL it replaces w as the
+                                  restoration weight of tt_attn_bwd and tt_restore_loss.          */
   int64_t n_tokens;
   int32_t n_nodes;
   int32_t n_blk;
@@ -146,6 +149,26 @@ tt_status tt_pack(const int32_t* parent, const int32_t* len, const int32_t* term
                   void* d_ws, size_t ws_bytes, tt_packed* out, tt_pack_info* info, tt_stream_t stream);
 
 /* --------------------------------------------------------------------------------------
+ * Real-valued leaf weights ("leaf_weights: per leaf in batch,
+ * real" and "tree_scale of a token in node u = sum of weights of leaves in u's subtree that are
+ * present in THIS traversal", "non-uniform leaf weights ... scaler = weight sums"; linear
+ * extension of Eq. 12, reading R20).
+ *   The training objective becomes sum_l alpha_l * Loss_l over trajectories l (alpha: e.g. RL
+ *   advantages, any sign).  By linearity every identity of the integer case holds with the
+ *   leaf count w_i replaced by W_i = sum of alpha_l over the trajectories through token i.
+ * traj_weight: HOST [n_traj] fp32, trajectory l in canonical order (DFS pre-order of trajectory
+ *   end nodes, roots / children ascending id, the term(u) trajectories of a node consecutive) —
+ *   the same order tt_plan_traversals numbers trajectories in; for one traversal of a plan, pass
+ *   the weights of its trajectories in that order over the forest tt_traversal_forest returns.
+ * parent/len/term/n_nodes: exactly the forest pk was packed from (checked: n_nodes, N).
+ * wr: DEVICE [n_blk * 128] fp32, 16-byte aligned, caller-owned; W per token (fp64 subtree sums
+ *   rounded once to fp32), 0 in the padding.  On success pk->wr = wr.  Host work O(n + N), one
+ *   async H2D copy on `stream` (the host image is staged before return).
+ * -------------------------------------------------------------------------------------- */
+tt_status tt_pack_weights(const int32_t* parent, const int32_t* len, const int32_t* term, int32_t n_nodes,
+                          const float* traj_weight, tt_packed* pk, float* wr, tt_stream_t stream);
+
+/* --------------------------------------------------------------------------------------
  * Tree-masked attention forward (Eq. 1 P:119-126 with softmax scale, R1; mask R2):
  *   O_i   = sum_{j : j <= i < E_j} softmax_j(scale * q_i . k_j) v_j
  *   LSE_i = ln sum_{j : j <= i < E_j} exp(scale * q_i . k_j)      (natural log, R9)
@@ -162,7 +185,7 @@ tt_status tt_attn_bwd_workspace(const tt_packed* pk, int32_t hq, int32_t hkv, in
 
 /* --------------------------------------------------------------------------------------
  * Tree-masked attention backward with Gradient Restoration (Eqs. 2, 14-16, 20-21; R6):
- *   omega_i = w_i if restore else 1;  P_ij = exp(scale q_i.k_j - LSE_i);  D_i = dO_i . O_i
+ *   omega_i = (pk->wr ? pk->wr[i] : w_i) if restore else 1;  P_ij = exp(scale q_i.k_j - LSE_i);  D_i = dO_i . O_i
  *   dV_j = sum_i omega_i P_ij dO_i
  *   dS_ij = omega_i P_ij (dO_i . v_j - D_i)
  *   dQ_i = scale sum_j dS_ij k_j,   dK_j = scale sum_i dS_ij q_i     (sums over j <= i < E_j)
@@ -181,7 +204,8 @@ tt_status tt_attn_bwd(const tt_packed* pk, const void* q, const void* k, const v
  * Gradient-Restoration loss (R6, R7, R8, R17).  For every packed row t
  * with targets T(t) (next token inside the node, else the continuation list succ_tok; a target
  * counts iff node_loss_mask[node(target)] != 0 when the mask is given, and — boundary_mode 1 —
- * only when t has exactly one continuation), each target k with weight omega_k = w[k]:
+ * only when t has exactly one continuation), each target k with weight omega_k = w[k] (pk->wr[k]
+ * when real-valued leaf weights are set, NEXT-f4):
  *   loss_t   = sum_k omega_k (lse(x_t) - x_t[tok[k]])
  *   dlogits_t = grad_scale * (Omega_t softmax(x_t) - sum_k omega_k e_{tok[k]}),  Omega_t = sum omega_k
  * logits [N, ld] bf16 (row stride ld >= vocab elements, 16-byte aligned rows); dlogits has the

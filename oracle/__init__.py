@@ -63,8 +63,8 @@ def lib():
             L.oracle_attn_fwd.argtypes = [C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_double,
                                           dp, dp, dp, C.c_int64, i64p, i32p, u8p, C.c_int32, dp, dp, C.c_int32]
             L.oracle_attn_bwd.argtypes = [C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_double,
-                                          dp, dp, dp, dp, C.c_int64, i64p, i32p, u8p, u8p, dp, dp, dp, C.c_int32]
-            L.oracle_loss.argtypes = [C.c_int64, C.c_int32, i32p, C.c_int64, i64p, i32p, u8p, C.c_int32,
+                                          dp, dp, dp, dp, C.c_int64, i64p, i32p, dp, u8p, u8p, dp, dp, dp, C.c_int32]
+            L.oracle_loss.argtypes = [C.c_int64, C.c_int32, i32p, C.c_int64, i64p, i32p, dp, u8p, C.c_int32,
                                       C.c_double, C.c_int64, i64p, dp, dp, dp, dp, C.c_int32]
             _lib = L
     return _lib
@@ -129,6 +129,15 @@ def pack(parent, length, term=None) -> dict:
     return out
 
 
+def _tw(pk, traj_weight):
+    if traj_weight is None:
+        return None
+    a = np.ascontiguousarray(np.asarray(traj_weight, dtype=np.float64))
+    if a.shape != (pk["n_traj"],):
+        raise ValueError("traj_weight must have one entry per trajectory")
+    return a
+
+
 def paths(pk) -> list:
     """Trajectory index paths as a list of int arrays (ascending trajectory order)."""
     p = pk["path_ptr"]
@@ -181,9 +190,10 @@ def attn_fwd(pk, q, k, v, scale, want=None, check_invariant=True, nthreads=None)
     return o, lse
 
 
-def attn_bwd(pk, q, k, v, g, scale, want_q=None, want_k=None, nthreads=None):
+def attn_bwd(pk, q, k, v, g, scale, want_q=None, want_k=None, nthreads=None, traj_weight=None):
     """Tree attention backward = sum over branches of ordinary causal-attention gradients with
-    per-token upstream gradient g [N,hq,d].  Returns (dq, dk, dv) fp64."""
+    per-token upstream gradient g [N,hq,d]; branch t weighted by traj_weight[t] when given (R20).
+    Returns (dq, dk, dv) fp64."""
     L = lib()
     q, k, v, g = _f64(q), _f64(k), _f64(v), _f64(g)
     N, hq, d = q.shape
@@ -195,6 +205,7 @@ def attn_bwd(pk, q, k, v, g, scale, want_q=None, want_k=None, nthreads=None):
     rc = L.oracle_attn_bwd(N, hq, hkv, d, float(scale), _ptr(q, C.c_double), _ptr(k, C.c_double),
                            _ptr(v, C.c_double), _ptr(g, C.c_double), pk["n_traj"],
                            _ptr(pk["path_ptr"], C.c_int64), _ptr(pk["path_idx"], C.c_int32),
+                           _ptr(_tw(pk, traj_weight), C.c_double),
                            _ptr(wq, C.c_uint8), _ptr(wk, C.c_uint8), _ptr(dq, C.c_double),
                            _ptr(dk, C.c_double), _ptr(dv, C.c_double), nthreads or default_threads())
     if rc:
@@ -202,10 +213,12 @@ def attn_bwd(pk, q, k, v, g, scale, want_q=None, want_k=None, nthreads=None):
     return dq, dk, dv
 
 
-def loss(pk, tok, vocab, row_ids, x_rows, gamma=1.0, node_loss_mask=None, boundary_mode=0, nthreads=None):
+def loss(pk, tok, vocab, row_ids, x_rows, gamma=1.0, node_loss_mask=None, boundary_mode=0, nthreads=None,
+         traj_weight=None):
     """Per-branch next-token CE at the listed rows.  x_rows [n_rows, vocab] are the logits of
     row_ids.  node_loss_mask (nullable, per node) supervises a prediction iff the TARGET token's
-    node is set (reading R17).  Returns (loss_rows, omega_rows, dx_rows)."""
+    node is set (reading R17).  traj_weight (nullable, per trajectory) weights branch t's CE
+    (R20).  Returns (loss_rows, omega_rows, dx_rows)."""
     L = lib()
     tok = _i32(tok)
     N = pk["n_tokens"]
@@ -218,7 +231,8 @@ def loss(pk, tok, vocab, row_ids, x_rows, gamma=1.0, node_loss_mask=None, bounda
         sup = _u8(np.asarray(node_loss_mask, dtype=np.uint8)[pk["node"]])
     lr = np.zeros(n_rows); om = np.zeros(n_rows); dx = np.zeros((n_rows, vocab))
     rc = L.oracle_loss(N, vocab, _ptr(tok, C.c_int32), pk["n_traj"], _ptr(pk["path_ptr"], C.c_int64),
-                       _ptr(pk["path_idx"], C.c_int32), _ptr(sup, C.c_uint8), int(boundary_mode),
+                       _ptr(pk["path_idx"], C.c_int32), _ptr(_tw(pk, traj_weight), C.c_double),
+                       _ptr(sup, C.c_uint8), int(boundary_mode),
                        float(gamma), n_rows, _ptr(row_ids, C.c_int64), _ptr(x, C.c_double),
                        _ptr(lr, C.c_double), _ptr(om, C.c_double), _ptr(dx, C.c_double),
                        nthreads or default_threads())

@@ -345,11 +345,13 @@ int oracle_attn_fwd(int64_t N, int32_t hq, int32_t hkv, int32_t d, double scale,
 //   Branch results are scatter-added into dq [N,hq,d], dk/dv [N,hkv,d] in ascending trajectory
 //   order; dk/dv of a kv group are the sum over its q heads in ascending head order.
 //   want_q / want_k (nullable [N]): rows whose dq / keys whose dk,dv are required.
+//   traj_weight (nullable [n_traj]): objective sum_t alpha_t Loss_t (SPEC S:332 leaf_weights, S:475;
+//   reading R20): branch t's gradients are multiplied by alpha_t before the scatter-add.
 // ---------------------------------------------------------------------------------------------
 int oracle_attn_bwd(int64_t N, int32_t hq, int32_t hkv, int32_t d, double scale,
                     const double* q, const double* k, const double* v, const double* gup,
                     int64_t n_traj, const int64_t* path_ptr, const int32_t* path_idx,
-                    const uint8_t* want_q, const uint8_t* want_k,
+                    const double* traj_weight, const uint8_t* want_q, const uint8_t* want_k,
                     double* dq, double* dk, double* dv, int32_t nthreads) {
   if (hq <= 0 || hkv <= 0 || hq % hkv || d <= 0) return OE_INVALID;
   const int g = hq / hkv;
@@ -412,12 +414,13 @@ int oracle_attn_bwd(int64_t N, int32_t hq, int32_t hkv, int32_t d, double scale,
         }
       }
       // scatter-add branch gradients into the tree arrays (Eq. 16: prefix grads are sums)
+      const double a = traj_weight ? traj_weight[t] : 1.0;
       for (int64_t p = 0; p < L; ++p) {
         const int64_t i = idx[p];
         for (int c = 0; c < d; ++c) {
-          dq[(i * hq + h) * d + c] += bq[p * d + c];
-          dk_h[h][i * d + c] += bk[p * d + c];
-          dv_h[h][i * d + c] += bv[p * d + c];
+          dq[(i * hq + h) * d + c] += a * bq[p * d + c];
+          dk_h[h][i * d + c] += a * bk[p * d + c];
+          dv_h[h][i * d + c] += a * bv[p * d + c];
         }
       }
     }
@@ -446,9 +449,11 @@ int oracle_attn_bwd(int64_t N, int32_t hq, int32_t hkv, int32_t d, double scale,
 //   Only rows listed in row_ids are evaluated; x_rows[r, :] are the logits of row_ids[r].
 //   Outputs per listed row: loss_rows (sum over branches of lse - x[target]), omega_rows (number
 //   of counted predictions), dx_rows = gamma * sum over counted predictions (softmax - onehot).
+//   traj_weight (nullable [n_traj]): each prediction of branch t counts alpha_t times (loss, omega
+//   and dx), the objective sum_t alpha_t Loss_t of SPEC S:332 / S:475 (reading R20).
 // ---------------------------------------------------------------------------------------------
 int oracle_loss(int64_t N, int32_t V, const int32_t* tok, int64_t n_traj, const int64_t* path_ptr,
-                const int32_t* path_idx, const uint8_t* target_sup, int32_t boundary_mode, double gamma,
+                const int32_t* path_idx, const double* traj_weight, const uint8_t* target_sup, int32_t boundary_mode, double gamma,
                 int64_t n_rows, const int64_t* row_ids, const double* x_rows,
                 double* loss_rows, double* omega_rows, double* dx_rows, int32_t nthreads) {
   if (V <= 0 || n_rows < 0) return OE_INVALID;
@@ -470,13 +475,14 @@ int oracle_loss(int64_t N, int32_t V, const int32_t* tok, int64_t n_traj, const 
     }
   }
   // occurrences (branch order) of every requested row
-  std::vector<std::vector<int64_t>> occ_next(n_rows);
+  std::vector<std::vector<std::pair<int64_t, double>>> occ_next(n_rows);
   for (int64_t t = 0; t < n_traj; ++t) {
     const int32_t* idx = path_idx + path_ptr[t];
     const int64_t L = path_ptr[t + 1] - path_ptr[t];
+    const double a = traj_weight ? traj_weight[t] : 1.0;
     for (int64_t p = 0; p + 1 < L; ++p) {
       int64_t r = slot[idx[p]];
-      if (r >= 0) occ_next[r].push_back(idx[p + 1]);
+      if (r >= 0) occ_next[r].push_back({idx[p + 1], a});
     }
   }
   for (int64_t i = 0; i < N; ++i)
@@ -487,7 +493,9 @@ int oracle_loss(int64_t N, int32_t V, const int32_t* tok, int64_t n_traj, const 
     for (int32_t c = 0; c < V; ++c) dx[c] = 0.0;
     double loss = 0.0, omega = 0.0;
     const int64_t i = row_ids[r];
-    for (int64_t nx : occ_next[r]) {
+    for (const auto& oc : occ_next[r]) {
+      const int64_t nx = oc.first;
+      const double a = oc.second;
       if (target_sup && !target_sup[nx]) continue;
       if (boundary_mode == 1 && diverge[i]) continue;
       double m = -INFINITY;
@@ -496,10 +504,10 @@ int oracle_loss(int64_t N, int32_t V, const int32_t* tok, int64_t n_traj, const 
       for (int32_t c = 0; c < V; ++c) l += std::exp(x[c] - m);
       double lse = m + std::log(l);
       int32_t y = tok[nx];
-      loss += lse - x[y];
-      omega += 1.0;
-      for (int32_t c = 0; c < V; ++c) dx[c] += gamma * std::exp(x[c] - lse);
-      dx[y] -= gamma;
+      loss += a * (lse - x[y]);
+      omega += a;
+      for (int32_t c = 0; c < V; ++c) dx[c] += gamma * a * std::exp(x[c] - lse);
+      dx[y] -= gamma * a;
     }
     loss_rows[r] = loss;
     omega_rows[r] = omega;

@@ -38,7 +38,7 @@ class TTPackInfo(C.Structure):
 
 
 _PTR_FIELDS = ["pos", "w", "E", "node", "node_start", "node_len", "node_sub_end", "node_depth", "node_leaves",
-               "succ_ptr", "succ_tok", "kblk_minE", "kblk_maxE", "fwd_cnt", "fwd_list"]
+               "succ_ptr", "succ_tok", "kblk_minE", "kblk_maxE", "fwd_cnt", "fwd_list", "wr"]
 
 
 class TTPlanInfo(C.Structure):
@@ -91,6 +91,8 @@ def lib():
             L.tt_grad_sqnorm.argtypes = [vp, C.c_int64, C.c_int, vp, vp, sz, st]
             L.tt_grad_sqnorm3.argtypes = [vp, C.c_int64, vp, C.c_int64, vp, C.c_int64, C.c_int, vp, vp, sz, st]
             L.tt_plan_traversals.argtypes = [i32p, i32p, i32p, C.c_int32, C.c_int64, i32p, C.POINTER(TTPlanInfo)]
+            L.tt_pack_weights.argtypes = [i32p, i32p, i32p, C.c_int32, C.POINTER(C.c_float), C.POINTER(TTPacked),
+                                          vp, st]
             L.tt_traversal_forest.argtypes = [i32p, i32p, i32p, C.c_int32, i32p, C.c_int32, i32p, i32p, i32p, i32p, i32p]
             L.tt_launch_count.restype = C.c_int64
             L.tt_launch_count.argtypes = []
@@ -168,6 +170,7 @@ class PackedTree:
         self.info = info
         self.ws = ws
         self.parent, self.length, self.term = parent, length, term
+        self.wr = None
 
     @property
     def n_tokens(self) -> int:
@@ -217,6 +220,26 @@ def tt_pack(parent, length, term=None, device=None, stream=None) -> PackedTree:
     d = {f: getattr(info2, f) for f, _ in TTPackInfo._fields_ if f != "reserved"}
     d["max_succ"] = int(c.max_succ)
     return PackedTree(c, d, ws, par, ln, tm)
+
+
+def tt_pack_weights(pk: PackedTree, traj_weight, stream=None):
+    """Real-valued leaf weights (NEXT-f4): W_i = sum of traj_weight over the trajectories through
+    token i (canonical trajectory order, include/tt.h).  Sets pk.c.wr; restoration in tt_attn_bwd
+    and tt_restore_loss then uses W instead of the integer leaf count.  Returns the device W."""
+    import numpy as np
+    import torch
+    a = np.ascontiguousarray(np.asarray(traj_weight, dtype=np.float32))
+    if a.shape != (int(pk.info["n_traj"]),):
+        raise ValueError(f"traj_weight must have n_traj = {pk.info['n_traj']} entries, got {a.shape}")
+    par, pp = _host_i32(pk.parent)
+    ln, lp = _host_i32(pk.length)
+    tm, tp = _host_i32(pk.term)
+    wr = torch.empty(pk.n_blk * 128, dtype=torch.float32, device=pk.ws.device)
+    _check("tt_pack_weights", lib().tt_pack_weights(pp, lp, tp, int(par.shape[0]),
+                                                    a.ctypes.data_as(C.POINTER(C.c_float)), C.byref(pk.c),
+                                                    C.c_void_p(wr.data_ptr()), _stream(stream)))
+    pk.wr = wr  # keep alive while pk references it
+    return wr
 
 
 def _scale(softmax_scale, d):

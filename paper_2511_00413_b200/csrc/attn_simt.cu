@@ -40,6 +40,7 @@ constexpr int kPerWarp = kRows / kWarps;  // 8
 struct PackView {
   int64_t N;
   const int32_t* w;
+  const float* wr;  // real-valued tree-scale (NEXT-f4) or null
   const int32_t* E;
   const int32_t* kmaxE;
   const int32_t* fwd_cnt;
@@ -186,7 +187,7 @@ __global__ void __launch_bounds__(kThreads) simt_dq_kernel(PackView pv, const T*
     const bool in = i < N;
     lse2[rr] = in ? lse[(int64_t)h * N + i] * kLog2e : 0.f;
     Di[rr] = in ? Dvec[(int64_t)h * N + i] : 0.f;
-    om[rr] = (in && restore) ? (float)pv.w[i] : 1.f;
+    om[rr] = (in && restore) ? (pv.wr ? pv.wr[i] : (float)pv.w[i]) : 1.f;
 #pragma unroll
     for (int cc = 0; cc < NC; ++cc) acc[rr][cc] = 0.f;
   }
@@ -314,7 +315,7 @@ __global__ void __launch_bounds__(kThreads) simt_dkdv_kernel(PackView pv, const 
         const bool in = i < N;
         sL[tid] = in ? lse[(int64_t)h * N + i] * kLog2e : 0.f;
         sD[tid] = in ? Dvec[(int64_t)h * N + i] : 0.f;
-        sW[tid] = (in && restore) ? (float)pv.w[i] : 1.f;
+        sW[tid] = (in && restore) ? (pv.wr ? pv.wr[i] : (float)pv.w[i]) : 1.f;
       }
       __syncthreads();
       const int64_t i = i0 + lane;
@@ -370,7 +371,7 @@ template <int D> constexpr size_t dkdv_smem() {
 }
 
 PackView view(const tt_packed& pk) {
-  return PackView{pk.n_tokens, pk.w, pk.E, pk.kblk_maxE, pk.fwd_cnt, pk.fwd_list};
+  return PackView{pk.n_tokens, pk.w, pk.wr, pk.E, pk.kblk_maxE, pk.fwd_cnt, pk.fwd_list};
 }
 
 template <typename T, int D>

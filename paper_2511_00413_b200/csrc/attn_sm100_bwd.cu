@@ -84,6 +84,8 @@ struct BwdParams {
   int64_t N;
   int hq, hkv, g, nb;
   int restore;
+  int head_major;  // CTA order: 1 = all k-blocks of kv head 0, then head 1, ... (dQ rows of one
+                   // head group stay L2-resident); 0 = heads fastest
   int dbg;  // development ablations (TT_DEBUG_BWD): 1 skip dQ reduce, 2 reuse Q/dO stage (no reload), 4 skip elementwise math
   float scale, scale_log2;
   const int32_t* E;
@@ -119,8 +121,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long t_kernel0 = TT_CLK();
-  const int kb = (int)(blockIdx.x / p.hkv);
-  const int hk = (int)(blockIdx.x % p.hkv);
+  const int kb = p.head_major ? (int)(blockIdx.x % p.nb) : (int)(blockIdx.x / p.hkv);
+  const int hk = p.head_major ? (int)(blockIdx.x / p.nb) : (int)(blockIdx.x % p.hkv);
   const int64_t k0 = (int64_t)kb * 128;
   const int qt0 = (int)(k0 / kBQ);                                    // first 64-row query tile
   const int qt1 = (int)((p.kmaxE[kb] + kBQ - 1) / kBQ);                // exclusive
@@ -486,7 +488,7 @@ tt_status sm100_attn_bwd(const tt_packed& pk, const void* q, const void* k, cons
   float* L2p = reinterpret_cast<float*>(w8 + al256b((size_t)hq * Np * 4));
   float* wf = reinterpret_cast<float*>(w8 + 2 * al256b((size_t)hq * Np * 4));
   float* dq_acc = reinterpret_cast<float*>(w8 + 2 * al256b((size_t)hq * Np * 4) + al256b((size_t)Np * 4));
-  tt_status s = launch_bwd_pre_tc(o, dout, lse, pk.w, restore, N, Np, hq, Dp, L2p, wf, dq_acc, st);
+  tt_status s = launch_bwd_pre_tc(o, dout, lse, pk.w, pk.wr, restore, N, Np, hq, Dp, L2p, wf, dq_acc, st);
   if (s) return s;
   CUtensorMap mq, mk, mv, mdo, mdq;
   const auto BF = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
@@ -507,6 +509,8 @@ tt_status sm100_attn_bwd(const tt_packed& pk, const void* q, const void* k, cons
   {
     const char* e = getenv("TT_DEBUG_BWD");
     prm.dbg = e ? atoi(e) : 0;
+    const char* o = getenv("TT_CTA_ORDER");  // development A/B: bit 1 = bwd head-major
+    prm.head_major = o ? ((atoi(o) >> 1) & 1) : 0;  // measured: head-major loses the global heavy-first order (8K -10%, wide -12%)
   }
   prm.scale = scale;
   prm.scale_log2 = scale * kLog2e;

@@ -60,6 +60,7 @@ struct FwdParams {
   int64_t N;
   int hq, hkv, nb, npairs;
   float scale_log2;
+  int head_major;  // CTA order: 1 = kv-head groups outermost (K/V of one group L2-resident)
   int dbg;
   const int32_t* E;
   const int32_t* fwd_cnt;
@@ -90,8 +91,12 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   uint8_t* flags1 = flags0 + p.nb + 4;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int pair = p.npairs - 1 - (int)(blockIdx.x / p.hq);  // heavy (late) query blocks first
-  const int h = (int)(blockIdx.x % p.hq);
+  // heavy (late) query blocks first; the q heads of one kv head adjacent
+  const int gq = p.hq / p.hkv;
+  const int pair = p.head_major ? p.npairs - 1 - (int)((blockIdx.x % (p.npairs * gq)) / gq)
+                                : p.npairs - 1 - (int)(blockIdx.x / p.hq);
+  const int h = p.head_major ? (int)(blockIdx.x / (p.npairs * gq)) * gq + (int)(blockIdx.x % gq)
+                             : (int)(blockIdx.x % p.hq);
   const int hk = h / (p.hq / p.hkv);
   const int qa = 2 * pair;
   const bool has1 = qa + 1 < p.nb && !(p.dbg & 16);  // dbg 16: development ablation, drop query tile 1
@@ -473,6 +478,8 @@ tt_status sm100_attn_fwd(const tt_packed& pk, const void* q, const void* k, cons
   {
     const char* e = getenv("TT_DEBUG_FWD");
     prm.dbg = e ? atoi(e) : 0;
+    const char* o = getenv("TT_CTA_ORDER");  // development A/B: bit 0 = fwd head-major
+    prm.head_major = o ? (atoi(o) & 1) : 0;
   }
   prm.E = pk.E;
   prm.fwd_cnt = pk.fwd_cnt;

@@ -110,7 +110,7 @@ template <int W> __device__ __forceinline__ void accum(float& m, float& s, const
 template <int W>
 __global__ void __launch_bounds__(kLossThreads) loss_kernel(
     int64_t N, const __nv_bfloat16* logits, int64_t ld, int V, const int32_t* __restrict__ tok,
-    const uint8_t* __restrict__ node_mask, int boundary_mode, float gamma, const int32_t* __restrict__ w,
+    const uint8_t* __restrict__ node_mask, int boundary_mode, float gamma, const int32_t* __restrict__ w, const float* __restrict__ wr,
     const int32_t* __restrict__ node, const int32_t* __restrict__ node_start, const int32_t* __restrict__ node_len,
     const int32_t* __restrict__ succ_ptr, const int32_t* __restrict__ succ_tok, __nv_bfloat16* dlogits,
     float* __restrict__ tok_loss, float* __restrict__ ws_loss, float* __restrict__ ws_omega, int32_t* d_err) {
@@ -152,7 +152,7 @@ __global__ void __launch_bounds__(kLossThreads) loss_kernel(
     for (int k = tid; k < nt; k += kLossThreads) {
       const int tg = s_y[k];
       const int y = tok[tg];
-      const float om = (float)w[tg];
+      const float om = wr ? wr[tg] : (float)w[tg];
       bad |= (y < 0 || y >= V);
       s_y[k] = y;
       s_om[k] = om;
@@ -301,7 +301,7 @@ __device__ __forceinline__ void mbar_expect_(uint64_t* b, uint32_t bytes) {
 
 __global__ void __launch_bounds__(kPipeThreads, 1) loss_pipe_kernel(
     int64_t N, const __nv_bfloat16* logits, int64_t ld, int V, const int32_t* __restrict__ tok,
-    const uint8_t* __restrict__ node_mask, int boundary_mode, float gamma, const int32_t* __restrict__ w,
+    const uint8_t* __restrict__ node_mask, int boundary_mode, float gamma, const int32_t* __restrict__ w, const float* __restrict__ wr,
     const int32_t* __restrict__ node, const int32_t* __restrict__ node_start, const int32_t* __restrict__ node_len,
     const int32_t* __restrict__ succ_ptr, const int32_t* __restrict__ succ_tok, __nv_bfloat16* dlogits,
     float* __restrict__ tok_loss, float* __restrict__ ws_loss, float* __restrict__ ws_omega, int32_t* d_err) {
@@ -375,7 +375,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) loss_pipe_kernel(
     for (int k = tid; k < nt; k += kPipeCompute) {
       const int tg = s_y[k];
       const int y = tok[tg];
-      const float om = (float)w[tg];
+      const float om = wr ? wr[tg] : (float)w[tg];
       bad |= (y < 0 || y >= V);
       s_y[k] = y;
       s_om[k] = om;
@@ -538,11 +538,11 @@ tt_status launch_loss(const tt_packed& pk, const __nv_bfloat16* logits, int64_t 
     const size_t smem = (size_t)kRing * kChunkElems * 2 + 2 * kRing * 8;
     cudaFuncSetAttribute(loss_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     loss_pipe_kernel<<<(unsigned)std::min<int64_t>(pk.n_tokens, sms), kPipeThreads, smem, st>>>(
-        pk.n_tokens, logits, ld, vocab, tok, node_mask, boundary_mode, gamma, pk.w, pk.node, pk.node_start,
+        pk.n_tokens, logits, ld, vocab, tok, node_mask, boundary_mode, gamma, pk.w, pk.wr, pk.node, pk.node_start,
         pk.node_len, pk.succ_ptr, pk.succ_tok, dlogits, tok_loss, ws_loss, ws_omega, d_err);
   } else {
     loss_kernel<8><<<(unsigned)grid, kLossThreads, 0, st>>>(pk.n_tokens, logits, ld, vocab, tok, node_mask, boundary_mode,
-                                                            gamma, pk.w, pk.node, pk.node_start, pk.node_len,
+                                                            gamma, pk.w, pk.wr, pk.node, pk.node_start, pk.node_len,
                                                             pk.succ_ptr, pk.succ_tok, dlogits, tok_loss, ws_loss,
                                                             ws_omega, d_err);
   }

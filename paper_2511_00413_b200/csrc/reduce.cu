@@ -56,6 +56,7 @@ __global__ void __launch_bounds__(256) bwd_pre_kernel(const T* __restrict__ o, c
 __global__ void __launch_bounds__(256) bwd_pre_tc_kernel(const __nv_bfloat16* __restrict__ o,
                                                          const __nv_bfloat16* __restrict__ dout,
                                                          const float* __restrict__ lse, const int32_t* __restrict__ w,
+                                                         const float* __restrict__ wr,
                                                          int restore, int64_t N, int64_t Np, int hq,
                                                          float* __restrict__ Dp, float* __restrict__ L2p,
                                                          float* __restrict__ wf, float* __restrict__ dq_acc) {
@@ -83,7 +84,7 @@ __global__ void __launch_bounds__(256) bwd_pre_tc_kernel(const __nv_bfloat16* __
   if (lane == 0) {
     Dp[(int64_t)h * Np + i] = -s;                                              // stored negated
     L2p[(int64_t)h * Np + i] = i < N ? -lse[(int64_t)h * N + i] * kLog2e : 0.f;  // stored negated
-    if (h == 0) wf[i] = i < N ? (restore ? (float)w[i] : 1.f) : 0.f;
+    if (h == 0) wf[i] = i < N ? (restore ? (wr ? wr[i] : (float)w[i]) : 1.f) : 0.f;
   }
 }
 
@@ -181,12 +182,12 @@ tt_status launch_bwd_pre(const void* o, const void* dout, tt_dtype dt, int64_t N
   return check_launch("bwd_pre_kernel");
 }
 
-tt_status launch_bwd_pre_tc(const void* o, const void* dout, const float* lse, const int32_t* w, int restore,
+tt_status launch_bwd_pre_tc(const void* o, const void* dout, const float* lse, const int32_t* w, const float* wr, int restore,
                             int64_t N, int64_t Np, int hq, float* Dp, float* L2p, float* wf, float* dq_acc,
                             cudaStream_t st) {
   const int64_t rows = Np * hq;
   bwd_pre_tc_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>((const __nv_bfloat16*)o, (const __nv_bfloat16*)dout,
-                                                               lse, w, restore, N, Np, hq, Dp, L2p, wf, dq_acc);
+                                                               lse, w, wr, restore, N, Np, hq, Dp, L2p, wf, dq_acc);
   count_launch();
   return check_launch("bwd_pre_tc_kernel");
 }

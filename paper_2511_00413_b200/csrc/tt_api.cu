@@ -1,5 +1,6 @@
 // tt_api.cu — C ABI entry points of libtt.so: argument validation, the O(n_nodes) host part of
 // Tree Packing, workspace carving and kernel dispatch.  See include/tt.h for the contract.
+#include <cmath>
 #include <algorithm>
 #include <cstring>
 #include <vector>
@@ -41,6 +42,7 @@ struct HostPack {
   std::vector<int32_t> start, len, sub_end, depth, leaves;  // per node
   std::vector<int32_t> succ_ptr, succ_tok;                  // per node CSR
   std::vector<int32_t> order, order_start;                  // nodes with len > 0, packed order
+  std::vector<int32_t> pre, kids_ptr, kids;                 // DFS pre-order, children CSR
   int32_t n_roots = 0;
   int64_t n_traj = 0, lin_tokens = 0, pairs = 0, lin_pairs = 0;
 };
@@ -146,9 +148,12 @@ static tt_status host_pack(const int32_t* parent, const int32_t* len, const int3
     }
   }
   H.succ_ptr[n] = (int32_t)H.succ_tok.size();
+  H.kids_ptr.assign(child_cnt.begin(), child_cnt.end());
+  H.kids.swap(kids);
+  H.pre.swap(pre);
   // packed-order list of nodes that own tokens
   H.order.clear(); H.order_start.clear();
-  for (int32_t u : pre)
+  for (int32_t u : H.pre)
     if (len[u] > 0) { H.order.push_back(u); H.order_start.push_back(H.start[u]); }
   return TT_OK;
 }
@@ -298,6 +303,48 @@ tt_status tt_pack(const int32_t* parent, const int32_t* len, const int32_t* term
     info->n_succ = n_succ; info->reserved = 0; info->n_tokens = H.N; info->n_linear_tokens = H.lin_tokens;
     info->n_pairs = H.pairs; info->n_linear_pairs = H.lin_pairs; info->ws_bytes = L.total;
   }
+  return TT_OK;
+}
+
+tt_status tt_pack_weights(const int32_t* parent, const int32_t* len, const int32_t* term, int32_t n_nodes,
+                          const float* traj_weight, tt_packed* pk, float* wr, tt_stream_t stream) {
+  clear_error();
+  if (!pk || !wr || !traj_weight) { set_error("tt_pack_weights: pk, traj_weight and wr must be non-null"); return TT_ERR_INVALID_ARGUMENT; }
+  if ((reinterpret_cast<uintptr_t>(wr) & 15u) != 0) { set_error("tt_pack_weights: wr must be 16-byte aligned"); return TT_ERR_ALIGNMENT; }
+  HostPack H;
+  tt_status s = host_pack(parent, len, term, n_nodes, H);
+  if (s) return s;
+  if (H.n != pk->n_nodes || H.N != pk->n_tokens) {
+    set_error("tt_pack_weights: forest (n=%d, N=%lld) is not the one pk was packed from (n=%d, N=%lld)", H.n,
+              (long long)H.N, pk->n_nodes, (long long)pk->n_tokens);
+    return TT_ERR_INVALID_ARGUMENT;
+  }
+  const int32_t n = H.n;
+  // alpha summed per end node in canonical trajectory order (pre-order, term copies consecutive),
+  // then subtree sums in reverse pre-order, all in fp64
+  std::vector<double> W(n, 0.0);
+  int64_t k = 0;
+  for (int32_t u : H.pre) {
+    const int64_t t = term ? term[u] : ((H.kids_ptr[u + 1] == H.kids_ptr[u]) ? 1 : 0);
+    for (int64_t c = 0; c < t; ++c, ++k) {
+      const float a = traj_weight[k];
+      if (!std::isfinite(a)) { set_error("tt_pack_weights: traj_weight[%lld] is not finite", (long long)k); return TT_ERR_INVALID_ARGUMENT; }
+      W[u] += (double)a;
+    }
+  }
+  for (int32_t t = n - 1; t >= 0; --t) {
+    const int32_t u = H.pre[t];
+    for (int32_t c = H.kids_ptr[u]; c < H.kids_ptr[u + 1]; ++c) W[u] += W[H.kids[c]];
+  }
+  const int64_t Np = (int64_t)pk->n_blk * kBlock;
+  std::vector<float> img((size_t)Np, 0.f);
+  for (int32_t u = 0; u < n; ++u) {
+    const float wu = (float)W[u];
+    for (int32_t i = H.start[u]; i < H.start[u] + H.len[u]; ++i) img[i] = wu;
+  }
+  cudaError_t e = cudaMemcpyAsync(wr, img.data(), img.size() * 4, cudaMemcpyHostToDevice, as_cuda(stream));
+  if (e != cudaSuccess) { set_error("tt_pack_weights: H2D copy failed: %s", cudaGetErrorString(e)); return TT_ERR_CUDA; }
+  pk->wr = wr;
   return TT_OK;
 }
 
