@@ -36,6 +36,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "tree-attn fwd+bwd effective TFLOP/s & % BF16 peak; speedup vs per-branch linear"
+LOSS_KERNEL = "loss_cluster_kernel"
 VOCAB = 151936
 
 
@@ -474,26 +475,40 @@ def main():
             result["per_op_ms"] = {k: round(v, 4) for k, v in per_op.items()}
             attn_ms = per_op["fwd"] + per_op["bwd"]
             result["attn_fwd_bwd_tflops"] = round(j0.flops() / (attn_ms * 1e-3) / 1e12, 2)
-            bwd_fl = 10.0 * j0.d * j0.hq * info["n_pairs"]
-            ach = bwd_fl / (per_op["bwd"] * 1e-3) / 1e12
-            traffic = None
-            prof = os.path.join(ROOT, "profiles", "ncu_bwd_summary.json")
+            traffic = {}
+            prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
             if os.path.exists(prof):
                 try:
-                    traffic = json.load(open(prof)).get(args.config, {}).get("dram_bytes_per_launch")
+                    traffic = json.load(open(prof)).get(args.config, {})
                 except Exception:
-                    traffic = None
-            result["roofline"] = {"bound": "tensor", "kernel": "tt_attn_bwd (bwd_pre + tree_attn_bwd_sm100 + dq_convert)",
-                                  "achieved": round(ach, 2), "peak": peaks["bf16"], "unit": "TFLOP/s",
-                                  "frac": round(ach / peaks["bf16"], 4), "traffic": traffic,
-                                  "peak_source": peaks["source"] + ", dense bf16 burst",
-                                  "frac_of_sustained": round(ach / peaks["bf16_sustained"], 4),
-                                  "algorithmic": "10 d Hq A FLOPs per launch (A = ancestor pairs)"}
+                    traffic = {}
+            # candidates for the dominant kernel of the step: attention bwd (tensor) and loss (HBM);
+            # algorithmic work per launch / event-timed launch duration
+            bwd_fl = 10.0 * j0.d * j0.hq * info["n_pairs"]
+            ach = bwd_fl / (per_op["bwd"] * 1e-3) / 1e12
+            cand = {"bwd": {"bound": "tensor", "kernel": "tt_attn_bwd (bwd_pre + tree_attn_bwd_sm100 + dq_convert)",
+                            "achieved": round(ach, 2), "peak": peaks["bf16"], "unit": "TFLOP/s",
+                            "frac": round(ach / peaks["bf16"], 4),
+                            "traffic": traffic.get("tree_attn_bwd_sm100"),
+                            "peak_source": peaks["source"] + ", dense bf16 burst",
+                            "frac_of_sustained": round(ach / peaks["bf16_sustained"], 4),
+                            "algorithmic": "10 d Hq A FLOPs per launch (A = ancestor pairs)",
+                            "ms": round(per_op["bwd"], 4)}}
             if with_loss:
                 lb = info["n_tokens"] * (4 * VOCAB + 12)
-                result["loss_hbm"] = {"bound": "hbm", "achieved": round(lb / (per_op["loss"] * 1e-3) / 1e9, 1),
-                                      "peak": peaks["hbm"], "unit": "GB/s",
-                                      "frac": round(lb / (per_op["loss"] * 1e-3) / 1e9 / peaks["hbm"], 4)}
+                gbs = lb / (per_op["loss"] * 1e-3) / 1e9
+                cand["loss"] = {"bound": "hbm", "kernel": "tt_restore_loss (" + LOSS_KERNEL + " + loss_sum_kernel)",
+                                "achieved": round(gbs, 1), "peak": peaks["hbm"], "unit": "GB/s",
+                                "frac": round(gbs / peaks["hbm"], 4), "traffic": traffic.get(LOSS_KERNEL),
+                                "peak_source": peaks["source"] + ", HBM copy bandwidth",
+                                "algorithmic": "N (4 V + 12) bytes per launch (read + write bf16 logits row, "
+                                               "token id, weight, loss)",
+                                "ms": round(per_op["loss"], 4)}
+            dom = max(cand, key=lambda k: cand[k]["ms"])
+            result["roofline"] = cand[dom]
+            for k in cand:
+                if k != dom:
+                    result["roofline_" + k] = cand[k]
         if e2e:
             result["e2e"] = e2e
         out = result

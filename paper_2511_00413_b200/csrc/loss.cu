@@ -17,8 +17,11 @@
 // traffic is therefore ~4 V bytes / row.  Rows with no target (Omega_t = 0, e.g.
 // the last token of every trajectory) skip both reads and only write zeros.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 #include "tt_internal.cuh"
+#include "sm100_ptx.cuh"
 
 namespace tt {
 namespace {
@@ -523,6 +526,378 @@ __global__ void __launch_bounds__(1024) loss_sum_kernel(int64_t N, const float* 
   if (threadIdx.x == 0) { sums[0] = sa[0]; sums[1] = sb[0]; }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Cluster variant (V % 8 == 0, rows 16-byte aligned): a thread-block cluster of CS CTAs owns one row
+// at a time; CTA c holds the c-th slice of Cq elements of the row in shared memory, so the row is
+// read from HBM exactly once and written exactly once (4 V bytes / row, the §8(d) algorithmic
+// traffic).  Per row: TMA bulk load of the slice (producer warp, NBUF-deep ring) -> pass 1 (max /
+// sum-exp, own-slice target logits) -> the CS partials are exchanged through distributed shared
+// memory (remote stores + remote mbarrier arrivals, no all-thread cluster barrier) -> pass 2
+// overwrites the slice in shared memory with dlogits -> TMA bulk store (producer warp) while the
+// compute warps already work on the next row.
+// ---------------------------------------------------------------------------------------------
+constexpr int kLcGroup = 256;                      // threads per compute group
+constexpr int kLcThreads = 2 * kLcGroup + 64;      // 2 compute groups + producer warp + meta warp
+constexpr int kLcSlots = 4;                        // exchange slots (row it uses it % 4)
+
+struct LcArgs {
+  int64_t N;
+  const __nv_bfloat16* logits;
+  int64_t ld;
+  int V, Cq, max_t;
+  const int32_t* tok;
+  const uint8_t* node_mask;
+  int boundary_mode;
+  float gamma;
+  const int32_t* w;
+  const float* wr;
+  const int32_t *node, *node_start, *node_len, *succ_ptr, *succ_tok;
+  __nv_bfloat16* dlogits;
+  float *tok_loss, *ws_loss, *ws_omega;
+  int32_t* d_err;
+};
+
+__device__ __forceinline__ uint32_t lc_rank() { uint32_t r; asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r)); return r; }
+__device__ __forceinline__ uint32_t lc_cid() { uint32_t r; asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r)); return r; }
+__device__ __forceinline__ uint32_t lc_ncl() { uint32_t r; asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r)); return r; }
+__device__ __forceinline__ uint32_t lc_mapa(uint32_t a, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void lc_cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void lc_wait_cluster(uint64_t* b, uint32_t ph) {
+  asm volatile("{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n@!p bra W_%=;\n}\n" ::"r"(
+                   smem_addr(b)),
+               "r"(ph)
+               : "memory");
+}
+
+// per-row metadata slot written by the meta warp: [nt, Omega, bad, pad] + y[max_t] + om[max_t] + xy[max_t]
+struct LcMeta {
+  int* hdr;
+  int* y;
+  float* om;
+  float* xy;
+};
+__device__ __forceinline__ LcMeta lc_meta(uint8_t* base, int slot, int max_t) {
+  uint8_t* p = base + (size_t)slot * (16 + (size_t)max_t * 12);
+  LcMeta m;
+  m.hdr = reinterpret_cast<int*>(p);
+  m.y = reinterpret_cast<int*>(p + 16);
+  m.om = reinterpret_cast<float*>(m.y + max_t);
+  m.xy = m.om + max_t;
+  return m;
+}
+
+// KPOLY: pairs (of 4 per 8-element vector) whose pass-2 exponentials run on the FMA pipe
+template <int CS, int NBUF, int KPOLY>
+__global__ void __launch_bounds__(kLcThreads, 1) loss_cluster_kernel(const LcArgs a) {
+  extern __shared__ __align__(128) uint8_t lsm[];
+  const int Cq = a.Cq;
+  __nv_bfloat16* bufs = reinterpret_cast<__nv_bfloat16*>(lsm);                     // NBUF x Cq bf16
+  float4* slots = reinterpret_cast<float4*>(lsm + (size_t)NBUF * Cq * 2);        // [kLcSlots][CS]
+  uint64_t* full = reinterpret_cast<uint64_t*>(slots + kLcSlots * CS);           // [NBUF] slice loaded
+  uint64_t* done = full + NBUF;                                                   // [NBUF] dlogits ready
+  uint64_t* mfull = done + NBUF;                                                  // [NBUF] metadata ready
+  uint64_t* mfree = mfull + NBUF;                                                 // [NBUF] metadata consumed
+  uint64_t* xchg = mfree + NBUF;                                                  // [kLcSlots]
+  uint8_t* meta_base = reinterpret_cast<uint8_t*>(xchg + kLcSlots);
+  __shared__ float s_red[2][3][kLcGroup / 32];
+  __shared__ float s_lse[2];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t cr = lc_rank();
+  const int64_t row0 = lc_cid(), rstep = lc_ncl();
+  const int off = (int)cr * Cq;
+  const int n = max(0, min(Cq, a.V - off));  // elements of this CTA's slice (multiple of 8)
+  if (tid == 0) {
+    for (int k = 0; k < NBUF; ++k) {
+      mbar_init_(&full[k], 1);
+      mbar_init_(&done[k], 1);
+      mbar_init_(&mfull[k], 1);
+      mbar_init_(&mfree[k], 1);
+    }
+    for (int k = 0; k < kLcSlots; ++k) mbar_init_(&xchg[k], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  lc_cluster_sync();  // peers' barriers initialised before any remote arrival
+
+  if (warp == 2 * kLcGroup / 32) {
+    // ===================== producer warp: loads and stores of this CTA's slices =====================
+    if (lane == 0) {
+      uint64_t pol;
+      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+      auto load = [&](int b, int64_t row) {
+        if (n > 0) {
+          mbar_expect_(&full[b], (uint32_t)n * 2);
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+                  smem_addr(bufs + (size_t)b * Cq)),
+              "l"(a.logits + row * a.ld + off), "r"(n * 2), "r"(smem_addr(&full[b])), "l"(pol)
+              : "memory");
+        } else {
+          mbar_arrive_(&full[b]);
+        }
+      };
+      for (int j = 0; j < NBUF; ++j) {
+        const int64_t row = row0 + j * rstep;
+        if (row >= a.N) break;
+        load(j, row);
+      }
+      int it = 0;
+      for (int64_t row = row0; row < a.N; row += rstep, ++it) {
+        const int b = it % NBUF;
+        mbar_wait_(&done[b], (uint32_t)((it / NBUF) & 1));
+        if (n > 0) {
+          asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(
+                           a.dlogits + row * a.ld + off),
+                       "r"(smem_addr(bufs + (size_t)b * Cq)), "r"(n * 2), "l"(pol)
+                       : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        const int64_t nrow = row + (int64_t)NBUF * rstep;
+        if (nrow < a.N) {
+          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // slice b free again
+          load(b, nrow);
+        }
+      }
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    }
+    __syncwarp();
+    lc_cluster_sync();  // no CTA leaves while a peer may still write into its shared memory
+    return;
+  }
+  if (warp == 2 * kLcGroup / 32 + 1) {
+    // ===================== meta warp: targets / weights of upcoming rows (R7, R17, boundary) =====================
+    int it = 0;
+    for (int64_t row = row0; row < a.N; row += rstep, ++it) {
+      const int b = it % NBUF;
+      if (it >= NBUF) mbar_wait_(&mfree[b], (uint32_t)(((it / NBUF) - 1) & 1));
+      LcMeta M = lc_meta(meta_base, b, a.max_t);
+      int nt = 0;
+      if (lane == 0) {
+        const int32_t u = a.node[row];
+        const bool last = row == (int64_t)a.node_start[u] + a.node_len[u] - 1;
+        if (!last) {
+          const int64_t tg = row + 1;
+          if (!a.node_mask || a.node_mask[a.node[tg]]) { M.y[0] = (int)tg; nt = 1; }
+        } else {
+          const int sb = a.succ_ptr[u], se = a.succ_ptr[u + 1];
+          if (!(a.boundary_mode == 1 && se - sb > 1)) {
+            for (int k = sb; k < se; ++k) {
+              const int tg = a.succ_tok[k];
+              if (!a.node_mask || a.node_mask[a.node[tg]]) M.y[nt++] = tg;
+            }
+          }
+        }
+      }
+      nt = __shfl_sync(0xffffffffu, nt, 0);
+      __syncwarp();
+      float om_part = 0.f;
+      int bad = 0;
+      for (int k = lane; k < nt; k += 32) {
+        const int tg = M.y[k];
+        const int y = a.tok[tg];
+        const float om = a.wr ? a.wr[tg] : (float)a.w[tg];
+        bad |= (y < 0 || y >= a.V);
+        M.y[k] = y;
+        M.om[k] = om;
+        om_part += om;
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        om_part += __shfl_xor_sync(0xffffffffu, om_part, o);
+        bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+      }
+      __syncwarp();  // every lane's y / om writes happen-before lane 0's release below
+      if (lane == 0) {
+        M.hdr[0] = nt;
+        reinterpret_cast<float*>(M.hdr)[1] = om_part;
+        M.hdr[2] = bad;
+        mbar_arrive_(&mfull[b]);  // release: the slot's writes above precede the arrival
+      }
+      __syncwarp();
+    }
+    lc_cluster_sync();
+    return;
+  }
+
+  // ===================== compute groups: group g takes rows it = g, g + 2, ... =====================
+  const int grp = warp / (kLcGroup / 32);
+  const int gt = tid - grp * kLcGroup, gw = gt >> 5;
+  auto bar_g = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "n"(kLcGroup) : "memory"); };
+  int it = grp;
+  for (int64_t row = row0 + grp * rstep; row < a.N; row += 2 * rstep, it += 2) {
+    const int b = it % NBUF;
+    const int xs_slot = it % kLcSlots;
+    mbar_wait_(&mfull[b], (uint32_t)((it / NBUF) & 1));
+    LcMeta M = lc_meta(meta_base, b, a.max_t);
+    const int nt = M.hdr[0];
+    const float Omega = reinterpret_cast<const float*>(M.hdr)[1];
+    const bool bad_any = M.hdr[2] != 0;
+    // ---- pass 1 over this CTA's slice in shared memory ----
+    mbar_wait_(&full[b], (uint32_t)((it / NBUF) & 1));
+    __nv_bfloat16* xs = bufs + (size_t)b * Cq;
+    const uint4* x4 = reinterpret_cast<const uint4*>(xs);
+    float m = -INFINITY, sum = 0.f;
+    for (int v = gt; v < n / 8; v += kLcGroup) {
+      const uint4 q = x4[v];
+      Vec<8> r;
+      r.u[0] = q.x; r.u[1] = q.y; r.u[2] = q.z; r.u[3] = q.w;
+      accum<8>(m, sum, r);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const float m2 = __shfl_xor_sync(0xffffffffu, m, o);
+      const float s2 = __shfl_xor_sync(0xffffffffu, sum, o);
+      const float mm = fmaxf(m, m2);
+      sum = (mm == -INFINITY) ? 0.f : sum * ex2f(m - mm) + s2 * ex2f(m2 - mm);
+      m = mm;
+    }
+    // target logits that live in this slice (read before pass 2 overwrites them)
+    float tx = 0.f;
+    for (int k = gt; k < nt; k += kLcGroup) {
+      const int y = M.y[k];
+      if (y >= off && y < off + n) {
+        const float xy = __bfloat162float(xs[y - off]);
+        M.xy[k] = xy;
+        tx += M.om[k] * xy;
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) tx += __shfl_xor_sync(0xffffffffu, tx, o);
+    if (lane == 0) { s_red[grp][0][gw] = m; s_red[grp][1][gw] = sum; s_red[grp][2][gw] = tx; }
+    bar_g();
+    if (gt == 0) {
+      float Mx = -INFINITY, S = 0.f, TX = 0.f;
+      for (int k = 0; k < kLcGroup / 32; ++k) {
+        const float m2 = s_red[grp][0][k], s2 = s_red[grp][1][k];
+        const float mm = fmaxf(Mx, m2);
+        S = (mm == -INFINITY) ? 0.f : S * ex2f(Mx - mm) + s2 * ex2f(m2 - mm);
+        Mx = mm;
+        TX += s_red[grp][2][k];
+      }
+      // ---- exchange (M, S, TX) with the CS CTAs of the cluster through DSMEM ----
+      // st.async: remote 16-byte store that completes as transaction bytes on the receiver's mbarrier
+      // (no release/acquire fences on the critical path); each receiver arms CS x 16 bytes.
+      const uint32_t my_slot = smem_addr(&slots[xs_slot * CS + cr]);
+      const uint32_t my_bar = smem_addr(&xchg[xs_slot]);
+#pragma unroll
+      for (int c = 0; c < CS; ++c)
+        asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
+                         lc_mapa(my_slot, (uint32_t)c)),
+                     "f"(Mx), "f"(S), "f"(TX), "f"(0.f), "r"(lc_mapa(my_bar, (uint32_t)c))
+                     : "memory");
+      mbar_expect_(&xchg[xs_slot], (uint32_t)(CS * 16));
+      mbar_wait_(&xchg[xs_slot], (uint32_t)((it / kLcSlots) & 1));
+      float GM = -INFINITY, GS = 0.f, GT = 0.f;
+      for (int c = 0; c < CS; ++c) {
+        const float4 sv = slots[xs_slot * CS + c];
+        const float mm = fmaxf(GM, sv.x);
+        GS = (mm == -INFINITY) ? 0.f : GS * ex2f(GM - mm) + sv.y * ex2f(sv.x - mm);
+        GM = mm;
+        GT += sv.z;
+      }
+      const float lse2 = GM + log2f(GS);
+      s_lse[grp] = lse2;
+      if (cr == 0) {
+        const float lv = bad_any ? __int_as_float(0x7fc00000) : (Omega == 0.f ? 0.f : Omega * lse2 * kLn2 - GT);
+        if (bad_any && a.d_err) atomicExch(a.d_err, 1);
+        a.ws_loss[row] = lv;
+        a.ws_omega[row] = bad_any ? 0.f : Omega;
+        if (a.tok_loss) a.tok_loss[row] = lv;
+      }
+    }
+    bar_g();
+    const float lse2 = s_lse[grp];
+    const float gO = bad_any ? 0.f : a.gamma * Omega;
+    // ---- pass 2: dlogits = gamma Omega softmax, in place in shared memory ----
+    uint4* y4 = reinterpret_cast<uint4*>(xs);
+    for (int v = gt; v < n / 8; v += kLcGroup) {
+      const uint4 q = y4[v];
+      const uint32_t in[4] = {q.x, q.y, q.z, q.w};
+      uint32_t o[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const float2 f = bf2f(in[t]);
+        if (t >= 4 - KPOLY) {  // part of the exponentials on the FMA pipe (degree-3 polynomial, rel. err ~1e-4 << bf16)
+          const float2 e = sm100::exp2_poly2(sm100::ffma2(f, make_float2(kLog2e, kLog2e), make_float2(-lse2, -lse2)));
+          o[t] = f2bf(gO * e.x, gO * e.y);
+        } else {
+          o[t] = f2bf(gO * ex2f(fmaf(f.x, kLog2e, -lse2)), gO * ex2f(fmaf(f.y, kLog2e, -lse2)));
+        }
+      }
+      y4[v] = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+    bar_g();
+    // ---- fix-up of the target entries of this slice: gamma (Omega p_y - sum_{k: y_k = y} omega_k) ----
+    if (!bad_any) {
+      for (int k = gt; k < nt; k += kLcGroup) {
+        const int y = M.y[k];
+        if (y < off || y >= off + n) continue;
+        bool first = true;
+        float om_y = 0.f;
+        for (int k2 = 0; k2 < nt; ++k2) {
+          if (M.y[k2] == y) {
+            if (k2 < k) first = false;
+            om_y += M.om[k2];
+          }
+        }
+        if (first) {
+          const float py = ex2f(fmaf(M.xy[k], kLog2e, -lse2));
+          xs[y - off] = __float2bfloat16_rn(a.gamma * (Omega * py - om_y));
+        }
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> TMA store
+    bar_g();
+    if (gt == 0) {
+      mbar_arrive_(&done[b]);
+      mbar_arrive_(&mfree[b]);
+    }
+  }
+  lc_cluster_sync();
+}
+
+template <int CS, int NBUF>
+size_t lc_smem(int Cq, int max_t) {
+  return (size_t)NBUF * Cq * 2 + kLcSlots * CS * 16 + (4 * NBUF + kLcSlots) * 8 + (size_t)NBUF * (16 + (size_t)max_t * 12);
+}
+
+template <int CS, int NBUF, int KPOLY = 1>
+bool try_launch_cluster(const LcArgs& a0, int sms, cudaStream_t st) {
+  LcArgs a = a0;
+  a.Cq = ((a.V + CS - 1) / CS + 7) / 8 * 8;
+  const size_t smem = lc_smem<CS, NBUF>(a.Cq, a.max_t);
+  if (smem + 1024 > 232448) return false;  // static shared memory + margin
+  auto kern = loss_cluster_kernel<CS, NBUF, KPOLY>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(CS * std::max(1, sms / CS)));
+  cfg.blockDim = dim3(kLcThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CS;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int ncl = 0;
+  if (cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg) != cudaSuccess || ncl <= 0) {
+    cudaGetLastError();
+    return false;
+  }
+  const int64_t want = std::min<int64_t>((int64_t)ncl, a.N);
+  if (getenv("TT_LOSS_DEBUG")) fprintf(stderr, "loss_cluster<%d,%d>: %d active clusters, Cq %d, smem %zu\n", CS, NBUF, ncl, a.Cq, smem);
+  cfg.gridDim = dim3((unsigned)(want * CS));
+  return cudaLaunchKernelEx(&cfg, kern, a) == cudaSuccess;
+}
+
 }  // namespace
 
 tt_status launch_loss(const tt_packed& pk, const __nv_bfloat16* logits, int64_t ld, int vocab, const int32_t* tok,
@@ -534,7 +909,21 @@ tt_status launch_loss(const tt_packed& pk, const __nv_bfloat16* logits, int64_t 
   // 1 CTA (1024 threads) per SM: 148 rows (~44 MB at V = 151,936) in flight, so pass 2 re-reads from L2
   const int64_t grid = std::min<int64_t>(pk.n_tokens, (int64_t)sms);
   const bool v16 = (ld % 16 == 0) && ((reinterpret_cast<uintptr_t>(logits) | reinterpret_cast<uintptr_t>(dlogits)) % 32 == 0);
-  if (v16) {
+  static const int variant = [] {
+    const char* e = getenv("TT_LOSS_VARIANT");  // development A/B: 0 ring/L2 kernel, 1 CS4x3 (else CS4x2), 2 CS4x2, 3 CS8x4
+    return e ? atoi(e) : 1;
+  }();
+  bool done = false;
+  if (variant != 0 && vocab % 8 == 0) {
+    LcArgs a{pk.n_tokens, logits, ld, vocab, 0, 0, tok, node_mask, boundary_mode, gamma, pk.w, pk.wr,
+             pk.node, pk.node_start, pk.node_len, pk.succ_ptr, pk.succ_tok, dlogits, tok_loss, ws_loss, ws_omega, d_err};
+    a.max_t = std::max(1, pk.max_succ);
+    if (variant == 1) done = try_launch_cluster<4, 3>(a, sms, st);  // fits while max_succ is small
+    else if (variant == 3) done = try_launch_cluster<8, 4>(a, sms, st);
+    if (!done) done = try_launch_cluster<4, 2>(a, sms, st);
+  }
+  if (done) {
+  } else if (v16) {
     const size_t smem = (size_t)kRing * kChunkElems * 2 + 2 * kRing * 8;
     cudaFuncSetAttribute(loss_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     loss_pipe_kernel<<<(unsigned)std::min<int64_t>(pk.n_tokens, sms), kPipeThreads, smem, st>>>(

@@ -125,3 +125,38 @@ def test_sqnorm3_matches_single(tt):
     torch.cuda.synchronize()
     for k in range(3):
         assert out[k].item() == singles[k].item()
+
+
+@pytest.mark.parametrize("V", [8, 64, 4104, 262144], ids=lambda v: f"V{v}")
+def test_loss_kernel_paths(tt, V):
+    """Every loss kernel path against the oracle: the 4-CTA cluster kernel (V % 8 == 0, slices in
+    shared memory; V = 8 leaves three CTAs of each cluster with empty slices), and the L2 ring
+    kernel when a slice no longer fits shared memory (V = 262,144)."""
+    t = trees.gen_agentic(300, root_len=50, seed=4)
+    _compare(tt, t, V=V, gamma=1.5, inplace=(V == 4104), seed=V % 97)
+
+
+def test_loss_many_continuations(tt):
+    """A node with 300 continuations (300-entry target lists in the cluster kernel's per-row
+    metadata) with a target-side node mask, and repeated target token ids at the branch point."""
+    import torch
+    par = [-1] + [0] * 300 + [1, 1]
+    ln = [40] + [2] * 300 + [3, 4]
+    t = trees.Tree(par, ln)
+    mask = np.ones(len(par), np.uint8)
+    mask[5:40] = 0
+    _compare(tt, t, V=2048, node_mask=mask, seed=3)
+    # repeated target ids at the branch point: all continuations start with the same token
+    pk = tt.tt_pack(t.parent, t.length)
+    N, V = pk.n_tokens, 512
+    x = tensors.logits_tensor(N, V, seed=8)
+    tok = tensors.token_ids(N, V, seed=9)
+    starts = pk.arrays()["node_start"].cpu().numpy()
+    tok[torch.as_tensor(starts[1:301].astype(np.int64))] = 7
+    sums, dl, _, err = tt.tt_restore_loss(pk, x.cuda(), tok.cuda())
+    torch.cuda.synchronize()
+    opk = oracle.pack(t.parent, t.length)
+    lr, om, dx = oracle.loss(opk, tok.numpy(), V, np.arange(N), x)
+    g = to64(dl.cpu())
+    assert np.all(np.abs(g - dx) <= 2.0 ** -8 * np.abs(dx) + 1e-5 * np.maximum(om, 1.0)[:, None])
+    assert abs(sums.cpu()[0].item() - lr.sum()) <= 1e-5 * max(1.0, abs(lr.sum()))
