@@ -367,8 +367,8 @@ def main():
     from paper_2511_00413_b200 import sharding
 
     def do_step(ev=None, h2d=False):
-        for j in jobs:
-            run_step(j, ev=ev if len(jobs) == 1 else None, h2d=h2d)
+        for i, j in enumerate(jobs):
+            run_step(j, ev=None if ev is None else ev[i], h2d=h2d)
         if world > 1:
             # a6: one NCCL all_gather of the fixed-size per-tree fp64 records; every rank then
             # sums them in tree-id order (identical totals at every world size)
@@ -384,7 +384,8 @@ def main():
 
     # ---- timed device region ----
     names = ["pack", "fwd", "loss", "bwd", "scal"]
-    evs = [{n: (torch.cuda.Event(True), torch.cuda.Event(True)) for n in names} for _ in range(args.steps)]
+    # per (step, tree) event pairs around each op: per-op times are summed over the rank's trees
+    evs = [[{n: (torch.cuda.Event(True), torch.cuda.Event(True)) for n in names} for _ in jobs] for _ in range(args.steps)]
     step_ev = [(torch.cuda.Event(True), torch.cuda.Event(True)) for _ in range(args.steps)]
     sampler = ClockSampler(local)
     if world > 1:
@@ -406,11 +407,10 @@ def main():
     step_ms = [a.elapsed_time(b) for a, b in step_ev]
     my_ms = float(sum(step_ms))
     per_op = {}
-    if len(jobs) == 1:
-        for n in names:
-            if n == "loss" and not with_loss:
-                continue
-            per_op[n] = float(np.mean([e[n][0].elapsed_time(e[n][1]) for e in evs]))
+    for n in names:
+        if n == "loss" and not with_loss:
+            continue
+        per_op[n] = float(np.mean([sum(e[n][0].elapsed_time(e[n][1]) for e in es) for es in evs]))
     flops_mine = sum(j.flops() for j in jobs) * args.steps
     t_max = my_ms
     flops_all = flops_mine
@@ -473,8 +473,13 @@ def main():
         }
         if per_op:
             result["per_op_ms"] = {k: round(v, 4) for k, v in per_op.items()}
+            if len(jobs) > 1:
+                result["per_op_ms"]["note"] = f"summed over the rank's {len(jobs)} trees (rank 0)"
             attn_ms = per_op["fwd"] + per_op["bwd"]
-            result["attn_fwd_bwd_tflops"] = round(j0.flops() / (attn_ms * 1e-3) / 1e12, 2)
+            my_flops = sum(j.flops() for j in jobs)
+            my_pairs = sum(j.info["n_pairs"] for j in jobs)
+            my_rows = sum(j.info["n_tokens"] for j in jobs)
+            result["attn_fwd_bwd_tflops"] = round(my_flops / (attn_ms * 1e-3) / 1e12, 2)
             traffic = {}
             prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
             if os.path.exists(prof):
@@ -484,9 +489,10 @@ def main():
                     traffic = {}
             # candidates for the dominant kernel of the step: attention bwd (tensor) and loss (HBM);
             # algorithmic work per launch / event-timed launch duration
-            bwd_fl = 10.0 * j0.d * j0.hq * info["n_pairs"]
+            bwd_fl = 10.0 * j0.d * j0.hq * my_pairs
             ach = bwd_fl / (per_op["bwd"] * 1e-3) / 1e12
-            cand = {"bwd": {"bound": "tensor", "kernel": "tt_attn_bwd (bwd_pre + tree_attn_bwd_sm100 + dq_convert)",
+            per_launch = "" if len(jobs) == 1 else f" (mean over the rank's {len(jobs)} launches)"
+            cand = {"bwd": {"bound": "tensor", "kernel": "tt_attn_bwd (bwd_pre + tree_attn_bwd_sm100 + dq_convert)" + per_launch,
                             "achieved": round(ach, 2), "peak": peaks["bf16"], "unit": "TFLOP/s",
                             "frac": round(ach / peaks["bf16"], 4),
                             "traffic": traffic.get("tree_attn_bwd_sm100"),
@@ -495,9 +501,9 @@ def main():
                             "algorithmic": "10 d Hq A FLOPs per launch (A = ancestor pairs)",
                             "ms": round(per_op["bwd"], 4)}}
             if with_loss:
-                lb = info["n_tokens"] * (4 * VOCAB + 12)
+                lb = my_rows * (4 * VOCAB + 12)
                 gbs = lb / (per_op["loss"] * 1e-3) / 1e9
-                cand["loss"] = {"bound": "hbm", "kernel": "tt_restore_loss (" + LOSS_KERNEL + " + loss_sum_kernel)",
+                cand["loss"] = {"bound": "hbm", "kernel": "tt_restore_loss (" + LOSS_KERNEL + " + loss_sum_kernel)" + per_launch,
                                 "achieved": round(gbs, 1), "peak": peaks["hbm"], "unit": "GB/s",
                                 "frac": round(gbs / peaks["hbm"], 4), "traffic": traffic.get(LOSS_KERNEL),
                                 "peak_source": peaks["source"] + ", HBM copy bandwidth",

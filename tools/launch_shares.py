@@ -9,7 +9,7 @@ import re
 import sys
 from collections import OrderedDict
 
-OURS = ("pack_fill_kernel", "pack_tiles_kernel", "tree_attn_fwd_sm100", "loss_pipe_kernel", "loss_kernel",
+OURS = ("pack_fill_kernel", "pack_tiles_kernel", "tree_attn_fwd_sm100", "loss_cluster_kernel", "loss_pipe_kernel", "loss_kernel",
         "loss_sum_kernel", "bwd_pre_tc_kernel", "tree_attn_bwd_sm100", "dq_convert_kernel",
         "sqnorm_partial_kernel", "sum_partials_kernel", "simt_")
 
