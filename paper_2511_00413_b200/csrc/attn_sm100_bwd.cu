@@ -20,15 +20,25 @@
 //                dV += P^T dO      (A = P^T from TMEM)  (M=128, N=128, K=64)
 //                dK += dS^T Q      (A = dS^T from smem) (M=128, N=128, K=64)
 //                dQ^T = K^T dS^T   (A = K^T MN-major)   (M=128 (d), N=64, K=128)
-//              Issue order per tile i: [softmax(i) done] dP(i+1), dV(i), dK(i), dQ(i), S(i+2):
-//              softmax(i+1) overlaps dV/dK/dQ(i); S^T is double buffered, dP^T and dQ^T single.
+//              Issue order per tile i: [P^T(i) ready] dV(i); [dP^T(i) read] dP(i+1);
+//              [dS^T(i) ready] dK(i), dQ(i); S(i+2).  S^T is double buffered, dP^T and dQ^T single.
+//              The element-wise warps run two phases per tile (P from S^T, then dS from dP^T), so the
+//              tensor pipe always has tile i's products or tile i+1's dP queued while they work.
+//              Measured bound (profiles/, tools/mma_rate.cu): shared-memory bandwidth.  Per 64-row
+//              tile the SS MMAs read 192 KB of operands (N = 64 SS MMAs run at 60% of the tensor
+//              peak because their A+B reads need 192 B/clk > 128 B/clk), TMA writes 32 KB, dS^T 16 KB,
+//              the dQ drain 64 KB (stage + TMA read): ~304 KB / 128 B/clk ~ 2400 cycles per tile.
 //   warps 2-9  two warpgroups sharing the 4 TMEM lane quadrants; warpgroup wg owns query columns
 //              [32 wg, 32 wg + 32) of each tile.  Element-wise (one thread per key row): P^T, dS^T
-//              with the tree-scale, P^T -> TMEM (bf16), dS^T -> smem (bf16, SWIZZLE_128B).  Then the
-//              dQ drain of the previous tile (one thread per head-dim lane of dQ^T): transposed
-//              through an 8 KB smem stage per warpgroup and added into the fp32 dQ accumulator
-//              with TMA bulk tensor reductions (cp.reduce.async.bulk.tensor .add.f32).  Epilogue:
-//              warpgroup 0 writes dV, warpgroup 1 writes dK.
+//              with the tree-scale, P^T -> TMEM (bf16), dS^T -> smem (bf16, SWIZZLE_128B).
+//              Epilogue: warpgroup 0 writes dV, warpgroup 1 writes dK.
+//   warps 10-13 dQ drain warpgroup (one thread per head-dim lane of dQ^T): per tile it reads the
+//              64 query columns of dQ^T from TMEM, releases the buffer to the MMA issuer, and adds
+//              them into the fp32 dQ accumulator through two 16 KB smem stages (32 query rows x 128
+//              fp32 each, [row][dim]) with TMA bulk tensor reductions (cp.reduce.async.bulk.tensor
+//              .add.f32).  Measured (TT_PROFILE_COUNTERS): with the drain on the element-wise warps
+//              their per-tile critical path (element-wise ~1250 + drain ~1040 cycles) exceeded the
+//              tensor pipe's ~1790 cycles per tile; on its own warpgroup the drain runs concurrently.
 // TMEM columns: dV 0-127 | dK 128-255 | S^T[2] 256-383 | dP^T 384-447 | dQ^T 448-511.
 #include <cudaTypedefs.h>
 
@@ -53,7 +63,7 @@ using namespace sm100;
 constexpr int kD = 128;
 constexpr int kBQ = 64;
 constexpr int kQStages = 3;
-constexpr int kBwdThreads = 320;
+constexpr int kBwdThreads = 448;   // producer, MMA, 2 element-wise warpgroups, drain warpgroup
 constexpr uint32_t kKVTile = 128 * kD * 2;     // 32 KB (two 16 KB chunks of 128 rows x 128 B)
 constexpr uint32_t kKVChunk = 128 * 64 * 2;    // 16 KB
 constexpr uint32_t kQTile = kBQ * kD * 2;      // 16 KB (two 8 KB chunks of 64 rows x 128 B)
@@ -63,12 +73,12 @@ constexpr uint32_t kOffV = kKVTile;
 constexpr uint32_t kOffQS = 2 * kKVTile;                     // stage s: Q at +s*32K, dO at +s*32K+16K
 constexpr uint32_t kDSTile = 128 * kBQ * 2;
 constexpr uint32_t kOffDS = kOffQS + kQStages * 2 * kQTile;      // dS^T[2], 16 KB each (1024-aligned)
-constexpr uint32_t kOffDQ = kOffDS + 2 * kDSTile;                 // dQ staging: 2 warpgroups x 32 rows x 128 fp32
+constexpr uint32_t kOffDQ = kOffDS + 2 * kDSTile;                 // dQ staging: 2 stages x 32 rows x 128 fp32
 constexpr uint32_t kDQStage = 32 * kD * 4;
 constexpr uint32_t kStatBytes = 768;                              // per stage: -LSE2 | -D | w (256 B each)
 constexpr uint32_t kOffStats = kOffDQ + 2 * kDQStage;
 constexpr uint32_t kOffBar = kOffStats + kQStages * kStatBytes;
-constexpr uint32_t kNumBars = 1 + 2 * kQStages + 8 + 1;
+constexpr uint32_t kNumBars = 1 + 2 * kQStages + 12 + 1;
 constexpr uint32_t kOffMisc = kOffBar + kNumBars * 8;
 // The dynamic shared-memory window is 1024-byte aligned on sm_100 (checked at run time; the kernel
 // traps otherwise), so no alignment slack is reserved.
@@ -112,11 +122,14 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   uint64_t* kv_full = bars;
   uint64_t* q_full = bars + 1;
   uint64_t* q_empty = q_full + kQStages;
-  uint64_t* s_full = q_empty + kQStages;  // [2]
-  uint64_t* sm_done = s_full + 2;         // [2]
-  uint64_t* dq_full = sm_done + 2;        // [2]
+  uint64_t* s_full = q_empty + kQStages;  // [2] S^T(i) in TMEM
+  uint64_t* p_ready = s_full + 2;         // [2] P^T(i) packed back into S^T[b] (256 arrivals)
+  uint64_t* ds_ready = p_ready + 2;       // [2] dS^T(i) in smem (256 arrivals)
+  uint64_t* dq_full = ds_ready + 2;       // [2]
   uint64_t* dq_free = dq_full + 2;        // [2]
-  uint64_t* acc_done = dq_free + 2;
+  uint64_t* dp_full = dq_free + 2;        // dP^T(i) in TMEM
+  uint64_t* dp_free = dp_full + 1;        // dP^T(i) read by the element-wise warps (256 arrivals)
+  uint64_t* acc_done = dp_free + 1;
   uint32_t* misc = reinterpret_cast<uint32_t*>(smem + kOffMisc);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -135,10 +148,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       for (int s = 0; s < kQStages; ++s) { mbar_init(&q_full[s], 1); mbar_init(&q_empty[s], 1); }
       for (int b = 0; b < 2; ++b) {
         mbar_init(&s_full[b], 1);
-        mbar_init(&sm_done[b], 256);
+        mbar_init(&p_ready[b], 256);
+        mbar_init(&ds_ready[b], 256);
         mbar_init(&dq_full[b], 1);
-        mbar_init(&dq_free[b], 256);
+        mbar_init(&dq_free[b], 128);
       }
+      mbar_init(dp_full, 1);
+      mbar_init(dp_free, 256);
       mbar_init(acc_done, 1);
       mbar_fence_init();
     }
@@ -219,35 +235,44 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       };
       long long w_sm = 0, w_dq = 0, w_q = 0, t_start = TT_CLK();
       mbar_wait(kv_full, 0);
-      // prologue: S(0), dP(0) -> s_full[0]; S(1)
+      // prologue: S(0) -> s_full[0], dP(0) -> dp_full, S(1) -> s_full[1]
       mbar_wait(&q_full[0], 0);
       tc_fence_after();
       issue_SP(0);
-      issue_dP(0);
       mma_commit_w(&s_full[0]);
+      issue_dP(0);
+      mma_commit_w(dp_full);
       if (n_it > 1) {
         mbar_wait(&q_full[1], 0);
         tc_fence_after();
         issue_SP(1);
+        mma_commit_w(&s_full[1]);
       }
+      // Per tile i the element-wise warps run two phases: P (needs S^T(i) only) then dS (needs
+      // dP^T(i)).  Each product is issued as soon as its operand is ready, so the tensor pipe works
+      // on tile i's dV / dK / dQ and tile i+1's dP / tile i+2's S while the warps run phase P of the
+      // next tile, and the warps never wait for a product issued after their previous tile finished.
       for (int it = 0; it < n_it; ++it) {
         const int s = it % kQStages, b = it & 1;
         const uint32_t qb = qs0 + s * 2 * kQTile;
         const uint32_t ob = qb + kQTile;
         const uint32_t dsb = ds0 + b * kDSTile;
-        { long long t0 = TT_CLK(); mbar_wait(&sm_done[b], (it >> 1) & 1); w_sm += TT_CLK() - t0; }
+        { long long t0 = TT_CLK(); mbar_wait(&p_ready[b], (it >> 1) & 1); w_sm += TT_CLK() - t0; }
         tc_fence_after();
-        // next tile's dP^T first (single buffer, free once softmax(it) has read it), so that
-        // softmax(it+1) overlaps this tile's dV / dK / dQ products
-        if (it + 1 < n_it) {
-          issue_dP(it + 1);
-          mma_commit_w(&s_full[(it + 1) & 1]);
-        }
         // dV += P^T dO   (A: P^T bf16 in TMEM over S^T[b]; B: dO MN-major, LBO = 8 KB d-chunk)
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)  // P^T of query columns 16 kk.. lives at S^T[b] + 32 (kk / 2) + 8 (kk % 2)
           mma_ts_w(tm + kColDV, tm + kColS + 64 * b + 32 * (kk >> 1) + 8 * (kk & 1), sdesc(ob + kk * 2048, kQChunk, 1024),
                    idVK, (it > 0 || kk > 0) ? 1u : 0u);
+        // next tile's dP^T (single buffer) as soon as the warps have read dP^T(it)
+        if (it + 1 < n_it) {
+          { long long t0 = TT_CLK(); mbar_wait(dp_free, it & 1); w_sm += TT_CLK() - t0; }
+          tc_fence_after();
+          issue_dP(it + 1);
+          mma_commit_w(dp_full);
+        }
+        { long long t0 = TT_CLK(); mbar_wait(&ds_ready[b], (it >> 1) & 1); w_sm += TT_CLK() - t0; }
+        tc_fence_after();
         // dK += dS^T Q   (A: dS^T K-major 128 x 64 in smem; B: Q MN-major)
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
@@ -264,10 +289,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                  idQ, kk > 0);
         mma_commit_w(&dq_full[0]);
         mma_commit_w(&q_empty[s]);
+        // S^T(it+2) into S^T[b] (in issue order after dV(it) read P^T(it) from it)
         if (it + 2 < n_it) {
           { long long t0 = TT_CLK(); mbar_wait(&q_full[(it + 2) % kQStages], ((it + 2) / kQStages) & 1); w_q += TT_CLK() - t0; }
           tc_fence_after();
           issue_SP(it + 2);
+          mma_commit_w(&s_full[b]);
         }
       }
       mma_commit_w(acc_done);
@@ -278,6 +305,64 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         atomicAdd(&g_bwd_dbg[3], (unsigned long long)w_q);
         atomicAdd(&g_bwd_dbg[4], (unsigned long long)n_it);
       }
+    }
+  } else if (warp >= 10) {
+    // ===================== dQ drain warpgroup (warps 10-13) =====================
+    const int q4 = warp & 3;
+    const int r = q4 * 32 + lane;                      // head-dim lane of dQ^T
+    const uint32_t tl = tmem + ((uint32_t)(q4 * 32) << 16);
+    long long c_wd = 0, c_dr = 0;
+    for (int it = 0; it < n_it; ++it) {
+      const int h = hk * p.g + it / nq;
+      const int q0 = (qt0 + it % nq) * kBQ;
+      { long long t0 = TT_CLK(); mbar_wait(&dq_full[0], it & 1); c_wd += TT_CLK() - t0; }
+      long long t_dr = TT_CLK();
+      tc_fence_after();
+      uint32_t v0[32], v1[32];
+      tmem_ld32(tl + kColQ, v0);
+      tmem_ld32(tl + kColQ + 32, v1);
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(&dq_free[0]);
+      if (p.dbg & 1) continue;
+      if (p.dbg & 16) {
+        // variant: coalesced fp32 REDs straight from registers (a warp instruction covers 32
+        // consecutive head dims of one query row = 128 contiguous bytes); no shared-memory staging
+        float* base = p.dq_acc + ((int64_t)q0 * p.hq + h) * kD + r;
+        const int64_t rs = (int64_t)p.hq * kD;
+        const int nv = (int)imin64(64, p.N - q0);
+#pragma unroll
+        for (int c = 0; c < 32; ++c)
+          if (c < nv) red_add_f32(base + c * rs, __uint_as_float(v0[c]) * p.scale);
+#pragma unroll
+        for (int c = 0; c < 32; ++c)
+          if (32 + c < nv) red_add_f32(base + (32 + c) * rs, __uint_as_float(v1[c]) * p.scale);
+        c_dr += TT_CLK() - t_dr;
+        continue;
+      }
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        // stage hh holds query rows [q0 + 32 hh, +32) x 128 dims ([row][dim], scaled fp32); its previous
+        // reduction (one half-tile earlier in issue order) must have finished reading it
+        float* stg = reinterpret_cast<float*>(smem + kOffDQ + hh * kDQStage);
+        if (r == 0) bulk_wait_read<1>();
+        named_bar_sync(1, 128);
+        const uint32_t* vv = hh ? v1 : v0;
+#pragma unroll
+        for (int c = 0; c < 32; ++c) stg[c * kD + r] = __uint_as_float(vv[c]) * p.scale;
+        fence_proxy_async_smem();
+        named_bar_sync(1, 128);
+        if (r == 0) {
+          tma_reduce_add_3d(&tmdQ, stg, 0, h, q0 + 32 * hh);
+          bulk_commit();
+        }
+      }
+      c_dr += TT_CLK() - t_dr;
+    }
+    if (r == 0) bulk_wait<0>();
+    if ((p.dbg & 8) && r == 0) {
+      atomicAdd(&g_bwd_dbg[7], (unsigned long long)c_dr);
+      atomicAdd(&g_bwd_dbg[8], (unsigned long long)c_wd);
     }
   } else {
     // ===================== compute warps 2-9 =====================
@@ -292,33 +377,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const uint32_t tl = tmem + ((uint32_t)(q4 * 32) << 16);
     const int Ej = (j < Nn) ? p.E[j] : -1;
     const float sl2 = p.scale_log2;
-    long long c_ws = 0, c_el = 0, c_dr = 0, c_wd = 0, c_ld = 0, c_math = 0, c_st = 0;
-    auto drain = [&](int it) {
-      const int h = hk * p.g + it / nq;
-      const int q0 = (qt0 + it % nq) * kBQ + 32 * wg;
-      { long long t0 = TT_CLK(); mbar_wait(&dq_full[0], it & 1); c_wd += TT_CLK() - t0; }
-      tc_fence_after();
-      uint32_t v[32];
-      tmem_ld32(tl + kColQ + 32 * wg, v);
-      tmem_wait_ld();
-      tc_fence_before();
-      mbar_arrive(&dq_free[0]);
-      if (p.dbg & 1) return;
-      // stage the warpgroup's 32 query rows x 128 dims (scaled, fp32, [row][dim]) in its own smem
-      // buffer and add them into the fp32 accumulator with one TMA bulk tensor reduction; the
-      // buffer is reused one tile later, so the reduction runs asynchronously for a whole tile
-      float* stg = reinterpret_cast<float*>(smem + kOffDQ + wg * kDQStage);
-      if (r == 0) bulk_wait_read<0>();  // the previous reduction of this warpgroup has read the buffer
-      named_bar_sync(1 + wg, 128);
-#pragma unroll
-      for (int c = 0; c < 32; ++c) stg[c * kD + r] = __uint_as_float(v[c]) * p.scale;
-      fence_proxy_async_smem();
-      named_bar_sync(1 + wg, 128);
-      if (r == 0) {
-        tma_reduce_add_3d(&tmdQ, stg, 0, h, q0);
-        bulk_commit();
-      }
-    };
+    long long c_ws = 0, c_el = 0, c_ld = 0, c_math = 0, c_st = 0;
     for (int it = 0; it < n_it; ++it) {
       const int s = it % kQStages, b = it & 1;
       const int q0 = (qt0 + it % nq) * kBQ;
@@ -327,7 +386,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       long long t_el = TT_CLK();
       if (p.dbg & 4) {
         tc_fence_before();
-        mbar_arrive(&sm_done[b]);
+        mbar_arrive(&p_ready[b]);
+        mbar_wait(dp_full, it & 1);
+        tc_fence_after();
+        tc_fence_before();
+        mbar_arrive(dp_free);
+        mbar_arrive(&ds_ready[b]);
       } else {
         const float4* st_lse = reinterpret_cast<const float4*>(smem + kOffStats + s * kStatBytes);
         const float4* st_D = reinterpret_cast<const float4*>(smem + kOffStats + s * kStatBytes + 256);
@@ -337,79 +401,89 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         // allowed query columns of this key form one interval: [max(j, c0), min(E_j, N)) - c0
         const int lo = max(j - c0, 0), hi = min(min(Ej, Nn) - c0, 32);
         const uint32_t cmask = (hi <= lo) ? 0u : ((hi >= 32 ? 0xffffffffu : ((1u << hi) - 1u)) & ~((1u << lo) - 1u));
-        uint32_t sv[32], pv[32];
-        long long tA = TT_CLK();
-        tmem_ld32(tl + kColS + 64 * b + 32 * wg, sv);
-        tmem_ld32(tl + kColP + 32 * wg, pv);
-        tmem_wait_ld();
-        c_ld += TT_CLK() - tA;
-        tA = TT_CLK();
-        uint32_t pwk[16], dsk[16];
         const bool all_in = __all_sync(0xffffffffu, cmask == 0xffffffffu);
         const float2 SL = make_float2(sl2, sl2);
+        // ---- phase P (S^T only): pw = w P, P^T -> TMEM as bf16 ----
+        float2 pw[16];
+        {
+          uint32_t sv[32], pwk[16];
+          long long tA = TT_CLK();
+          tmem_ld32(tl + kColS + 64 * b + 32 * wg, sv);
+          tmem_wait_ld();
+          c_ld += TT_CLK() - tA;
+          tA = TT_CLK();
 #pragma unroll
-        for (int c4 = 0; c4 < 8; ++c4) {
-          const int cg = 8 * wg + c4;  // float4 group within the 64 columns
-          const float4 NL = st_lse[cg];  // -LSE * log2e
-          const float4 ND = st_D[cg];    // -D
-          const float4 W = st_w[cg];
-          const int c = 4 * c4;
-          // P = 2^(s * scale * log2e - LSE2): columns c, c+1 on the MUFU, c+2, c+3 on the FMA pipe
-          const float2 a01 = ffma2(make_float2(__uint_as_float(sv[c]), __uint_as_float(sv[c + 1])), SL, make_float2(NL.x, NL.y));
-          const float2 a23 = ffma2(make_float2(__uint_as_float(sv[c + 2]), __uint_as_float(sv[c + 3])), SL, make_float2(NL.z, NL.w));
-          float2 p01 = make_float2(ex2(a01.x), ex2(a01.y));
+          for (int c4 = 0; c4 < 8; ++c4) {
+            const int cg = 8 * wg + c4;  // float4 group within the 64 columns
+            const float4 NL = st_lse[cg];  // -LSE * log2e
+            const float4 W = st_w[cg];
+            const int c = 4 * c4;
+            // P = 2^(s * scale * log2e - LSE2): columns c, c+1 on the MUFU, c+2, c+3 on the FMA pipe
+            const float2 a01 = ffma2(make_float2(__uint_as_float(sv[c]), __uint_as_float(sv[c + 1])), SL, make_float2(NL.x, NL.y));
+            const float2 a23 = ffma2(make_float2(__uint_as_float(sv[c + 2]), __uint_as_float(sv[c + 3])), SL, make_float2(NL.z, NL.w));
+            float2 p01 = make_float2(ex2(a01.x), ex2(a01.y));
 #ifndef TT_BWD_POLY
 #define TT_BWD_POLY 1
 #endif
-          // 2 x TT_BWD_POLY of every 8 exponentials run on the FMA pipe
-          float2 p23 = (TT_BWD_POLY == 2 || (TT_BWD_POLY == 1 && (c4 & 1))) ? exp2_poly2(a23)
-                                                                           : make_float2(ex2(a23.x), ex2(a23.y));
-          if (!all_in) {
-            p01.x = ((cmask >> c) & 1u) ? p01.x : 0.f;
-            p01.y = ((cmask >> (c + 1)) & 1u) ? p01.y : 0.f;
-            p23.x = ((cmask >> (c + 2)) & 1u) ? p23.x : 0.f;
-            p23.y = ((cmask >> (c + 3)) & 1u) ? p23.y : 0.f;
+            // 2 x TT_BWD_POLY of every 8 exponentials run on the FMA pipe
+            float2 p23 = (TT_BWD_POLY == 2 || (TT_BWD_POLY == 1 && (c4 & 1))) ? exp2_poly2(a23)
+                                                                             : make_float2(ex2(a23.x), ex2(a23.y));
+            if (!all_in) {
+              p01.x = ((cmask >> c) & 1u) ? p01.x : 0.f;
+              p01.y = ((cmask >> (c + 1)) & 1u) ? p01.y : 0.f;
+              p23.x = ((cmask >> (c + 2)) & 1u) ? p23.x : 0.f;
+              p23.y = ((cmask >> (c + 3)) & 1u) ? p23.y : 0.f;
+            }
+            pw[2 * c4] = fmul2(p01, make_float2(W.x, W.y));
+            pw[2 * c4 + 1] = fmul2(p23, make_float2(W.z, W.w));
+            pwk[2 * c4] = pack_bf16(pw[2 * c4].x, pw[2 * c4].y);
+            pwk[2 * c4 + 1] = pack_bf16(pw[2 * c4 + 1].x, pw[2 * c4 + 1].y);
           }
-          const float2 pw01 = fmul2(p01, make_float2(W.x, W.y));
-          const float2 pw23 = fmul2(p23, make_float2(W.z, W.w));
-          const float2 ds01 = fmul2(pw01, fadd2(make_float2(__uint_as_float(pv[c]), __uint_as_float(pv[c + 1])), make_float2(ND.x, ND.y)));
-          const float2 ds23 = fmul2(pw23, fadd2(make_float2(__uint_as_float(pv[c + 2]), __uint_as_float(pv[c + 3])), make_float2(ND.z, ND.w)));
-          pwk[2 * c4] = pack_bf16(pw01.x, pw01.y);
-          pwk[2 * c4 + 1] = pack_bf16(pw23.x, pw23.y);
-          dsk[2 * c4] = pack_bf16(ds01.x, ds01.y);
-          dsk[2 * c4 + 1] = pack_bf16(ds23.x, ds23.y);
+          // P^T (bf16) over this warpgroup's own S^T[b] columns: [32 wg, 32 wg + 16) — never over
+          // columns the other warpgroup may still be reading
+          tmem_st16(tl + kColS + 64 * b + 32 * wg, pwk);
+          tmem_wait_st();
+          tc_fence_before();
+          mbar_arrive(&p_ready[b]);
+          c_math += TT_CLK() - tA;
         }
-        c_math += TT_CLK() - tA;
-        tA = TT_CLK();
-        // P^T (bf16) over this warpgroup's own S^T[b] columns: [32 wg, 32 wg + 16) — never over
-        // columns the other warpgroup may still be reading
-        tmem_st16(tl + kColS + 64 * b + 32 * wg, pwk);
-        // dS^T row r into the SWIZZLE_128B smem tile: 16-byte chunk c at (c ^ (r & 7))
-        uint8_t* drow = smem + kOffDS + b * kDSTile + r * 128;
+        // ---- phase dS (dP^T): dS^T = pw (dP - D) -> smem ----
+        {
+          uint32_t pv[32], dsk[16];
+          long long tA = TT_CLK();
+          { long long t0 = TT_CLK(); mbar_wait(dp_full, it & 1); c_ws += TT_CLK() - t0; }
+          tc_fence_after();
+          tmem_ld32(tl + kColP + 32 * wg, pv);
+          tmem_wait_ld();
+          tc_fence_before();
+          mbar_arrive(dp_free);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const int ch = 4 * wg + c;
-          *reinterpret_cast<uint4*>(drow + ((ch ^ (r & 7)) << 4)) =
-              make_uint4(dsk[4 * c], dsk[4 * c + 1], dsk[4 * c + 2], dsk[4 * c + 3]);
+          for (int c4 = 0; c4 < 8; ++c4) {
+            const float4 ND = st_D[8 * wg + c4];  // -D
+            const int c = 4 * c4;
+            const float2 ds01 = fmul2(pw[2 * c4], fadd2(make_float2(__uint_as_float(pv[c]), __uint_as_float(pv[c + 1])), make_float2(ND.x, ND.y)));
+            const float2 ds23 = fmul2(pw[2 * c4 + 1], fadd2(make_float2(__uint_as_float(pv[c + 2]), __uint_as_float(pv[c + 3])), make_float2(ND.z, ND.w)));
+            dsk[2 * c4] = pack_bf16(ds01.x, ds01.y);
+            dsk[2 * c4 + 1] = pack_bf16(ds23.x, ds23.y);
+          }
+          // dS^T row r into the SWIZZLE_128B smem tile: 16-byte chunk c at (c ^ (r & 7))
+          uint8_t* drow = smem + kOffDS + b * kDSTile + r * 128;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const int ch = 4 * wg + c;
+            *reinterpret_cast<uint4*>(drow + ((ch ^ (r & 7)) << 4)) =
+                make_uint4(dsk[4 * c], dsk[4 * c + 1], dsk[4 * c + 2], dsk[4 * c + 3]);
+          }
+          fence_proxy_async_smem();
+          mbar_arrive(&ds_ready[b]);
+          c_st += TT_CLK() - tA;
         }
-        tmem_wait_st();
-        fence_proxy_async_smem();
-        tc_fence_before();
-        mbar_arrive(&sm_done[b]);
-        c_st += TT_CLK() - tA;
       }
       c_el += TT_CLK() - t_el;
-      long long t_dr = TT_CLK();
-      if (it > 0) drain(it - 1);
-      c_dr += TT_CLK() - t_dr;
     }
-    drain(n_it - 1);
-    if (r == 0) bulk_wait<0>();
     if ((p.dbg & 8) && r == 0 && wg == 0) {
       atomicAdd(&g_bwd_dbg[5], (unsigned long long)c_ws);
       atomicAdd(&g_bwd_dbg[6], (unsigned long long)c_el);
-      atomicAdd(&g_bwd_dbg[7], (unsigned long long)c_dr);
-      atomicAdd(&g_bwd_dbg[8], (unsigned long long)c_wd);
       atomicAdd(&g_bwd_dbg[9], (unsigned long long)c_ld);
       atomicAdd(&g_bwd_dbg[10], (unsigned long long)c_math);
       atomicAdd(&g_bwd_dbg[11], (unsigned long long)c_st);
