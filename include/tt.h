@@ -265,6 +265,28 @@ tt_status tt_traversal_forest(const int32_t* parent, const int32_t* len, const i
                               const int32_t* traversal_of_traj, int32_t traversal, int32_t* out_parent,
                               int32_t* out_len, int32_t* out_term, int32_t* out_node, int32_t* n_out);
 
+/* --------------------------------------------------------------------------------------
+ * Position-embedding correction (Eq. 23):
+ * RoPE must rotate every token by its RESTORED position pos_i (pk->pos, R4) so that dY/dX is the
+ * same in tree and per-branch packing.  Convention (reading R21): rotate-half over the whole head
+ * dim d, theta_j = base^(-2j/d) for j < d/2, a = pos_i * theta_j,
+ *   y_j = x_j cos a - x_{j+d/2} sin a,   y_{j+d/2} = x_j sin a + x_{j+d/2} cos a.
+ * inverse != 0 rotates by -a (the backward: dX = R(-a) dY).  Angles are reduced mod 2 pi in fp64.
+ * x: DEVICE [N, n_heads, d] (dtype dt, contiguous, 16-byte aligned), rotated IN PLACE.
+ * d in {64, 128}; base > 0 (Qwen3: 1e6).  HBM-bound: reads and writes x once.
+ * -------------------------------------------------------------------------------------- */
+tt_status tt_rope(const tt_packed* pk, void* x, tt_dtype dt, int32_t n_heads, int32_t d, double base,
+                  int32_t inverse, tt_stream_t stream);
+
+/* --------------------------------------------------------------------------------------
+ * Gradient Scaler for an arbitrary upstream gradient ("a gradient scaling step before the
+ * backward propagation"; Fig. 4gradient): g[i, :] *= W_i IN PLACE, W_i = pk->wr[i] when
+ * tt_pack_weights set real weights (R20), else the leaf count pk->w[i] (R5).  After it, every later
+ * backward op runs uncorrected (transitivity, Eqs. 17-21), e.g. tt_attn_bwd(restore=0).
+ * g: DEVICE [N, row_elems] (dtype dt, contiguous, 16-byte aligned, row bytes a multiple of 16).
+ * -------------------------------------------------------------------------------------- */
+tt_status tt_restore_grad(const tt_packed* pk, void* g, tt_dtype dt, int64_t row_elems, tt_stream_t stream);
+
 /* Kernel-level launch counters (for bench.py's gpu_launches claim): number of kernels this
  * thread has launched through the library since the last reset. */
 int64_t tt_launch_count(void);

@@ -94,13 +94,15 @@ def lib():
             L.tt_pack_weights.argtypes = [i32p, i32p, i32p, C.c_int32, C.POINTER(C.c_float), C.POINTER(TTPacked),
                                           vp, st]
             L.tt_traversal_forest.argtypes = [i32p, i32p, i32p, C.c_int32, i32p, C.c_int32, i32p, i32p, i32p, i32p, i32p]
+            L.tt_rope.argtypes = [C.POINTER(TTPacked), vp, C.c_int, C.c_int32, C.c_int32, C.c_double, C.c_int32, st]
+            L.tt_restore_grad.argtypes = [C.POINTER(TTPacked), vp, C.c_int, C.c_int64, st]
             L.tt_launch_count.restype = C.c_int64
             L.tt_launch_count.argtypes = []
             L.tt_launch_count_reset.argtypes = []
             L.tt_launch_count_reset.restype = None
             for fn in ("tt_pack_plan", "tt_pack", "tt_attn_fwd", "tt_attn_bwd_workspace", "tt_attn_bwd",
                        "tt_restore_loss", "tt_grad_sqnorm", "tt_grad_sqnorm3", "tt_plan_traversals",
-                       "tt_traversal_forest"):
+                       "tt_traversal_forest", "tt_rope", "tt_restore_grad"):
                 getattr(L, fn).restype = C.c_int
             _lib = L
     return _lib
@@ -334,6 +336,25 @@ def tt_grad_sqnorm3(x0, x1, x2, out=None, ws=None, stream=None):
                                                 int(x2.numel()), _dt(x0), _p(out), _p(ws), int(ws.numel()),
                                                 _stream(stream)))
     return out
+
+
+def tt_rope(pk: PackedTree, x, base=1.0e6, inverse=False, stream=None):
+    """Rotate x [N, H, d] in place by the restored positions of pk (NEXT-f2, reading R21)."""
+    if not x.is_contiguous() or x.dim() != 3:
+        raise ValueError("x must be a contiguous [N, H, d] tensor")
+    N, H, d = x.shape
+    _check("tt_rope", lib().tt_rope(C.byref(pk.c), _p(x), _dt(x), H, d, float(base), int(bool(inverse)),
+                                    _stream(stream)))
+    return x
+
+
+def tt_restore_grad(pk: PackedTree, g, stream=None):
+    """Gradient Scaler: g[i, ...] *= tree-scale of token i, in place."""
+    if not g.is_contiguous():
+        raise ValueError("g must be contiguous")
+    row = g.numel() // g.shape[0]
+    _check("tt_restore_grad", lib().tt_restore_grad(C.byref(pk.c), _p(g), _dt(g), int(row), _stream(stream)))
+    return g
 
 
 def tt_plan_traversals(parent, length, capacity, term=None):

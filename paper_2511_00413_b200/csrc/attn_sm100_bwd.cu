@@ -109,7 +109,7 @@ struct BwdParams {
   __nv_bfloat16* dv;
 };
 
-__global__ void __launch_bounds__(kBwdThreads, 1)
+__global__ void __maxnreg__(128)
     tree_attn_bwd_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                         const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
                         const __grid_constant__ CUtensorMap tmdQ, const BwdParams p) {

@@ -471,4 +471,23 @@ tt_status tt_grad_sqnorm3(const void* x0, int64_t n0, const void* x1, int64_t n1
   return launch_sqnorm(xs, ns, 3, dt, out, static_cast<double*>(d_ws), as_cuda(stream));
 }
 
+tt_status tt_rope(const tt_packed* pk, void* x, tt_dtype dt, int32_t n_heads, int32_t d, double base,
+                  int32_t inverse, tt_stream_t stream) {
+  clear_error();
+  if (!pk || !x || !pk->pos || n_heads <= 0 || !(base > 0.0)) { set_error("tt_rope: bad argument"); return TT_ERR_INVALID_ARGUMENT; }
+  if (dt != TT_BF16 && dt != TT_FP32) { set_error("tt_rope: bad dtype"); return TT_ERR_INVALID_ARGUMENT; }
+  if (d != 64 && d != 128) { set_error("tt_rope: head_dim %d unsupported (64, 128)", d); return TT_ERR_UNSUPPORTED; }
+  if (!aligned16(x)) { set_error("tt_rope: x must be 16-byte aligned"); return TT_ERR_ALIGNMENT; }
+  return launch_rope(*pk, x, dt, n_heads, d, base, inverse, as_cuda(stream));
+}
+
+tt_status tt_restore_grad(const tt_packed* pk, void* g, tt_dtype dt, int64_t row_elems, tt_stream_t stream) {
+  clear_error();
+  if (!pk || !g || !pk->w || row_elems <= 0) { set_error("tt_restore_grad: bad argument"); return TT_ERR_INVALID_ARGUMENT; }
+  if (dt != TT_BF16 && dt != TT_FP32) { set_error("tt_restore_grad: bad dtype"); return TT_ERR_INVALID_ARGUMENT; }
+  if (row_elems % (dt == TT_BF16 ? 8 : 4)) { set_error("tt_restore_grad: row_elems must be a multiple of 16 bytes"); return TT_ERR_ALIGNMENT; }
+  if (!aligned16(g)) { set_error("tt_restore_grad: g must be 16-byte aligned"); return TT_ERR_ALIGNMENT; }
+  return launch_restore_grad(*pk, g, dt, row_elems, as_cuda(stream));
+}
+
 }  // extern "C"

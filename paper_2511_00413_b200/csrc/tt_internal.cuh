@@ -76,6 +76,10 @@ tt_status launch_loss(const tt_packed& pk, const __nv_bfloat16* logits, int64_t 
 tt_status launch_sqnorm(const void* const* xs, const int64_t* ns, int count, tt_dtype dt, double* out,
                         double* partials, cudaStream_t st);
 
+tt_status launch_rope(const tt_packed& pk, void* x, tt_dtype dt, int H, int d, double base, int inverse,
+                      cudaStream_t st);
+tt_status launch_restore_grad(const tt_packed& pk, void* g, tt_dtype dt, int64_t row_elems, cudaStream_t st);
+
 constexpr int kSqnormBlocks = 296;
 
 }  // namespace tt
