@@ -545,6 +545,33 @@ def main():
                                   "ERR": round(1 - pinfo["planned_tokens"] / pinfo["linear_tokens"], 4),
                                   "POR": round(1 - pinfo["tree_tokens"] / pinfo["linear_tokens"], 4),
                                   "host_plan_ms": round(plan_ms, 4)}
+    if rank == 0:
+        # NEXT-f2: restored-position RoPE on this tree's Q and K, and the Gradient Scaler on its
+        # upstream gradient (HBM-bound: each reads and writes its tensor once), event-timed
+        j0 = jobs[0]
+        pk0 = tt.tt_pack(j0.tree.parent, j0.tree.length)
+        qc, kc, gc = j0.q.clone(), j0.k.clone(), j0.g.clone()
+
+        def _t(fn, reps=10):
+            fn()
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(True), torch.cuda.Event(True)
+            a.record()
+            for _ in range(reps):
+                fn()
+            b.record()
+            torch.cuda.synchronize()
+            return a.elapsed_time(b) / reps
+
+        rope_ms = _t(lambda: (tt.tt_rope(pk0, qc), tt.tt_rope(pk0, kc)))
+        rg_ms = _t(lambda: tt.tt_restore_grad(pk0, gc))
+        rb = 2 * (qc.numel() + kc.numel()) * qc.element_size()
+        gb = 2 * gc.numel() * gc.element_size()
+        out["next_f2"] = {"rope_qk_ms": round(rope_ms, 4), "rope_gbs": round(rb / rope_ms / 1e6, 1),
+                          "restore_grad_ms": round(rg_ms, 4), "restore_grad_gbs": round(gb / rg_ms / 1e6, 1),
+                          "hbm_peak_gbs": peaks["hbm"],
+                          "algorithmic": "read + write of Q and K (rope), of G (restore_grad), bf16"}
+        del qc, kc, gc
     if rank == 0 and world == 1 and not args.no_cpu:
         dt, share, ntraj, cores = oracle_sample(jobs[0].tree, cfg, budget_s=args.cpu_budget)
         full_s = dt / share

@@ -266,6 +266,29 @@ tt_status tt_traversal_forest(const int32_t* parent, const int32_t* len, const i
                               int32_t* out_len, int32_t* out_term, int32_t* out_node, int32_t* n_out);
 
 /* --------------------------------------------------------------------------------------
+ * LM head + Gradient-Restoration cross entropy without materialising [N, V] logits
+ * (P:549 and readings R6-R8, R17, R20 exactly as tt_restore_loss, on logits
+ * X = H W^T computed and kept in fp32):
+ *   loss_t = sum_k omega_k (lse(x_t) - x_t[y_k]),   G_t = gamma (Omega_t softmax(x_t) - sum_k omega_k e_{y_k})
+ *   dH = G W  [N, hidden],   dW = G^T H  [vocab, hidden]
+ * The vocabulary is processed in chunks of vocab_chunk columns (largest temporary [N, vocab_chunk]
+ * fp32 + bf16); logits are computed twice (sweep 1: lse, sweep 2: G), G is rounded to bf16 once as
+ * the operand of the dH / dW GEMMs.  The four GEMMs per chunk are plain cuBLASLt calls (bf16 in,
+ * fp32 compute); the cross-entropy steps are libtt kernels.
+ * h: DEVICE [N, hidden] bf16; w: DEVICE [vocab, hidden] bf16 (row-major, the LM-head weight);
+ * tok / node_loss_mask / boundary_mode / grad_scale / tok_loss / sums / d_err: as tt_restore_loss.
+ * dh: DEVICE [N, hidden] bf16 (written); dw: DEVICE [vocab, hidden] bf16 (written).
+ * d_ws: DEVICE workspace of tt_lmhead_loss_workspace bytes (16-byte aligned), caller-owned.
+ * hidden % 8 == 0.  Errors: as tt_restore_loss; TT_ERR_CUDA if a cuBLASLt call fails.
+ * -------------------------------------------------------------------------------------- */
+tt_status tt_lmhead_loss_workspace(const tt_packed* pk, int32_t hidden, int32_t vocab, int32_t vocab_chunk,
+                                   size_t* bytes);
+tt_status tt_lmhead_loss(const tt_packed* pk, const void* h, const void* w, int32_t hidden, int32_t vocab,
+                         int32_t vocab_chunk, const int32_t* tok, const uint8_t* node_loss_mask, int32_t boundary_mode,
+                         float grad_scale, void* dh, void* dw, float* tok_loss, double* sums, int32_t* d_err,
+                         void* d_ws, size_t ws_bytes, tt_stream_t stream);
+
+/* --------------------------------------------------------------------------------------
  * Position-embedding correction (Eq. 23):
  * RoPE must rotate every token by its RESTORED position pos_i (pk->pos, R4) so that dY/dX is the
  * same in tree and per-branch packing.  Convention (reading R21): rotate-half over the whole head

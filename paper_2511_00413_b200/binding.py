@@ -94,6 +94,10 @@ def lib():
             L.tt_pack_weights.argtypes = [i32p, i32p, i32p, C.c_int32, C.POINTER(C.c_float), C.POINTER(TTPacked),
                                           vp, st]
             L.tt_traversal_forest.argtypes = [i32p, i32p, i32p, C.c_int32, i32p, C.c_int32, i32p, i32p, i32p, i32p, i32p]
+            L.tt_lmhead_loss_workspace.argtypes = [C.POINTER(TTPacked), C.c_int32, C.c_int32, C.c_int32,
+                                                   C.POINTER(C.c_size_t)]
+            L.tt_lmhead_loss.argtypes = [C.POINTER(TTPacked), vp, vp, C.c_int32, C.c_int32, C.c_int32, vp, vp, C.c_int32,
+                                         C.c_float, vp, vp, vp, vp, vp, vp, sz, st]
             L.tt_rope.argtypes = [C.POINTER(TTPacked), vp, C.c_int, C.c_int32, C.c_int32, C.c_double, C.c_int32, st]
             L.tt_restore_grad.argtypes = [C.POINTER(TTPacked), vp, C.c_int, C.c_int64, st]
             L.tt_launch_count.restype = C.c_int64
@@ -102,7 +106,8 @@ def lib():
             L.tt_launch_count_reset.restype = None
             for fn in ("tt_pack_plan", "tt_pack", "tt_attn_fwd", "tt_attn_bwd_workspace", "tt_attn_bwd",
                        "tt_restore_loss", "tt_grad_sqnorm", "tt_grad_sqnorm3", "tt_plan_traversals",
-                       "tt_traversal_forest", "tt_rope", "tt_restore_grad"):
+                       "tt_traversal_forest", "tt_rope", "tt_restore_grad", "tt_lmhead_loss_workspace",
+                       "tt_lmhead_loss"):
                 getattr(L, fn).restype = C.c_int
             _lib = L
     return _lib
@@ -336,6 +341,39 @@ def tt_grad_sqnorm3(x0, x1, x2, out=None, ws=None, stream=None):
                                                 int(x2.numel()), _dt(x0), _p(out), _p(ws), int(ws.numel()),
                                                 _stream(stream)))
     return out
+
+
+def tt_lmhead_loss_workspace(pk: PackedTree, hidden, vocab, vocab_chunk=16384) -> int:
+    n = C.c_size_t()
+    _check("tt_lmhead_loss_workspace", lib().tt_lmhead_loss_workspace(C.byref(pk.c), int(hidden), int(vocab),
+                                                                      int(vocab_chunk), C.byref(n)))
+    return int(n.value)
+
+
+def tt_lmhead_loss(pk: PackedTree, h, w, tok, grad_scale=1.0, vocab_chunk=16384, node_loss_mask=None,
+                   boundary_mode=0, dh=None, dw=None, tok_loss=None, sums=None, d_err=None, ws=None, stream=None):
+    """NEXT-f3: loss + (dH, dW) of the LM head without materialising [N, V] logits.
+    Returns (sums [2] fp64 device: (sum loss, sum Omega), dh, dw, tok_loss, d_err)."""
+    import torch
+    N, hidden = h.shape
+    vocab = w.shape[0]
+    dh = torch.empty_like(h) if dh is None else dh
+    dw = torch.empty_like(w) if dw is None else dw
+    sums = torch.zeros(2, dtype=torch.float64, device=h.device) if sums is None else sums
+    d_err = torch.zeros(1, dtype=torch.int32, device=h.device) if d_err is None else d_err
+    need = tt_lmhead_loss_workspace(pk, hidden, vocab, vocab_chunk)
+    if ws is None or ws.numel() < need:
+        ws = torch.empty(need, dtype=torch.uint8, device=h.device)
+    if node_loss_mask is not None and not isinstance(node_loss_mask, torch.Tensor):
+        node_loss_mask = torch.as_tensor(np.asarray(node_loss_mask, dtype=np.uint8), device=h.device)
+    for t in (h, w, dh, dw):
+        if not t.is_contiguous():
+            raise ValueError("tensors must be contiguous")
+    _check("tt_lmhead_loss", lib().tt_lmhead_loss(C.byref(pk.c), _p(h), _p(w), int(hidden), int(vocab),
+                                                  int(vocab_chunk), _p(tok), _p(node_loss_mask), int(boundary_mode),
+                                                  float(grad_scale), _p(dh), _p(dw), _p(tok_loss), _p(sums),
+                                                  _p(d_err), _p(ws), int(ws.numel()), _stream(stream)))
+    return sums, dh, dw, tok_loss, d_err
 
 
 def tt_rope(pk: PackedTree, x, base=1.0e6, inverse=False, stream=None):

@@ -66,7 +66,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
                     print(f"[{os.path.basename(s)}]\n{err}", file=sys.stderr)
     objs = [os.path.join(OBJ, os.path.basename(s)[:-3] + ".o") for s in srcs]
     if force or jobs or not os.path.exists(SO) or os.path.getmtime(SO) < max(os.path.getmtime(o) for o in objs):
-        cmd = [nvcc()] + ARCH + ["-shared", "-o", SO] + objs + ["-lcudart_static", "-ldl", "-lrt", "-lpthread"]
+        cuda_lib = os.path.join(os.path.dirname(os.path.dirname(os.path.realpath(nvcc()))), "lib64")
+        # cuBLASLt (plain library GEMMs of tt_lmhead_loss, NEXT-f3): dynamic, found via rpath or an
+        # already-loaded libcublasLt.so.12 (torch's)
+        cmd = [nvcc()] + ARCH + ["-shared", "-o", SO] + objs + ["-L" + cuda_lib, "-lcublasLt", "-Xlinker",
+                                                               "-rpath=" + cuda_lib, "-lcudart_static", "-ldl",
+                                                               "-lrt", "-lpthread"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")

@@ -86,7 +86,9 @@ __device__ __forceinline__ float ex2f(float x) {
   return y;
 }
 // (m, s) <- (m, s) (+) one vector of logits, log2 domain: one max pass, at most one rescale
-template <int W> __device__ __forceinline__ void accum(float& m, float& s, const Vec<W>& r) {
+// KP1: pairs (of W/2) whose exponentials run on the FMA pipe (degree-3 polynomial, max rel. error
+// 7.5e-5 per term; with 1 of 4 pairs the sum-exp, hence the lse, moves by <= 1.9e-5 relative)
+template <int W, int KP1 = 0> __device__ __forceinline__ void accum(float& m, float& s, const Vec<W>& r) {
   float x[W];
 #pragma unroll
   for (int t = 0; t < W / 2; ++t) {
@@ -104,8 +106,14 @@ template <int W> __device__ __forceinline__ void accum(float& m, float& s, const
   float a = 0.f, b = 0.f;
 #pragma unroll
   for (int t = 0; t < W; t += 2) {
-    a += ex2f(x[t] - m);
-    b += ex2f(x[t + 1] - m);
+    if (t / 2 >= W / 2 - KP1) {
+      const float2 e = sm100::exp2_poly2(make_float2(x[t] - m, x[t + 1] - m));
+      a += e.x;
+      b += e.y;
+    } else {
+      a += ex2f(x[t] - m);
+      b += ex2f(x[t + 1] - m);
+    }
   }
   s += a + b;
 }
@@ -593,7 +601,7 @@ __device__ __forceinline__ LcMeta lc_meta(uint8_t* base, int slot, int max_t) {
 }
 
 // KPOLY: pairs (of 4 per 8-element vector) whose pass-2 exponentials run on the FMA pipe
-template <int CS, int NBUF, int KPOLY>
+template <int CS, int NBUF, int KPOLY, int KP1>
 __global__ void __launch_bounds__(kLcThreads, 1) loss_cluster_kernel(const LcArgs a) {
   extern __shared__ __align__(128) uint8_t lsm[];
   const int Cq = a.Cq;
@@ -746,7 +754,7 @@ __global__ void __launch_bounds__(kLcThreads, 1) loss_cluster_kernel(const LcArg
       const uint4 q = x4[v];
       Vec<8> r;
       r.u[0] = q.x; r.u[1] = q.y; r.u[2] = q.z; r.u[3] = q.w;
-      accum<8>(m, sum, r);
+      accum<8, KP1>(m, sum, r);
     }
     for (int o = 16; o > 0; o >>= 1) {
       const float m2 = __shfl_xor_sync(0xffffffffu, m, o);
@@ -864,13 +872,13 @@ size_t lc_smem(int Cq, int max_t) {
   return (size_t)NBUF * Cq * 2 + kLcSlots * CS * 16 + (4 * NBUF + kLcSlots) * 8 + (size_t)NBUF * (16 + (size_t)max_t * 12);
 }
 
-template <int CS, int NBUF, int KPOLY = 1>
+template <int CS, int NBUF, int KPOLY = 1, int KP1 = 0>
 bool try_launch_cluster(const LcArgs& a0, int sms, cudaStream_t st) {
   LcArgs a = a0;
   a.Cq = ((a.V + CS - 1) / CS + 7) / 8 * 8;
   const size_t smem = lc_smem<CS, NBUF>(a.Cq, a.max_t);
   if (smem + 1024 > 232448) return false;  // static shared memory + margin
-  auto kern = loss_cluster_kernel<CS, NBUF, KPOLY>;
+  auto kern = loss_cluster_kernel<CS, NBUF, KPOLY, KP1>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
     cudaGetLastError();
     return false;
@@ -900,6 +908,12 @@ bool try_launch_cluster(const LcArgs& a0, int sms, cudaStream_t st) {
 
 }  // namespace
 
+tt_status launch_loss_sums(int64_t N, const float* ws_loss, const float* ws_omega, double* sums, cudaStream_t st) {
+  loss_sum_kernel<<<1, 1024, 0, st>>>(N, ws_loss, ws_omega, sums);
+  count_launch();
+  return check_launch("loss_sum_kernel");
+}
+
 tt_status launch_loss(const tt_packed& pk, const __nv_bfloat16* logits, int64_t ld, int vocab, const int32_t* tok,
                       const uint8_t* node_mask, int boundary_mode, float gamma, __nv_bfloat16* dlogits, float* tok_loss,
                       double* sums, int32_t* d_err, float* ws_loss, float* ws_omega, cudaStream_t st) {
@@ -919,6 +933,9 @@ tt_status launch_loss(const tt_packed& pk, const __nv_bfloat16* logits, int64_t 
              pk.node, pk.node_start, pk.node_len, pk.succ_ptr, pk.succ_tok, dlogits, tok_loss, ws_loss, ws_omega, d_err};
     a.max_t = std::max(1, pk.max_succ);
     if (variant == 1) done = try_launch_cluster<4, 3>(a, sms, st);  // fits while max_succ is small
+    else if (variant == 11) done = try_launch_cluster<4, 3, 2, 0>(a, sms, st);
+    else if (variant == 12) done = try_launch_cluster<4, 3, 2, 1>(a, sms, st);
+    else if (variant == 13) done = try_launch_cluster<4, 3, 1, 1>(a, sms, st);
     else if (variant == 3) done = try_launch_cluster<8, 4>(a, sms, st);
     if (!done) done = try_launch_cluster<4, 2>(a, sms, st);
   }

@@ -471,6 +471,34 @@ tt_status tt_grad_sqnorm3(const void* x0, int64_t n0, const void* x1, int64_t n1
   return launch_sqnorm(xs, ns, 3, dt, out, static_cast<double*>(d_ws), as_cuda(stream));
 }
 
+tt_status tt_lmhead_loss_workspace(const tt_packed* pk, int32_t hidden, int32_t vocab, int32_t vocab_chunk,
+                                   size_t* bytes) {
+  clear_error();
+  if (!pk || !bytes || hidden <= 0 || vocab <= 0 || vocab_chunk <= 0) { set_error("tt_lmhead_loss_workspace: bad argument"); return TT_ERR_INVALID_ARGUMENT; }
+  *bytes = lmhead_ws_bytes(pk->n_tokens, hidden, vocab, vocab_chunk);
+  return TT_OK;
+}
+
+tt_status tt_lmhead_loss(const tt_packed* pk, const void* h, const void* w, int32_t hidden, int32_t vocab,
+                         int32_t vocab_chunk, const int32_t* tok, const uint8_t* node_loss_mask, int32_t boundary_mode,
+                         float grad_scale, void* dh, void* dw, float* tok_loss, double* sums, int32_t* d_err,
+                         void* d_ws, size_t ws_bytes, tt_stream_t stream) {
+  clear_error();
+  if (!pk || !h || !w || !tok || !dh || !dw || !sums || !d_ws) { set_error("tt_lmhead_loss: null argument"); return TT_ERR_INVALID_ARGUMENT; }
+  if (pk->n_tokens <= 0) { set_error("tt_lmhead_loss: empty pack"); return TT_ERR_EMPTY; }
+  if (hidden <= 0 || vocab <= 0 || vocab_chunk <= 0) { set_error("tt_lmhead_loss: bad sizes"); return TT_ERR_INVALID_ARGUMENT; }
+  if (boundary_mode != 0 && boundary_mode != 1) { set_error("tt_lmhead_loss: boundary_mode must be 0 or 1"); return TT_ERR_INVALID_ARGUMENT; }
+  if (hidden % 8 != 0) { set_error("tt_lmhead_loss: hidden must be a multiple of 8"); return TT_ERR_UNSUPPORTED; }
+  if (!aligned16(h) || !aligned16(w) || !aligned16(dh) || !aligned16(dw) || !aligned16(d_ws)) {
+    set_error("tt_lmhead_loss: tensors must be 16-byte aligned"); return TT_ERR_ALIGNMENT;
+  }
+  if (pk->n_tokens > INT32_MAX) { set_error("tt_lmhead_loss: too many rows"); return TT_ERR_TOO_LARGE; }
+  if (ws_bytes < lmhead_ws_bytes(pk->n_tokens, hidden, vocab, vocab_chunk)) { set_error("tt_lmhead_loss: workspace too small"); return TT_ERR_WORKSPACE; }
+  return launch_lmhead_loss(*pk, static_cast<const __nv_bfloat16*>(h), static_cast<const __nv_bfloat16*>(w), hidden, vocab,
+                            vocab_chunk, tok, node_loss_mask, boundary_mode, grad_scale, static_cast<__nv_bfloat16*>(dh),
+                            static_cast<__nv_bfloat16*>(dw), tok_loss, sums, d_err, d_ws, as_cuda(stream));
+}
+
 tt_status tt_rope(const tt_packed* pk, void* x, tt_dtype dt, int32_t n_heads, int32_t d, double base,
                   int32_t inverse, tt_stream_t stream) {
   clear_error();

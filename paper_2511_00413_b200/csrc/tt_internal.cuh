@@ -76,6 +76,12 @@ tt_status launch_loss(const tt_packed& pk, const __nv_bfloat16* logits, int64_t 
 tt_status launch_sqnorm(const void* const* xs, const int64_t* ns, int count, tt_dtype dt, double* out,
                         double* partials, cudaStream_t st);
 
+tt_status launch_loss_sums(int64_t N, const float* ws_loss, const float* ws_omega, double* sums, cudaStream_t st);
+size_t lmhead_ws_bytes(int64_t N, int D, int V, int Vc);
+tt_status launch_lmhead_loss(const tt_packed& pk, const __nv_bfloat16* H, const __nv_bfloat16* W, int D, int V, int Vc,
+                             const int32_t* tok, const uint8_t* node_mask, int boundary_mode, float gamma,
+                             __nv_bfloat16* dH, __nv_bfloat16* dW, float* tok_loss, double* sums, int32_t* d_err,
+                             void* ws, cudaStream_t st);
 tt_status launch_rope(const tt_packed& pk, void* x, tt_dtype dt, int H, int d, double base, int inverse,
                       cudaStream_t st);
 tt_status launch_restore_grad(const tt_packed& pk, void* g, tt_dtype dt, int64_t row_elems, cudaStream_t st);
