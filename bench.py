@@ -331,6 +331,7 @@ def main():
     ap.add_argument("--no-linear", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-lmhead", action="store_true", help="skip the NEXT-f3 LM-head measurement")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
@@ -572,6 +573,25 @@ def main():
                           "hbm_peak_gbs": peaks["hbm"],
                           "algorithmic": "read + write of Q and K (rope), of G (restore_grad), bf16"}
         del qc, kc, gc
+        if not args.no_lmhead:
+            # NEXT-f3: LM head (Qwen3-8B hidden 4096, vocab 151,936) + restoration CE without the [N, V]
+            # logits: 4 GEMMs of 2 N V D FLOPs each (two logits sweeps, dH, dW) + chunked CE kernels
+            D_h, vc = 4096, 16384
+            g2 = torch.Generator(device="cuda").manual_seed(77)
+            Hh = torch.randn(j0.N, D_h, device="cuda", generator=g2).to(torch.bfloat16)
+            Wl = (2.0 / D_h ** 0.5 * torch.randn(VOCAB, D_h, device="cuda", generator=g2)).to(torch.bfloat16)
+            tokl = torch.randint(0, VOCAB, (j0.N,), device="cuda", dtype=torch.int32, generator=g2)
+            wsl = torch.empty(tt.tt_lmhead_loss_workspace(pk0, D_h, VOCAB, vc), dtype=torch.uint8, device="cuda")
+            dHl, dWl = torch.empty_like(Hh), torch.empty_like(Wl)
+            lm_ms = _t(lambda: tt.tt_lmhead_loss(pk0, Hh, Wl, tokl, vocab_chunk=vc, dh=dHl, dw=dWl, ws=wsl), reps=3)
+            fl = 8.0 * j0.N * VOCAB * D_h
+            out["next_f3_lmhead"] = {"ms": round(lm_ms, 3), "hidden": D_h, "vocab": VOCAB, "vocab_chunk": vc,
+                                     "achieved_tflops": round(fl / lm_ms / 1e9, 1), "peak_tflops": peaks["bf16"],
+                                     "frac": round(fl / lm_ms / 1e9 / peaks["bf16"], 4),
+                                     "algorithmic": "8 N V D FLOPs (logits twice, dH, dW)",
+                                     "workspace_bytes": int(wsl.numel()),
+                                     "materialised_logits_bytes_avoided": int(2 * 2 * j0.N * VOCAB)}
+            del Hh, Wl, dHl, dWl, wsl
     if rank == 0 and world == 1 and not args.no_cpu:
         dt, share, ntraj, cores = oracle_sample(jobs[0].tree, cfg, budget_s=args.cpu_budget)
         full_s = dt / share

@@ -151,6 +151,13 @@ def _p(t):
     return None if t is None else C.c_void_p(t.data_ptr())
 
 
+def _need(t, dtype, name):
+    """Checks a caller-supplied output's dtype (the C ABI takes typed pointers: a mismatched torch
+    dtype would be silently reinterpreted)."""
+    if t is not None and t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+
+
 def tt_launch_count() -> int:
     return int(lib().tt_launch_count())
 
@@ -264,6 +271,8 @@ def tt_attn_fwd(pk: PackedTree, q, k, v, softmax_scale=None, out=None, lse=None,
     for t in (q, k, v, out, lse):
         if not t.is_contiguous():
             raise ValueError("tensors must be contiguous")
+    _need(lse, torch.float32, "lse")
+    _need(out, q.dtype, "out")
     _check("tt_attn_fwd", lib().tt_attn_fwd(C.byref(pk.c), _p(q), _p(k), _p(v), _dt(q), hq, hkv, d,
                                             _scale(softmax_scale, d), _p(out), _p(lse), _stream(stream)))
     return out, lse
@@ -310,6 +319,10 @@ def tt_restore_loss(pk: PackedTree, logits, tok, grad_scale=1.0, node_loss_mask=
         ws = torch.empty(need, dtype=torch.uint8, device=logits.device)
     if node_loss_mask is not None and not isinstance(node_loss_mask, torch.Tensor):
         node_loss_mask = torch.as_tensor(np.asarray(node_loss_mask, dtype=np.uint8), device=logits.device)
+    _need(tok_loss, torch.float32, "tok_loss")
+    _need(sums, torch.float64, "sums")
+    _need(d_err, torch.int32, "d_err")
+    _need(tok, torch.int32, "tok")
     _check("tt_restore_loss", L.tt_restore_loss(C.byref(pk.c), _p(logits), int(ld), vocab, _p(tok),
                                                 _p(node_loss_mask), int(boundary_mode), float(grad_scale),
                                                 _p(dlogits), _p(tok_loss), _p(sums), _p(d_err), _p(ws),
@@ -369,6 +382,12 @@ def tt_lmhead_loss(pk: PackedTree, h, w, tok, grad_scale=1.0, vocab_chunk=16384,
     for t in (h, w, dh, dw):
         if not t.is_contiguous():
             raise ValueError("tensors must be contiguous")
+    for t, n in ((h, "h"), (w, "w"), (dh, "dh"), (dw, "dw")):
+        _need(t, torch.bfloat16, n)
+    _need(tok_loss, torch.float32, "tok_loss")
+    _need(sums, torch.float64, "sums")
+    _need(d_err, torch.int32, "d_err")
+    _need(tok, torch.int32, "tok")
     _check("tt_lmhead_loss", lib().tt_lmhead_loss(C.byref(pk.c), _p(h), _p(w), int(hidden), int(vocab),
                                                   int(vocab_chunk), _p(tok), _p(node_loss_mask), int(boundary_mode),
                                                   float(grad_scale), _p(dh), _p(dw), _p(tok_loss), _p(sums),

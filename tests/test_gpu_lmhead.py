@@ -46,7 +46,7 @@ def test_lmhead_loss_matches_oracle(tt, name, t, D, V, vc, opt):
     if opt.get("weights"):
         alpha = np.random.default_rng(3).normal(0.4, 1.0, pk.info["n_traj"]).astype(np.float32)
         tt.tt_pack_weights(pk, alpha)
-    tl = torch.empty(N, device="cuda")
+    tl = torch.empty(N, device="cuda", dtype=torch.float32)
     sums, dh, dw, tl, err = tt.tt_lmhead_loss(pk, H.cuda(), W.cuda(), tok.cuda(), grad_scale=gamma, vocab_chunk=vc,
                                               node_loss_mask=mask, boundary_mode=opt.get("boundary_mode", 0),
                                               tok_loss=tl)
@@ -58,7 +58,8 @@ def test_lmhead_loss_matches_oracle(tt, name, t, D, V, vc, opt):
     assert int(err.item()) == 0
     lr = r["loss_rows"]
     got = to64(tl)
-    assert np.all(np.abs(got - lr) <= 1e-4 * np.maximum(1.0, np.abs(lr))), float(np.abs(got - lr).max())
+    badr = np.flatnonzero(~(np.abs(got - lr) <= 1e-4 * np.maximum(1.0, np.abs(lr))))
+    assert len(badr) == 0, (len(badr), badr[:10].tolist(), got[badr[:5]].tolist(), lr[badr[:5]].tolist())
     s = sums.cpu().numpy()
     assert abs(s[0] - lr.sum()) <= 1e-5 * max(1.0, abs(lr.sum()))
     assert abs(s[1] - r["omega_rows"].sum()) <= 1e-5 * max(1.0, abs(r["omega_rows"].sum()))
@@ -75,7 +76,7 @@ def test_lmhead_bad_token_sets_error(tt):
     W = torch.randn(V, D).to(torch.bfloat16).cuda()
     tok = torch.randint(0, V, (N,), dtype=torch.int32)
     tok[5] = V + 3   # an out-of-range target: its predicting row reports NaN and the error word is set
-    tl = torch.empty(N, device="cuda")
+    tl = torch.empty(N, device="cuda", dtype=torch.float32)
     sums, dh, dw, tl, err = tt.tt_lmhead_loss(pk, H, W, tok.cuda(), vocab_chunk=256, tok_loss=tl)
     torch.cuda.synchronize()
     assert int(err.item()) == 1

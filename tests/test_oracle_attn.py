@@ -21,7 +21,16 @@ import torch
 import oracle
 from workloads import trees
 
-torch.set_default_dtype(torch.float64)
+
+
+@pytest.fixture(autouse=True, scope="module")
+def _fp64_default():
+    # fp64 default dtype for this module's tensors only (restored afterwards, so it cannot leak into
+    # other modules' tensors, e.g. fp32 GPU outputs)
+    prev = torch.get_default_dtype()
+    torch.set_default_dtype(torch.float64)
+    yield
+    torch.set_default_dtype(prev)
 
 
 def _rand(N, hq, hkv, d, seed):
