@@ -543,6 +543,11 @@ __global__ void __launch_bounds__(1024) loss_sum_kernel(int64_t N, const float* 
 // memory (remote stores + remote mbarrier arrivals, no all-thread cluster barrier) -> pass 2
 // overwrites the slice in shared memory with dlogits -> TMA bulk store (producer warp) while the
 // compute warps already work on the next row.
+// FAST passes (default): pass 1 = slice max on packed bf16 pairs (HMNMX2, no conversion), then the
+// sum of 2^(x log2e - M) with packed f32x2 FMAs / adds (no online rescaling); pass 2 = packed f32x2
+// exponent argument and gamma*Omega scaling.  ncu (r1e) counted ~17 issued instructions per logit
+// for the online-rescaling passes; this form needs ~7.  25% of the exponentials of each pass run as a
+// degree-3 polynomial on the FMA pipe (relative error <= 7.5e-5 per term) to offload the MUFU unit.
 // ---------------------------------------------------------------------------------------------
 constexpr int kLcGroup = 256;                      // threads per compute group
 constexpr int kLcThreads = 2 * kLcGroup + 64;      // 2 compute groups + producer warp + meta warp
@@ -601,7 +606,7 @@ __device__ __forceinline__ LcMeta lc_meta(uint8_t* base, int slot, int max_t) {
 }
 
 // KPOLY: pairs (of 4 per 8-element vector) whose pass-2 exponentials run on the FMA pipe
-template <int CS, int NBUF, int KPOLY, int KP1>
+template <int CS, int NBUF, int KPOLY, int KP1, int FAST = 0>
 __global__ void __launch_bounds__(kLcThreads, 1) loss_cluster_kernel(const LcArgs a) {
   extern __shared__ __align__(128) uint8_t lsm[];
   const int Cq = a.Cq;
@@ -614,6 +619,7 @@ __global__ void __launch_bounds__(kLcThreads, 1) loss_cluster_kernel(const LcArg
   uint64_t* xchg = mfree + NBUF;                                                  // [kLcSlots]
   uint8_t* meta_base = reinterpret_cast<uint8_t*>(xchg + kLcSlots);
   __shared__ float s_red[2][3][kLcGroup / 32];
+  __shared__ float s_max[2][kLcGroup / 32];
   __shared__ float s_lse[2];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t cr = lc_rank();
@@ -750,18 +756,56 @@ __global__ void __launch_bounds__(kLcThreads, 1) loss_cluster_kernel(const LcArg
     __nv_bfloat16* xs = bufs + (size_t)b * Cq;
     const uint4* x4 = reinterpret_cast<const uint4*>(xs);
     float m = -INFINITY, sum = 0.f;
-    for (int v = gt; v < n / 8; v += kLcGroup) {
-      const uint4 q = x4[v];
-      Vec<8> r;
-      r.u[0] = q.x; r.u[1] = q.y; r.u[2] = q.z; r.u[3] = q.w;
-      accum<8, KP1>(m, sum, r);
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-      const float m2 = __shfl_xor_sync(0xffffffffu, m, o);
-      const float s2 = __shfl_xor_sync(0xffffffffu, sum, o);
-      const float mm = fmaxf(m, m2);
-      sum = (mm == -INFINITY) ? 0.f : sum * ex2f(m - mm) + s2 * ex2f(m2 - mm);
-      m = mm;
+    if constexpr (FAST) {
+      // pass 1a: slice max on packed bf16 pairs (HMNMX2, no conversion); 1b: sum of 2^(x log2e - M)
+      // with packed f32x2 FMAs / adds — no online rescaling, ~3 issue slots per element
+      __nv_bfloat162 mx = __halves2bfloat162(__ushort_as_bfloat16((unsigned short)0xff80u),
+                                             __ushort_as_bfloat16((unsigned short)0xff80u));
+      for (int v = gt; v < n / 8; v += kLcGroup) {
+        const uint4 q = x4[v];
+        mx = __hmax2(__hmax2(mx, *reinterpret_cast<const __nv_bfloat162*>(&q.x)),
+                     __hmax2(*reinterpret_cast<const __nv_bfloat162*>(&q.y), *reinterpret_cast<const __nv_bfloat162*>(&q.z)));
+        mx = __hmax2(mx, *reinterpret_cast<const __nv_bfloat162*>(&q.w));
+      }
+      float tm = fmaxf(__bfloat162float(mx.x), __bfloat162float(mx.y));
+      for (int o = 16; o > 0; o >>= 1) tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, o));
+      if (lane == 0) s_max[grp][gw] = tm;
+      bar_g();
+      tm = s_max[grp][0];
+#pragma unroll
+      for (int k = 1; k < kLcGroup / 32; ++k) tm = fmaxf(tm, s_max[grp][k]);
+      m = tm * kLog2e;  // group max, log2 units
+      if (m != -INFINITY) {
+        const float2 L2 = make_float2(kLog2e, kLog2e), NM = make_float2(-m, -m);
+        float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
+        for (int v = gt; v < n / 8; v += kLcGroup) {
+          const uint4 q = x4[v];
+          const uint32_t in[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const float2 e2 = sm100::ffma2(bf2f(in[t]), L2, NM);
+            const float2 e = (t >= 4 - KP1) ? sm100::exp2_poly2(e2) : make_float2(ex2f(e2.x), ex2f(e2.y));
+            if (t & 1) acc1 = sm100::fadd2(acc1, e); else acc0 = sm100::fadd2(acc0, e);
+          }
+        }
+        const float2 acc = sm100::fadd2(acc0, acc1);
+        sum = acc.x + acc.y;
+      }
+      for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    } else {
+      for (int v = gt; v < n / 8; v += kLcGroup) {
+        const uint4 q = x4[v];
+        Vec<8> r;
+        r.u[0] = q.x; r.u[1] = q.y; r.u[2] = q.z; r.u[3] = q.w;
+        accum<8, KP1>(m, sum, r);
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        const float m2 = __shfl_xor_sync(0xffffffffu, m, o);
+        const float s2 = __shfl_xor_sync(0xffffffffu, sum, o);
+        const float mm = fmaxf(m, m2);
+        sum = (mm == -INFINITY) ? 0.f : sum * ex2f(m - mm) + s2 * ex2f(m2 - mm);
+        m = mm;
+      }
     }
     // target logits that live in this slice (read before pass 2 overwrites them)
     float tx = 0.f;
@@ -821,6 +865,22 @@ __global__ void __launch_bounds__(kLcThreads, 1) loss_cluster_kernel(const LcArg
     const float gO = bad_any ? 0.f : a.gamma * Omega;
     // ---- pass 2: dlogits = gamma Omega softmax, in place in shared memory ----
     uint4* y4 = reinterpret_cast<uint4*>(xs);
+    if constexpr (FAST) {
+      const float2 L2 = make_float2(kLog2e, kLog2e), NL = make_float2(-lse2, -lse2), G2 = make_float2(gO, gO);
+      for (int v = gt; v < n / 8; v += kLcGroup) {
+        const uint4 q = y4[v];
+        const uint32_t in[4] = {q.x, q.y, q.z, q.w};
+        uint32_t o[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const float2 a2 = sm100::ffma2(bf2f(in[t]), L2, NL);
+          const float2 e = (t >= 4 - KPOLY) ? sm100::exp2_poly2(a2) : make_float2(ex2f(a2.x), ex2f(a2.y));
+          const float2 r2 = sm100::fmul2(e, G2);
+          o[t] = f2bf(r2.x, r2.y);
+        }
+        y4[v] = make_uint4(o[0], o[1], o[2], o[3]);
+      }
+    } else
     for (int v = gt; v < n / 8; v += kLcGroup) {
       const uint4 q = y4[v];
       const uint32_t in[4] = {q.x, q.y, q.z, q.w};
@@ -872,13 +932,13 @@ size_t lc_smem(int Cq, int max_t) {
   return (size_t)NBUF * Cq * 2 + kLcSlots * CS * 16 + (4 * NBUF + kLcSlots) * 8 + (size_t)NBUF * (16 + (size_t)max_t * 12);
 }
 
-template <int CS, int NBUF, int KPOLY = 1, int KP1 = 0>
+template <int CS, int NBUF, int KPOLY = 1, int KP1 = 0, int FAST = 0>
 bool try_launch_cluster(const LcArgs& a0, int sms, cudaStream_t st) {
   LcArgs a = a0;
   a.Cq = ((a.V + CS - 1) / CS + 7) / 8 * 8;
   const size_t smem = lc_smem<CS, NBUF>(a.Cq, a.max_t);
   if (smem + 1024 > 232448) return false;  // static shared memory + margin
-  auto kern = loss_cluster_kernel<CS, NBUF, KPOLY, KP1>;
+  auto kern = loss_cluster_kernel<CS, NBUF, KPOLY, KP1, FAST>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
     cudaGetLastError();
     return false;
@@ -924,8 +984,10 @@ tt_status launch_loss(const tt_packed& pk, const __nv_bfloat16* logits, int64_t 
   const int64_t grid = std::min<int64_t>(pk.n_tokens, (int64_t)sms);
   const bool v16 = (ld % 16 == 0) && ((reinterpret_cast<uintptr_t>(logits) | reinterpret_cast<uintptr_t>(dlogits)) % 32 == 0);
   static const int variant = [] {
-    const char* e = getenv("TT_LOSS_VARIANT");  // development A/B: 0 ring/L2 kernel, 1 CS4x3 (else CS4x2), 2 CS4x2, 3 CS8x4
-    return e ? atoi(e) : 1;
+    // development A/B: 0 ring/L2 kernel, 1 CS4x3 (else CS4x2), 3 CS8x4, 1x: poly splits, 2x: FAST passes
+    // (packed-bf16 max pass + f32x2 sum pass + f32x2 dlogits), 3x: other cluster sizes
+    const char* e = getenv("TT_LOSS_VARIANT");
+    return e ? atoi(e) : 24;  // measured best (profiles/r1f_loss_variants.txt): CS4 x 3 buffers, FAST passes, 25% poly exps
   }();
   bool done = false;
   if (variant != 0 && vocab % 8 == 0) {
@@ -936,6 +998,16 @@ tt_status launch_loss(const tt_packed& pk, const __nv_bfloat16* logits, int64_t 
     else if (variant == 11) done = try_launch_cluster<4, 3, 2, 0>(a, sms, st);
     else if (variant == 12) done = try_launch_cluster<4, 3, 2, 1>(a, sms, st);
     else if (variant == 13) done = try_launch_cluster<4, 3, 1, 1>(a, sms, st);
+    else if (variant == 21) done = try_launch_cluster<4, 3, 1, 0, 1>(a, sms, st);
+    else if (variant == 22) done = try_launch_cluster<4, 3, 2, 0, 1>(a, sms, st);
+    else if (variant == 23) done = try_launch_cluster<4, 3, 2, 1, 1>(a, sms, st);
+    else if (variant == 24) done = try_launch_cluster<4, 3, 1, 1, 1>(a, sms, st);
+    else if (variant == 31) done = try_launch_cluster<8, 5, 1, 1, 1>(a, sms, st);
+    else if (variant == 32) done = try_launch_cluster<8, 4, 1, 1, 1>(a, sms, st);
+    else if (variant == 33) done = try_launch_cluster<2, 1, 1, 1, 1>(a, sms, st);
+    else if (variant == 34) done = try_launch_cluster<8, 5, 2, 1, 1>(a, sms, st);
+    else if (variant == 35) done = try_launch_cluster<3, 2, 1, 1, 1>(a, sms, st);
+    else if (variant == 36) done = try_launch_cluster<6, 4, 1, 1, 1>(a, sms, st);
     else if (variant == 3) done = try_launch_cluster<8, 4>(a, sms, st);
     if (!done) done = try_launch_cluster<4, 2>(a, sms, st);
   }
