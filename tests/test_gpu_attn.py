@@ -193,3 +193,68 @@ def test_bwd_dk_dv_bitwise_deterministic(tt):
         assert torch.equal(d[1], ref[1]) and torch.equal(d[2], ref[2])
         # dQ accumulates with fp32 reductions: order-dependent rounding only
         assert (d[0].float() - ref[0].float()).abs().max().item() <= 2e-2
+
+
+EDGE_CASES = [
+    # degenerate shapes on the tcgen05 path: one token, one partial block, exactly one block,
+    # a forest of single-block roots with zero-length nodes, 1-token nodes straddling block edges
+    ("one_token", trees.Tree([-1], [1]), 2, 1),
+    ("one_partial_block", trees.Tree([-1, 0, 0], [40, 20, 17]), 2, 2),
+    ("exactly_128", trees.Tree([-1, 0, 0], [64, 32, 32]), 2, 1),
+    ("forest_zero_len", trees.Tree([-1, -1, 1, 1, -1, 4, 2], [127, 0, 129, 1, 255, 0, 2]), 4, 2),
+    ("block_edge_nodes", trees.Tree([-1, 0, 1, 1, 0, 4], [127, 1, 128, 1, 1, 127]), 2, 2),
+]
+
+
+@pytest.mark.parametrize("name,t,hq,hkv", EDGE_CASES, ids=[c[0] for c in EDGE_CASES])
+def test_bf16_edge_shapes(tt, name, t, hq, hkv):
+    pk, (q, k, v, G, scale), (o, lse, dq, dk, dv) = _run(tt, t, hq, hkv, 128, "bf16", seed=13)
+    opk, oo, olse, odq, odk, odv = _oracle(t, q, k, v, G, scale)
+    m = _on_path(opk)
+    assert max_abs(o[m], oo[m]) <= TOL_O_BF16
+    assert max_abs(lse[:, m], olse[:, m]) <= TOL_O_BF16
+    for a, b in ((dq, odq), (dk, odk), (dv, odv)):
+        # a one-token tree has dQ = dK = 0 exactly (dS = P (dO.v - dO.O) with P = 1, O = v): there
+        # the check is absolute (bf16 rounding of O leaves ~1e-8)
+        assert rel_l2(a[m], b[m]) <= TOL_G_BF16 or (np.abs(to64(b[m])).max() == 0 and max_abs(a[m], b[m]) <= 1e-5)
+
+
+def test_large_tree_sampled_rows(tt):
+    """A ~100K-token tree (2K prefix, 400 leaves) — 790 query blocks, near the forward tile-list
+    budget of one launch — checked on sampled rows / leaf keys."""
+    import torch
+    rng = np.random.default_rng(9)
+    n_leaves = 400
+    t = trees.Tree(np.array([-1] + [0] * n_leaves, np.int32),
+                   np.array([2048] + list(rng.integers(150, 350, n_leaves)), np.int32))
+    pk, (q, k, v, G, scale), (o, lse, dq, dk, dv) = _run(tt, t, 2, 1, 128, "bf16", seed=17)
+    opk = oracle.pack(t.parent, t.length)
+    N = opk["n_tokens"]
+    assert N > 90000
+    want = np.zeros(N, np.uint8)
+    want[rng.choice(N, 40, replace=False)] = 1
+    want[[0, N - 1]] = 1
+    span = opk["E"] - np.arange(N)
+    wk = np.zeros(N, np.uint8)
+    wk[rng.choice(np.flatnonzero(span <= 300), 16, replace=False)] = 1
+    oo, olse = oracle.attn_fwd(opk, q, k, v, scale, want=want, check_invariant=False)
+    mq = want.astype(bool)
+    assert max_abs(o[mq], oo[mq]) <= TOL_O_BF16
+    assert max_abs(lse[:, mq], olse[:, mq]) <= TOL_O_BF16
+    odq, odk, odv = oracle.attn_bwd(opk, q, k, v, G, scale, want_q=want, want_k=wk)
+    mk = wk.astype(bool)
+    assert rel_l2(dq[mq], odq[mq]) <= TOL_G_BF16
+    assert rel_l2(dk[mk], odk[mk]) <= TOL_G_BF16
+    assert rel_l2(dv[mk], odv[mk]) <= TOL_G_BF16
+
+
+def test_too_many_blocks_fails_loudly(tt):
+    """Beyond the forward kernel's tile-list budget the call returns TT_ERR_TOO_LARGE (no silent
+    truncation, no fallback)."""
+    import torch
+    N = 512 * 1024
+    pk = tt.tt_pack([-1], [N])
+    q = torch.zeros(N, 1, 128, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(tt.TTError) as ei:
+        tt.tt_attn_fwd(pk, q, q, q)
+    assert ei.value.code == 4
