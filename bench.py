@@ -2,9 +2,10 @@
 """bench.py — Tree Training hot path on B200: one JSON line per run (driver contract).
 
 A "step" is one pass of the whole hot path of SURVEY.md §8(a) over one tree per rank:
-  a1 tt_pack (host DFS + device fill/tile lists)   a2 tt_attn_fwd   a3 tt_restore_loss
-  a4+a5 tt_attn_bwd (preprocess + main + dQ convert)   a6 tt_grad_sqnorm x3 + NCCL all_gather
-  of the per-tree fp64 scalars (N > 1).
+  a1 tt_pack (host DFS + device fill/tile lists)   a2 tt_attn_fwd   a3 tt_restore_loss (+ loss sums)
+  a4+a5 tt_attn_bwd (preprocess + main + dQ convert)   a6 ||dQ||^2, ||dK||^2, ||dV||^2 fused into
+  tt_attn_bwd (per-CTA partials, fixed-order fp64 sum) + NCCL all_gather of the per-tree fp64
+  scalars (N > 1).
 Default workload (N = 1): BASELINE.json configs[1] "agentic tree 8K packed tokens, branching
 factor 2-4, depth 6, 32 heads, head_dim 128, bf16" (workloads.gen_agentic seed = rank), with the
 Gradient-Restoration loss at the Qwen3 vocabulary (151,936).  Each rank processes its own tree
@@ -221,12 +222,9 @@ def run_step(job, ev=None, h2d=False):
     if job.ws is None or job.ws.numel() < need:
         job.ws = torch.empty(need, dtype=torch.uint8, device="cuda")
     mark("bwd", 0)
-    tt.tt_attn_bwd(pk, job.q, job.k, job.v, job.o, job.lse, job.g, restore=True,          # a4 + a5
-                   dq=job.dq, dk=job.dk, dv=job.dv, ws=job.ws)
+    tt.tt_attn_bwd(pk, job.q, job.k, job.v, job.o, job.lse, job.g, restore=True,          # a4 + a5 (+ a6:
+                   dq=job.dq, dk=job.dk, dv=job.dv, ws=job.ws, sqnorm=job.rec[2:5])       # fused norms)
     mark("bwd", 1)
-    mark("scal", 0)
-    tt.tt_grad_sqnorm3(job.dq, job.dk, job.dv, out=job.rec[2:5])                          # a6
-    mark("scal", 1)
     if h2d:
         job.rec_host.copy_(job.rec, non_blocking=True)
     return pk
@@ -384,7 +382,7 @@ def main():
     torch.cuda.synchronize()
 
     # ---- timed device region ----
-    names = ["pack", "fwd", "loss", "bwd", "scal"]
+    names = ["pack", "fwd", "loss", "bwd"]
     # per (step, tree) event pairs around each op: per-op times are summed over the rank's trees
     evs = [[{n: (torch.cuda.Event(True), torch.cuda.Event(True)) for n in names} for _ in jobs] for _ in range(args.steps)]
     step_ev = [(torch.cuda.Event(True), torch.cuda.Event(True)) for _ in range(args.steps)]

@@ -194,11 +194,15 @@ tt_status tt_attn_bwd_workspace(const tt_packed* pk, int32_t hq, int32_t hkv, in
  * every branch through the token) and the outputs equal the sum over branches of ordinary
  * causal-attention gradients.  With restore = 0, `dout` must already be restored (w (.) G).
  * o / lse are the outputs of tt_attn_fwd.  dq [N,hq,d], dk/dv [N,hkv,d] in dtype dt.
+ * sqnorm (nullable, DEVICE double[3]): the per-tree gradient-norm scalars of SURVEY §8(a) row a6,
+ *   ||dQ||^2, ||dK||^2, ||dV||^2 of the STORED outputs, fused into the backward (per-CTA / per-block
+ *   partials written by the kernels that produce dK/dV and dQ, summed in a fixed order in fp64:
+ *   bitwise reproducible, no extra pass over the gradients).
  * -------------------------------------------------------------------------------------- */
 tt_status tt_attn_bwd(const tt_packed* pk, const void* q, const void* k, const void* v, const void* o,
                       const float* lse, const void* dout, int32_t restore, tt_dtype dt, int32_t hq,
-                      int32_t hkv, int32_t d, float softmax_scale, void* dq, void* dk, void* dv, void* d_ws,
-                      size_t ws_bytes, tt_stream_t stream);
+                      int32_t hkv, int32_t d, float softmax_scale, void* dq, void* dk, void* dv, double* sqnorm,
+                      void* d_ws, size_t ws_bytes, tt_stream_t stream);
 
 /* --------------------------------------------------------------------------------------
  * Gradient-Restoration loss (R6, R7, R8, R17).  For every packed row t

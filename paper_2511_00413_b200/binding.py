@@ -81,7 +81,7 @@ def lib():
             L.tt_attn_bwd_workspace.argtypes = [C.POINTER(TTPacked), C.c_int32, C.c_int32, C.c_int32, C.c_int,
                                                 C.POINTER(C.c_size_t)]
             L.tt_attn_bwd.argtypes = [C.POINTER(TTPacked), vp, vp, vp, vp, vp, vp, C.c_int32, C.c_int, C.c_int32,
-                                      C.c_int32, C.c_int32, C.c_float, vp, vp, vp, vp, sz, st]
+                                      C.c_int32, C.c_int32, C.c_float, vp, vp, vp, vp, vp, sz, st]
             L.tt_restore_loss_workspace.restype = C.c_size_t
             L.tt_restore_loss_workspace.argtypes = [C.POINTER(TTPacked)]
             L.tt_restore_loss.argtypes = [C.POINTER(TTPacked), vp, C.c_int64, C.c_int32, vp, vp, C.c_int32, C.c_float,
@@ -287,7 +287,8 @@ def tt_attn_bwd_workspace(pk: PackedTree, hq, hkv, d, dtype) -> int:
 
 
 def tt_attn_bwd(pk: PackedTree, q, k, v, o, lse, dout, restore=True, softmax_scale=None, dq=None, dk=None, dv=None,
-                ws=None, stream=None):
+                ws=None, sqnorm=None, stream=None):
+    """sqnorm: optional fp64 device tensor [3] receiving ||dQ||^2, ||dK||^2, ||dV||^2 (fused, row a6)."""
     import torch
     N, hq, d = q.shape
     hkv = k.shape[1]
@@ -297,9 +298,11 @@ def tt_attn_bwd(pk: PackedTree, q, k, v, o, lse, dout, restore=True, softmax_sca
     need = tt_attn_bwd_workspace(pk, hq, hkv, d, q.dtype)
     if ws is None or ws.numel() < need:
         ws = torch.empty(need, dtype=torch.uint8, device=q.device)
+    _need(sqnorm, torch.float64, "sqnorm")
     _check("tt_attn_bwd", lib().tt_attn_bwd(C.byref(pk.c), _p(q), _p(k), _p(v), _p(o), _p(lse), _p(dout),
                                             int(bool(restore)), _dt(q), hq, hkv, d, _scale(softmax_scale, d),
-                                            _p(dq), _p(dk), _p(dv), _p(ws), int(ws.numel()), _stream(stream)))
+                                            _p(dq), _p(dk), _p(dv), _p(sqnorm), _p(ws), int(ws.numel()),
+                                            _stream(stream)))
     return dq, dk, dv
 
 

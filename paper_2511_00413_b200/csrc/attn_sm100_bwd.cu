@@ -82,7 +82,9 @@ constexpr uint32_t kNumBars = 1 + 2 * kQStages + 12 + 1;
 constexpr uint32_t kOffMisc = kOffBar + kNumBars * 8;
 // The dynamic shared-memory window is 1024-byte aligned on sm_100 (checked at run time; the kernel
 // traps otherwise), so no alignment slack is reserved.
-constexpr uint32_t kSmemBytes = kOffMisc + 16;
+constexpr uint32_t kOffRed = kOffMisc + 16;                       // a6 reduction scratch: double [2][4]
+// (no static __shared__ in this kernel: it would shift the 1024-byte aligned dynamic window)
+constexpr uint32_t kSmemBytes = kOffRed + 64;
 static_assert(kSmemBytes <= 232448, "backward kernel exceeds 227 KB of shared memory");
 
 constexpr uint32_t kColDV = 0, kColDK = 128, kColS = 256, kColP = 384, kColQ = 448;
@@ -107,6 +109,7 @@ struct BwdParams {
   float* dq_acc;
   __nv_bfloat16* dk;
   __nv_bfloat16* dv;
+  double* part_kv;  // nullable: [grid][2] fp64 partial sums of squares of this CTA's dV (0) / dK (1) rows
 };
 
 __global__ void __maxnreg__(128)
@@ -495,6 +498,7 @@ __global__ void __maxnreg__(128)
       const uint32_t col = wg == 0 ? kColDV : kColDK;
       const float mul = wg == 0 ? 1.f : p.scale;
       __nv_bfloat16* dst = (wg == 0 ? p.dv : p.dk) + ((int64_t)j * p.hkv + hk) * kD;
+      double sq = 0.0;  // a6: sum of squares of the stored (bf16-rounded) values, fp32 per 8 / fp64 across
 #pragma unroll 1
       for (int cc = 0; cc < 4; ++cc) {
         uint32_t ov[32];
@@ -508,7 +512,27 @@ __global__ void __maxnreg__(128)
           uint4* d4 = reinterpret_cast<uint4*>(dst + 32 * cc);
 #pragma unroll
           for (int u = 0; u < 4; ++u) d4[u] = make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+          if (p.part_kv) {
+#pragma unroll
+            for (int u8 = 0; u8 < 4; ++u8) {
+              float s8 = 0.f;
+#pragma unroll
+              for (int u = 4 * u8; u < 4 * u8 + 4; ++u) {
+                const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&pk[u]));
+                s8 = fmaf(f.x, f.x, fmaf(f.y, f.y, s8));
+              }
+              sq += (double)s8;
+            }
+          }
         }
+      }
+      if (p.part_kv) {
+        // fixed-order reduction over the warpgroup's 128 rows -> one fp64 partial per (CTA, tensor)
+        double (*red)[4] = reinterpret_cast<double (*)[4]>(smem + kOffRed);
+        for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+        if (lane == 0) red[wg][q4] = sq;
+        named_bar_sync(2 + wg, 128);
+        if (r == 0) p.part_kv[2 * (int64_t)blockIdx.x + wg] = ((red[wg][0] + red[wg][1]) + red[wg][2]) + red[wg][3];
       }
     }
   }
@@ -524,13 +548,51 @@ __global__ void __maxnreg__(128)
   }
 }
 
-// dQ fp32 accumulator -> bf16 output
+// dQ fp32 accumulator -> bf16 output; optionally the per-block fp64 sum of squares of the rounded
+// values (fixed grid and grid-stride assignment: bitwise reproducible)
 __global__ void __launch_bounds__(256) dq_convert_kernel(const float4* __restrict__ acc, uint2* __restrict__ out,
-                                                         int64_t n4) {
+                                                         int64_t n4, double* __restrict__ part_q) {
+  double sq = 0.0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
     const float4 a = acc[i];
-    out[i] = make_uint2(pack_bf16(a.x, a.y), pack_bf16(a.z, a.w));
+    const uint2 o = make_uint2(pack_bf16(a.x, a.y), pack_bf16(a.z, a.w));
+    out[i] = o;
+    if (part_q) {
+      const float2 lo = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&o.x));
+      const float2 hi = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&o.y));
+      sq += (double)fmaf(lo.x, lo.x, fmaf(lo.y, lo.y, fmaf(hi.x, hi.x, hi.y * hi.y)));
+    }
   }
+  if (!part_q) return;
+  __shared__ double red[8];
+  for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sq;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += red[w];
+    part_q[blockIdx.x] = t;
+  }
+}
+
+// a6: ||dQ||^2, ||dK||^2, ||dV||^2 from the per-block / per-CTA partials, fixed order, one CTA
+__global__ void __launch_bounds__(256) sqnorm_final_kernel(const double* __restrict__ part_q, int nq,
+                                                           const double* __restrict__ part_kv, int nkv,
+                                                           double* __restrict__ out) {
+  __shared__ double red[3][256];
+  double a = 0.0, b = 0.0, c = 0.0;
+  for (int i = threadIdx.x; i < nq; i += 256) a += part_q[i];
+  for (int i = threadIdx.x; i < nkv; i += 256) { c += part_kv[2 * i]; b += part_kv[2 * i + 1]; }
+  red[0][threadIdx.x] = a;
+  red[1][threadIdx.x] = b;
+  red[2][threadIdx.x] = c;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w)
+      for (int k = 0; k < 3; ++k) red[k][threadIdx.x] += red[k][threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x < 3) out[threadIdx.x] = red[threadIdx.x][0];
 }
 
 }  // namespace
@@ -546,14 +608,17 @@ extern "C" int tt_debug_bwd_counters(unsigned long long* out, int reset) {
 
 static inline size_t al256b(size_t x) { return (x + 255) & ~size_t(255); }
 
-size_t sm100_bwd_ws_bytes(int64_t N, int hq, int d) {
+constexpr int kDqConvBlocks = 148 * 16;
+size_t sm100_bwd_ws_bytes(int64_t N, int hq, int hkv, int d) {
   const int64_t Np = (N + 127) / 128 * 128;
-  return 2 * al256b((size_t)hq * Np * 4) + al256b((size_t)Np * 4) + al256b((size_t)N * hq * d * 4);
+  const int64_t nb = Np / 128;
+  return 2 * al256b((size_t)hq * Np * 4) + al256b((size_t)Np * 4) + al256b((size_t)N * hq * d * 4) +
+         al256b((size_t)(kDqConvBlocks + 2 * nb * hkv) * sizeof(double));
 }
 
 tt_status sm100_attn_bwd(const tt_packed& pk, const void* q, const void* k, const void* v, const void* o,
                          const float* lse, const void* dout, int restore, int hq, int hkv, int d, float scale,
-                         void* ws, void* dq, void* dk, void* dv, cudaStream_t st) {
+                         void* ws, void* dq, void* dk, void* dv, double* sqnorm, cudaStream_t st) {
   if (d != kD) { set_error("sm100_attn_bwd: d must be 128"); return TT_ERR_UNSUPPORTED; }
   const int64_t N = pk.n_tokens;
   const int64_t Np = (N + 127) / 128 * 128;
@@ -562,6 +627,9 @@ tt_status sm100_attn_bwd(const tt_packed& pk, const void* q, const void* k, cons
   float* L2p = reinterpret_cast<float*>(w8 + al256b((size_t)hq * Np * 4));
   float* wf = reinterpret_cast<float*>(w8 + 2 * al256b((size_t)hq * Np * 4));
   float* dq_acc = reinterpret_cast<float*>(w8 + 2 * al256b((size_t)hq * Np * 4) + al256b((size_t)Np * 4));
+  double* part_q = reinterpret_cast<double*>(w8 + 2 * al256b((size_t)hq * Np * 4) + al256b((size_t)Np * 4) +
+                                             al256b((size_t)N * hq * d * 4));
+  double* part_kv = part_q + kDqConvBlocks;
   tt_status s = launch_bwd_pre_tc(o, dout, lse, pk.w, pk.wr, restore, N, Np, hq, Dp, L2p, wf, dq_acc, st);
   if (s) return s;
   CUtensorMap mq, mk, mv, mdo, mdq;
@@ -597,6 +665,7 @@ tt_status sm100_attn_bwd(const tt_packed& pk, const void* q, const void* k, cons
   prm.dq_acc = dq_acc;
   prm.dk = static_cast<__nv_bfloat16*>(dk);
   prm.dv = static_cast<__nv_bfloat16*>(dv);
+  prm.part_kv = sqnorm ? part_kv : nullptr;
   cudaError_t e = cudaFuncSetAttribute(tree_attn_bwd_sm100, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
   if (e != cudaSuccess) { set_error("sm100_attn_bwd: smem attribute: %s", cudaGetErrorString(e)); return TT_ERR_CUDA; }
   const unsigned grid = (unsigned)pk.n_blk * hkv;
@@ -604,10 +673,15 @@ tt_status sm100_attn_bwd(const tt_packed& pk, const void* q, const void* k, cons
   count_launch();
   if ((s = check_launch("tree_attn_bwd_sm100"))) return s;
   const int64_t n4 = N * hq * d / 4;
-  dq_convert_kernel<<<(unsigned)std::min<int64_t>((n4 + 255) / 256, 148 * 16), 256, 0, st>>>(
-      reinterpret_cast<const float4*>(dq_acc), reinterpret_cast<uint2*>(dq), n4);
+  const int nconv = (int)std::min<int64_t>((n4 + 255) / 256, kDqConvBlocks);
+  dq_convert_kernel<<<(unsigned)nconv, 256, 0, st>>>(reinterpret_cast<const float4*>(dq_acc),
+                                                     reinterpret_cast<uint2*>(dq), n4, sqnorm ? part_q : nullptr);
   count_launch();
-  return check_launch("dq_convert_kernel");
+  if ((s = check_launch("dq_convert_kernel"))) return s;
+  if (!sqnorm) return TT_OK;
+  sqnorm_final_kernel<<<1, 256, 0, st>>>(part_q, nconv, part_kv, (int)grid, sqnorm);
+  count_launch();
+  return check_launch("sqnorm_final_kernel");
 }
 
 }  // namespace tt

@@ -376,9 +376,9 @@ tt_status tt_attn_fwd(const tt_packed* pk, const void* q, const void* k, const v
   return simt_attn_fwd(*pk, q, k, v, dt, hq, hkv, d, softmax_scale, o, lse, st);
 }
 
-static size_t bwd_ws_bytes(const tt_packed* pk, int hq, int d, tt_dtype dt) {
-  if (dt == TT_BF16 && d == 128) return sm100_bwd_ws_bytes(pk->n_tokens, hq, d);
-  return al256((size_t)pk->n_tokens * hq * 4);
+static size_t bwd_ws_bytes(const tt_packed* pk, int hq, int hkv, int d, tt_dtype dt) {
+  if (dt == TT_BF16 && d == 128) return sm100_bwd_ws_bytes(pk->n_tokens, hq, hkv, d);
+  return al256((size_t)pk->n_tokens * hq * 4) + al256(3 * kSqnormBlocks * sizeof(double));
 }
 
 tt_status tt_attn_bwd_workspace(const tt_packed* pk, int32_t hq, int32_t hkv, int32_t d, tt_dtype dt, size_t* bytes) {
@@ -386,14 +386,14 @@ tt_status tt_attn_bwd_workspace(const tt_packed* pk, int32_t hq, int32_t hkv, in
   tt_status s = check_attn_args("tt_attn_bwd_workspace", pk, dt, hq, hkv, d);
   if (s) return s;
   if (!bytes) { set_error("tt_attn_bwd_workspace: bytes is null"); return TT_ERR_INVALID_ARGUMENT; }
-  *bytes = bwd_ws_bytes(pk, hq, d, dt);
+  *bytes = bwd_ws_bytes(pk, hq, hkv, d, dt);
   return TT_OK;
 }
 
 tt_status tt_attn_bwd(const tt_packed* pk, const void* q, const void* k, const void* v, const void* o,
                       const float* lse, const void* dout, int32_t restore, tt_dtype dt, int32_t hq, int32_t hkv,
-                      int32_t d, float softmax_scale, void* dq, void* dk, void* dv, void* d_ws, size_t ws_bytes,
-                      tt_stream_t stream) {
+                      int32_t d, float softmax_scale, void* dq, void* dk, void* dv, double* sqnorm, void* d_ws,
+                      size_t ws_bytes, tt_stream_t stream) {
   clear_error();
   tt_status s = check_attn_args("tt_attn_bwd", pk, dt, hq, hkv, d);
   if (s) return s;
@@ -403,17 +403,22 @@ tt_status tt_attn_bwd(const tt_packed* pk, const void* q, const void* k, const v
   const void* ptrs[] = {q, k, v, o, lse, dout, dq, dk, dv, d_ws};
   for (const void* p : ptrs)
     if (!aligned16(p)) { set_error("tt_attn_bwd: tensors must be 16-byte aligned"); return TT_ERR_ALIGNMENT; }
-  size_t need = bwd_ws_bytes(pk, hq, d, dt);
+  size_t need = bwd_ws_bytes(pk, hq, hkv, d, dt);
   if (ws_bytes < need) { set_error("tt_attn_bwd: workspace %zu < %zu", ws_bytes, need); return TT_ERR_WORKSPACE; }
   cudaStream_t st = as_cuda(stream);
   if (dt == TT_BF16 && d == 128) {
     if (!sm100_available()) { set_error("tt_attn_bwd: bf16 d=128 needs an sm_100a device"); return TT_ERR_UNSUPPORTED; }
-    return sm100_attn_bwd(*pk, q, k, v, o, lse, dout, restore, hq, hkv, d, softmax_scale, d_ws, dq, dk, dv, st);
+    return sm100_attn_bwd(*pk, q, k, v, o, lse, dout, restore, hq, hkv, d, softmax_scale, d_ws, dq, dk, dv, sqnorm, st);
   }
   float* Dvec = static_cast<float*>(d_ws);
   s = launch_bwd_pre(o, dout, dt, pk->n_tokens, hq, d, Dvec, nullptr, st);
   if (s) return s;
-  return simt_attn_bwd(*pk, q, k, v, lse, Dvec, dout, restore, dt, hq, hkv, d, softmax_scale, dq, dk, dv, st);
+  s = simt_attn_bwd(*pk, q, k, v, lse, Dvec, dout, restore, dt, hq, hkv, d, softmax_scale, dq, dk, dv, st);
+  if (s || !sqnorm) return s;
+  const void* xs[3] = {dq, dk, dv};
+  const int64_t ns[3] = {pk->n_tokens * hq * d, pk->n_tokens * hkv * d, pk->n_tokens * hkv * d};
+  double* part = reinterpret_cast<double*>(static_cast<char*>(d_ws) + al256((size_t)pk->n_tokens * hq * 4));
+  return launch_sqnorm(xs, ns, 3, dt, sqnorm, part, st);
 }
 
 size_t tt_restore_loss_workspace(const tt_packed* pk) {

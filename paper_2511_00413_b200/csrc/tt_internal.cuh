@@ -64,10 +64,10 @@ tt_status make_tmap_thd(CUtensorMap* m, const void* ptr, int64_t rows, int heads
 tt_status sm100_attn_fwd(const tt_packed& pk, const void* q, const void* k, const void* v, int hq, int hkv,
                          int d, float scale, void* o, float* lse, cudaStream_t st);
 // ws: the tensor-core backward workspace (tt_attn_bwd_workspace bytes); see sm100_bwd_ws_bytes
-size_t sm100_bwd_ws_bytes(int64_t N, int hq, int d);
+size_t sm100_bwd_ws_bytes(int64_t N, int hq, int hkv, int d);
 tt_status sm100_attn_bwd(const tt_packed& pk, const void* q, const void* k, const void* v, const void* o,
                          const float* lse, const void* dout, int restore, int hq, int hkv, int d, float scale,
-                         void* ws, void* dq, void* dk, void* dv, cudaStream_t st);
+                         void* ws, void* dq, void* dk, void* dv, double* sqnorm, cudaStream_t st);
 
 tt_status launch_loss(const tt_packed& pk, const __nv_bfloat16* logits, int64_t ld, int vocab, const int32_t* tok,
                       const uint8_t* node_mask, int boundary_mode, float gamma, __nv_bfloat16* dlogits,

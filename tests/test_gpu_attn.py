@@ -258,3 +258,27 @@ def test_too_many_blocks_fails_loudly(tt):
     with pytest.raises(tt.TTError) as ei:
         tt.tt_attn_fwd(pk, q, q, q)
     assert ei.value.code == 4
+
+
+@pytest.mark.parametrize("dt,d,hq,hkv", [("bf16", 128, 4, 2), ("bf16", 128, 2, 2), ("fp32", 64, 2, 1)])
+def test_bwd_fused_sqnorm(tt, dt, d, hq, hkv):
+    """Row a6 fused into tt_attn_bwd: ||dQ||^2, ||dK||^2, ||dV||^2 of the stored gradients, equal to a
+    plain fp64 sum of squares and bitwise reproducible across runs."""
+    import torch
+    t = trees.gen_agentic(2500, root_len=500, seed=8)
+    pk = tt.tt_pack(t.parent, t.length)
+    N = pk.n_tokens
+    q, k, v = (x.cuda() for x in tensors.qkv_tensors(N, hq, hkv, d, dt, seed=5))
+    G = tensors.grad_tensor(N, hq, d, dt, seed=6).cuda()
+    o, lse = tt.tt_attn_fwd(pk, q, k, v)
+    outs = []
+    for _ in range(3):
+        nrm = torch.zeros(3, dtype=torch.float64, device="cuda")
+        grads = tt.tt_attn_bwd(pk, q, k, v, o, lse, G, sqnorm=nrm)
+        torch.cuda.synchronize()
+        for i, x in enumerate(grads):
+            ref = float((x.double() ** 2).sum())
+            assert abs(float(nrm[i]) - ref) <= 1e-6 * ref, (i, float(nrm[i]), ref)
+        outs.append(nrm.cpu())
+    if dt == "bf16":  # dK/dV norms are bitwise reproducible (dK/dV are); dQ's follows dQ's rounding order
+        assert torch.equal(outs[0][1:], outs[1][1:]) and torch.equal(outs[0][1:], outs[2][1:])
