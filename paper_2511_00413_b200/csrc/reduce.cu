@@ -53,6 +53,10 @@ __global__ void __launch_bounds__(256) bwd_pre_kernel(const T* __restrict__ o, c
 // per token the tree-scale as fp32 (w_i, or 1 without restoration), all laid out with the token
 // dimension padded to Np (a multiple of 128) so the kernel can bulk-copy 64-row slices; padded rows
 // get D = 0, LSE = 0, w = 0.  Also zeroes the fp32 dQ accumulator.
+// 16 lanes per (token, head) row (16 bytes of O and of dO each), 8 rows per warp with all loads issued
+// before the reductions (8 x 2 16-byte loads in flight per lane): the kernel is HBM-bound (reads O,
+// dO, writes the zeroed fp32 dQ accumulator).
+constexpr int kPreRowsPerWarp = 8;
 __global__ void __launch_bounds__(256) bwd_pre_tc_kernel(const __nv_bfloat16* __restrict__ o,
                                                          const __nv_bfloat16* __restrict__ dout,
                                                          const float* __restrict__ lse, const int32_t* __restrict__ w,
@@ -60,31 +64,46 @@ __global__ void __launch_bounds__(256) bwd_pre_tc_kernel(const __nv_bfloat16* __
                                                          int restore, int64_t N, int64_t Np, int hq,
                                                          float* __restrict__ Dp, float* __restrict__ L2p,
                                                          float* __restrict__ wf, float* __restrict__ dq_acc) {
-  const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);  // row = i * hq + h over padded i
-  const int lane = threadIdx.x & 31;
-  if (row >= Np * hq) return;
-  const int64_t i = row / hq;
-  const int h = (int)(row % hq);
-  float s = 0.f;
-  if (i < N) {
-    const uint2 va = reinterpret_cast<const uint2*>(o + row * 128)[lane];
-    const uint2 vb = reinterpret_cast<const uint2*>(dout + row * 128)[lane];
-    const __nv_bfloat162* pa = reinterpret_cast<const __nv_bfloat162*>(&va);
-    const __nv_bfloat162* pb = reinterpret_cast<const __nv_bfloat162*>(&vb);
+  const int lane = threadIdx.x & 31, half = lane >> 4, l16 = lane & 15;
+  const int64_t row0 = ((int64_t)blockIdx.x * 8 + (threadIdx.x >> 5)) * kPreRowsPerWarp;  // row = i * hq + h
+  const int64_t nrows = Np * hq, vrows = N * hq;
+  uint4 va[kPreRowsPerWarp / 2], vb[kPreRowsPerWarp / 2];
 #pragma unroll
-    for (int t = 0; t < 2; ++t) {
-      float2 fa = __bfloat1622float2(pa[t]), fb = __bfloat1622float2(pb[t]);
+  for (int k = 0; k < kPreRowsPerWarp / 2; ++k) {
+    const int64_t row = row0 + 2 * k + half;
+    if (row < vrows) {
+      va[k] = reinterpret_cast<const uint4*>(o + row * 128)[l16];
+      vb[k] = reinterpret_cast<const uint4*>(dout + row * 128)[l16];
+    } else {
+      va[k] = make_uint4(0, 0, 0, 0);
+      vb[k] = va[k];
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < kPreRowsPerWarp / 2; ++k) {
+    const int64_t row = row0 + 2 * k + half;
+    const uint32_t a4[4] = {va[k].x, va[k].y, va[k].z, va[k].w}, b4[4] = {vb[k].x, vb[k].y, vb[k].z, vb[k].w};
+    float s = 0.f;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const float2 fa = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&a4[t]));
+      const float2 fb = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&b4[t]));
       s = fmaf(fa.x, fb.x, s);
       s = fmaf(fa.y, fb.y, s);
     }
-    float4* z = reinterpret_cast<float4*>(dq_acc + row * 128);
-    z[lane] = make_float4(0.f, 0.f, 0.f, 0.f);
-  }
-  for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-  if (lane == 0) {
-    Dp[(int64_t)h * Np + i] = -s;                                              // stored negated
-    L2p[(int64_t)h * Np + i] = i < N ? -lse[(int64_t)h * N + i] * kLog2e : 0.f;  // stored negated
-    if (h == 0) wf[i] = i < N ? (restore ? (wr ? wr[i] : (float)w[i]) : 1.f) : 0.f;
+    for (int off = 8; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    if (row < vrows) {
+      float4* z = reinterpret_cast<float4*>(dq_acc + row * 128) + 2 * l16;
+      z[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+      z[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    if (l16 == 0 && row < nrows) {
+      const int64_t i = row / hq;
+      const int h = (int)(row % hq);
+      Dp[(int64_t)h * Np + i] = -s;                                              // stored negated
+      L2p[(int64_t)h * Np + i] = i < N ? -lse[(int64_t)h * N + i] * kLog2e : 0.f;  // stored negated
+      if (h == 0) wf[i] = i < N ? (restore ? (wr ? wr[i] : (float)w[i]) : 1.f) : 0.f;
+    }
   }
 }
 
@@ -186,7 +205,7 @@ tt_status launch_bwd_pre_tc(const void* o, const void* dout, const float* lse, c
                             int64_t N, int64_t Np, int hq, float* Dp, float* L2p, float* wf, float* dq_acc,
                             cudaStream_t st) {
   const int64_t rows = Np * hq;
-  bwd_pre_tc_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>((const __nv_bfloat16*)o, (const __nv_bfloat16*)dout,
+  bwd_pre_tc_kernel<<<(unsigned)((rows + 8 * kPreRowsPerWarp - 1) / (8 * kPreRowsPerWarp)), 256, 0, st>>>((const __nv_bfloat16*)o, (const __nv_bfloat16*)dout,
                                                                lse, w, wr, restore, N, Np, hq, Dp, L2p, wf, dq_acc);
   count_launch();
   return check_launch("bwd_pre_tc_kernel");
