@@ -91,6 +91,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   uint8_t* flags1 = flags0 + p.nb + 4;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long t_kernel0 = TT_CLK();
   // heavy (late) query blocks first; the q heads of one kv head adjacent
   const int gq = p.hq / p.hkv;
   const int pair = p.head_major ? p.npairs - 1 - (int)((blockIdx.x % (p.npairs * gq)) / gq)
@@ -191,6 +192,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       mbar_wait(bar_q, 0);
       if (T > 0) {
         mbar_wait(&full[0], 0);
+        if ((p.dbg & 8) && lane == 0) atomicAdd(&g_fwd_dbg[8], (unsigned long long)(TT_CLK() - t_kernel0));
         tc_fence_after();
 #pragma unroll
         for (int i = 0; i < 2; ++i)
@@ -411,6 +413,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
+  }
+  if ((p.dbg & 8) && threadIdx.x == 0) {
+    atomicAdd(&g_fwd_dbg[12], (unsigned long long)(TT_CLK() - t_kernel0));
+    atomicAdd(&g_fwd_dbg[13], 1ull);
   }
 }
 
