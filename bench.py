@@ -281,6 +281,16 @@ def linear_attention_time(job, reps=5):
 
 
 # ------------------------------------------------------------------------------------ cpu oracle
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def oracle_sample(job_tree, cfg, budget_s=20.0, nthreads=None):
     """Time the fp64 oracle (as it stands: per-branch linearisation, one std::thread per q head) on
     a bounded sample of the workload: H = min(Hq, host cores) heads over the first trajectories of
@@ -479,13 +489,15 @@ def main():
             my_pairs = sum(j.info["n_pairs"] for j in jobs)
             my_rows = sum(j.info["n_tokens"] for j in jobs)
             result["attn_fwd_bwd_tflops"] = round(my_flops / (attn_ms * 1e-3) / 1e12, 2)
-            traffic = {}
+            traffic, tpipe = {}, {}
             prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
             if os.path.exists(prof):
                 try:
-                    traffic = json.load(open(prof)).get(args.config, {})
+                    pj = json.load(open(prof))
+                    traffic = pj.get(args.config, {})
+                    tpipe = pj.get("tensor_pipe_pct", {}).get(args.config, {})
                 except Exception:
-                    traffic = {}
+                    traffic, tpipe = {}, {}
             # candidates for the dominant kernel of the step: attention bwd (tensor) and loss (HBM);
             # algorithmic work per launch / event-timed launch duration
             bwd_fl = 10.0 * j0.d * j0.hq * my_pairs
@@ -495,6 +507,7 @@ def main():
                             "achieved": round(ach, 2), "peak": peaks["bf16"], "unit": "TFLOP/s",
                             "frac": round(ach / peaks["bf16"], 4),
                             "traffic": traffic.get("tree_attn_bwd_sm100"),
+                            "ncu_tensor_pipe_pct": tpipe.get("tree_attn_bwd_sm100"),
                             "peak_source": peaks["source"] + ", dense bf16 burst",
                             "frac_of_sustained": round(ach / peaks["bf16_sustained"], 4),
                             "algorithmic": "10 d Hq A FLOPs per launch (A = ancestor pairs)",
@@ -598,7 +611,8 @@ def main():
                                "sample": f"fp64 oracle fwd+bwd, {cores} of {cfg['hq']} heads (one thread each), first {ntraj} trajectories "
                                          f"({share * 100:.3f}% of the workload's per-branch pairs x heads), "
                                          f"{dt:.1f} s measured, extrapolated linearly to the full tree",
-                               "extrapolated_full_step_s": round(full_s, 1)}
+                               "extrapolated_full_step_s": round(full_s, 1), "cpu_model": cpu_model(),
+                               "host_cpus": os.cpu_count()}
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:

@@ -28,6 +28,8 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxe
          "-Xptxas", "-warn-spills", "-I", os.path.join(ROOT, "include")]
 if os.environ.get("TT_PROFILE_COUNTERS"):
     FLAGS += ["-DTT_PROFILE_COUNTERS"]  # development cycle counters in the tensor-core kernels
+if os.environ.get("TT_EXTRA_NVCC_FLAGS"):
+    FLAGS += os.environ["TT_EXTRA_NVCC_FLAGS"].split()  # development A/B of compile-time variants
 
 
 def nvcc() -> str:
