@@ -78,7 +78,7 @@ constexpr uint32_t kDQStage = 32 * kD * 4;
 constexpr uint32_t kStatBytes = 768;                              // per stage: -LSE2 | -D | w (256 B each)
 constexpr uint32_t kOffStats = kOffDQ + 2 * kDQStage;
 constexpr uint32_t kOffBar = kOffStats + kQStages * kStatBytes;
-constexpr uint32_t kNumBars = 1 + 2 * kQStages + 12 + 1;
+constexpr uint32_t kNumBars = 1 + 2 * kQStages + 12 + 1 + 1;
 constexpr uint32_t kOffMisc = kOffBar + kNumBars * 8;
 // The dynamic shared-memory window is 1024-byte aligned on sm_100 (checked at run time; the kernel
 // traps otherwise), so no alignment slack is reserved.
@@ -87,7 +87,15 @@ constexpr uint32_t kOffRed = kOffMisc + 16;                       // a6 reductio
 constexpr uint32_t kSmemBytes = kOffRed + 64;
 static_assert(kSmemBytes <= 232448, "backward kernel exceeds 227 KB of shared memory");
 
-constexpr uint32_t kColDV = 0, kColDK = 128, kColS = 256, kColP = 384, kColQ = 448;
+// TT_BWD_KTMEM: K resident in TMEM (A operand of S^T = K Q^T as a TS MMA: the 32 KB per tile of K
+// re-reads from shared memory disappear) at the price of a single S^T buffer.
+#ifndef TT_BWD_KTMEM
+#define TT_BWD_KTMEM 1
+#endif
+constexpr bool kKT = TT_BWD_KTMEM != 0;
+// TMEM columns: dV 0-127 | dK 128-255 | S^T 256-319 (KTMEM) or S^T x2 256-383 | K 320-383 (KTMEM) |
+// dP^T 384-447 | dQ^T 448-511
+constexpr uint32_t kColDV = 0, kColDK = 128, kColS = 256, kColK = 320, kColP = 384, kColQ = 448;
 
 // development instrumentation (TT_DEBUG_BWD & 8): per-role cycle counters summed over CTAs
 __device__ unsigned long long g_bwd_dbg[16];
@@ -110,6 +118,7 @@ struct BwdParams {
   __nv_bfloat16* dk;
   __nv_bfloat16* dv;
   double* part_kv;  // nullable: [grid][2] fp64 partial sums of squares of this CTA's dV (0) / dK (1) rows
+  const __nv_bfloat16* kmat;  // K [N, hkv, 128] (KTMEM: rows copied into TMEM by the drain warpgroup)
 };
 
 __global__ void __maxnreg__(128)
@@ -133,6 +142,7 @@ __global__ void __maxnreg__(128)
   uint64_t* dp_full = dq_free + 2;        // dP^T(i) in TMEM
   uint64_t* dp_free = dp_full + 1;        // dP^T(i) read by the element-wise warps (256 arrivals)
   uint64_t* acc_done = dp_free + 1;
+  uint64_t* k_tmem = acc_done + 1;        // K written into TMEM (128 arrivals, KTMEM)
   uint32_t* misc = reinterpret_cast<uint32_t*>(smem + kOffMisc);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -159,6 +169,7 @@ __global__ void __maxnreg__(128)
       mbar_init(dp_full, 1);
       mbar_init(dp_free, 256);
       mbar_init(acc_done, 1);
+      mbar_init(k_tmem, 128);
       mbar_fence_init();
     }
     __syncwarp();
@@ -222,7 +233,10 @@ __global__ void __maxnreg__(128)
         for (int kk = 0; kk < 8; ++kk) {
           const uint32_t offk = (kk >> 2) * kKVChunk + (kk & 3) * 32;
           const uint32_t offq = (kk >> 2) * kQChunk + (kk & 3) * 32;
-          mma_ss_w(tm + kColS + 64 * b, sdesc(kb_s + offk, 16, 1024), sdesc(qb + offq, 16, 1024), idSP, kk > 0);
+          if constexpr (kKT)
+            mma_ts_w(tm + kColS, tm + kColK + 8 * kk, sdesc(qb + offq, 16, 1024), idSP, kk > 0);
+          else
+            mma_ss_w(tm + kColS + 64 * b, sdesc(kb_s + offk, 16, 1024), sdesc(qb + offq, 16, 1024), idSP, kk > 0);
         }
         return ob;
       };
@@ -240,12 +254,13 @@ __global__ void __maxnreg__(128)
       mbar_wait(kv_full, 0);
       // prologue: S(0) -> s_full[0], dP(0) -> dp_full, S(1) -> s_full[1]
       mbar_wait(&q_full[0], 0);
+      if constexpr (kKT) mbar_wait(k_tmem, 0);
       tc_fence_after();
       issue_SP(0);
       mma_commit_w(&s_full[0]);
       issue_dP(0);
       mma_commit_w(dp_full);
-      if (n_it > 1) {
+      if (!kKT && n_it > 1) {
         mbar_wait(&q_full[1], 0);
         tc_fence_after();
         issue_SP(1);
@@ -260,13 +275,21 @@ __global__ void __maxnreg__(128)
         const uint32_t qb = qs0 + s * 2 * kQTile;
         const uint32_t ob = qb + kQTile;
         const uint32_t dsb = ds0 + b * kDSTile;
-        { long long t0 = TT_CLK(); mbar_wait(&p_ready[b], (it >> 1) & 1); w_sm += TT_CLK() - t0; }
+        const int pb = kKT ? 0 : b;
+        { long long t0 = TT_CLK(); mbar_wait(&p_ready[pb], kKT ? (it & 1) : ((it >> 1) & 1)); w_sm += TT_CLK() - t0; }
         tc_fence_after();
         // dV += P^T dO   (A: P^T bf16 in TMEM over S^T[b]; B: dO MN-major, LBO = 8 KB d-chunk)
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)  // P^T of query columns 16 kk.. lives at S^T[b] + 32 (kk / 2) + 8 (kk % 2)
-          mma_ts_w(tm + kColDV, tm + kColS + 64 * b + 32 * (kk >> 1) + 8 * (kk & 1), sdesc(ob + kk * 2048, kQChunk, 1024),
+          mma_ts_w(tm + kColDV, tm + kColS + 64 * pb + 32 * (kk >> 1) + 8 * (kk & 1), sdesc(ob + kk * 2048, kQChunk, 1024),
                    idVK, (it > 0 || kk > 0) ? 1u : 0u);
+        // KTMEM: the single S^T buffer takes S^T(it+1) right after dV(it) has read P^T(it) from it
+        if (kKT && it + 1 < n_it) {
+          { long long t0 = TT_CLK(); mbar_wait(&q_full[(it + 1) % kQStages], ((it + 1) / kQStages) & 1); w_q += TT_CLK() - t0; }
+          tc_fence_after();
+          issue_SP(it + 1);
+          mma_commit_w(&s_full[0]);
+        }
         // next tile's dP^T (single buffer) as soon as the warps have read dP^T(it)
         if (it + 1 < n_it) {
           { long long t0 = TT_CLK(); mbar_wait(dp_free, it & 1); w_sm += TT_CLK() - t0; }
@@ -293,7 +316,7 @@ __global__ void __maxnreg__(128)
         mma_commit_w(&dq_full[0]);
         mma_commit_w(&q_empty[s]);
         // S^T(it+2) into S^T[b] (in issue order after dV(it) read P^T(it) from it)
-        if (it + 2 < n_it) {
+        if (!kKT && it + 2 < n_it) {
           { long long t0 = TT_CLK(); mbar_wait(&q_full[(it + 2) % kQStages], ((it + 2) / kQStages) & 1); w_q += TT_CLK() - t0; }
           tc_fence_after();
           issue_SP(it + 2);
@@ -315,6 +338,28 @@ __global__ void __maxnreg__(128)
     const int r = q4 * 32 + lane;                      // head-dim lane of dQ^T
     const uint32_t tl = tmem + ((uint32_t)(q4 * 32) << 16);
     long long c_wd = 0, c_dr = 0;
+    if constexpr (kKT) {
+      // K row (key k0 + r) -> TMEM lane r, columns kColK.. as packed bf16 pairs along d: the A-operand
+      // layout of a TS MMA (same packing as P^T)
+      const int64_t jr = k0 + r;
+      uint32_t kv[64];
+      if (jr < p.N) {
+        const uint4* src = reinterpret_cast<const uint4*>(p.kmat + (jr * p.hkv + hk) * kD);
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          const uint4 x = src[u];
+          kv[4 * u] = x.x; kv[4 * u + 1] = x.y; kv[4 * u + 2] = x.z; kv[4 * u + 3] = x.w;
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < 64; ++u) kv[u] = 0u;
+      }
+      tmem_st32(tl + kColK, *reinterpret_cast<const uint32_t(*)[32]>(&kv[0]));
+      tmem_st32(tl + kColK + 32, *reinterpret_cast<const uint32_t(*)[32]>(&kv[32]));
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(k_tmem);
+    }
     for (int it = 0; it < n_it; ++it) {
       const int h = hk * p.g + it / nq;
       const int q0 = (qt0 + it % nq) * kBQ;
@@ -384,12 +429,13 @@ __global__ void __maxnreg__(128)
     for (int it = 0; it < n_it; ++it) {
       const int s = it % kQStages, b = it & 1;
       const int q0 = (qt0 + it % nq) * kBQ;
-      { long long t0 = TT_CLK(); mbar_wait(&s_full[b], (it >> 1) & 1); c_ws += TT_CLK() - t0; }
+      const int sb = kKT ? 0 : b;
+      { long long t0 = TT_CLK(); mbar_wait(&s_full[sb], kKT ? (it & 1) : ((it >> 1) & 1)); c_ws += TT_CLK() - t0; }
       tc_fence_after();
       long long t_el = TT_CLK();
       if (p.dbg & 4) {
         tc_fence_before();
-        mbar_arrive(&p_ready[b]);
+        mbar_arrive(&p_ready[sb]);
         mbar_wait(dp_full, it & 1);
         tc_fence_after();
         tc_fence_before();
@@ -411,7 +457,7 @@ __global__ void __maxnreg__(128)
         {
           uint32_t sv[32], pwk[16];
           long long tA = TT_CLK();
-          tmem_ld32(tl + kColS + 64 * b + 32 * wg, sv);
+          tmem_ld32(tl + kColS + 64 * sb + 32 * wg, sv);
           tmem_wait_ld();
           c_ld += TT_CLK() - tA;
           tA = TT_CLK();
@@ -444,10 +490,10 @@ __global__ void __maxnreg__(128)
           }
           // P^T (bf16) over this warpgroup's own S^T[b] columns: [32 wg, 32 wg + 16) — never over
           // columns the other warpgroup may still be reading
-          tmem_st16(tl + kColS + 64 * b + 32 * wg, pwk);
+          tmem_st16(tl + kColS + 64 * sb + 32 * wg, pwk);
           tmem_wait_st();
           tc_fence_before();
-          mbar_arrive(&p_ready[b]);
+          mbar_arrive(&p_ready[sb]);
           c_math += TT_CLK() - tA;
         }
         // ---- phase dS (dP^T): dS^T = pw (dP - D) -> smem ----
@@ -666,6 +712,7 @@ tt_status sm100_attn_bwd(const tt_packed& pk, const void* q, const void* k, cons
   prm.dk = static_cast<__nv_bfloat16*>(dk);
   prm.dv = static_cast<__nv_bfloat16*>(dv);
   prm.part_kv = sqnorm ? part_kv : nullptr;
+  prm.kmat = static_cast<const __nv_bfloat16*>(k);
   cudaError_t e = cudaFuncSetAttribute(tree_attn_bwd_sm100, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
   if (e != cudaSuccess) { set_error("sm100_attn_bwd: smem attribute: %s", cudaGetErrorString(e)); return TT_ERR_CUDA; }
   const unsigned grid = (unsigned)pk.n_blk * hkv;
