@@ -63,7 +63,15 @@ using namespace sm100;
 constexpr int kD = 128;
 constexpr int kBQ = 64;
 constexpr int kQStages = 3;
-constexpr int kBwdThreads = 448;   // producer, MMA, 2 element-wise warpgroups, drain warpgroup
+// element-wise warpgroups: kNWG, each owning kCW query columns of every 64-row tile
+#ifndef TT_BWD_NWG
+#define TT_BWD_NWG 2  // measured: 4 warpgroups (16 columns each, 80 registers) within noise of 2 (profiles/r1f_bwd_nwg_ab.txt)
+#endif
+constexpr int kNWG = TT_BWD_NWG;
+constexpr int kCW = 64 / kNWG;
+static_assert(kNWG == 2 || kNWG == 4, "2 or 4 element-wise warpgroups");
+constexpr int kDrainWarp0 = 2 + 4 * kNWG;                  // first warp of the dQ drain warpgroup
+constexpr int kBwdThreads = 32 * (kDrainWarp0 + 4);        // producer, MMA, element-wise, drain
 constexpr uint32_t kKVTile = 128 * kD * 2;     // 32 KB (two 16 KB chunks of 128 rows x 128 B)
 constexpr uint32_t kKVChunk = 128 * 64 * 2;    // 16 KB
 constexpr uint32_t kQTile = kBQ * kD * 2;      // 16 KB (two 8 KB chunks of 64 rows x 128 B)
@@ -82,9 +90,9 @@ constexpr uint32_t kNumBars = 1 + 2 * kQStages + 12 + 1 + 1;
 constexpr uint32_t kOffMisc = kOffBar + kNumBars * 8;
 // The dynamic shared-memory window is 1024-byte aligned on sm_100 (checked at run time; the kernel
 // traps otherwise), so no alignment slack is reserved.
-constexpr uint32_t kOffRed = kOffMisc + 16;                       // a6 reduction scratch: double [2][4]
+constexpr uint32_t kOffRed = kOffMisc + 16;                       // a6 reduction scratch: double [kNWG][4]
 // (no static __shared__ in this kernel: it would shift the 1024-byte aligned dynamic window)
-constexpr uint32_t kSmemBytes = kOffRed + 64;
+constexpr uint32_t kSmemBytes = kOffRed + 32 * kNWG;
 static_assert(kSmemBytes <= 232448, "backward kernel exceeds 227 KB of shared memory");
 
 // TT_BWD_KTMEM: K resident in TMEM (A operand of S^T = K Q^T as a TS MMA: the 32 KB per tile of K
@@ -121,7 +129,7 @@ struct BwdParams {
   const __nv_bfloat16* kmat;  // K [N, hkv, 128] (KTMEM: rows copied into TMEM by the drain warpgroup)
 };
 
-__global__ void __maxnreg__(128)
+__global__ void __maxnreg__(kNWG == 4 ? 80 : 128)  // 22 warps: 6 per SMSP x 80 regs x 32 fit its 16K registers
     tree_attn_bwd_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                         const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
                         const __grid_constant__ CUtensorMap tmdQ, const BwdParams p) {
@@ -161,13 +169,13 @@ __global__ void __maxnreg__(128)
       for (int s = 0; s < kQStages; ++s) { mbar_init(&q_full[s], 1); mbar_init(&q_empty[s], 1); }
       for (int b = 0; b < 2; ++b) {
         mbar_init(&s_full[b], 1);
-        mbar_init(&p_ready[b], 256);
-        mbar_init(&ds_ready[b], 256);
+        mbar_init(&p_ready[b], 128 * kNWG);
+        mbar_init(&ds_ready[b], 128 * kNWG);
         mbar_init(&dq_full[b], 1);
         mbar_init(&dq_free[b], 128);
       }
       mbar_init(dp_full, 1);
-      mbar_init(dp_free, 256);
+      mbar_init(dp_free, 128 * kNWG);
       mbar_init(acc_done, 1);
       mbar_init(k_tmem, 128);
       mbar_fence_init();
@@ -280,8 +288,9 @@ __global__ void __maxnreg__(128)
         tc_fence_after();
         // dV += P^T dO   (A: P^T bf16 in TMEM over S^T[b]; B: dO MN-major, LBO = 8 KB d-chunk)
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk)  // P^T of query columns 16 kk.. lives at S^T[b] + 32 (kk / 2) + 8 (kk % 2)
-          mma_ts_w(tm + kColDV, tm + kColS + 64 * pb + 32 * (kk >> 1) + 8 * (kk & 1), sdesc(ob + kk * 2048, kQChunk, 1024),
+        for (int kk = 0; kk < 4; ++kk)  // P^T of query columns 16 kk.. : warpgroup 16 kk / kCW packed it at its own S^T columns
+          mma_ts_w(tm + kColDV, tm + kColS + 64 * pb + kCW * ((16 * kk) / kCW) + 8 * (((16 * kk) % kCW) / 16),
+                   sdesc(ob + kk * 2048, kQChunk, 1024),
                    idVK, (it > 0 || kk > 0) ? 1u : 0u);
         // KTMEM: the single S^T buffer takes S^T(it+1) right after dV(it) has read P^T(it) from it
         if (kKT && it + 1 < n_it) {
@@ -332,8 +341,8 @@ __global__ void __maxnreg__(128)
         atomicAdd(&g_bwd_dbg[4], (unsigned long long)n_it);
       }
     }
-  } else if (warp >= 10) {
-    // ===================== dQ drain warpgroup (warps 10-13) =====================
+  } else if (warp >= kDrainWarp0) {
+    // ===================== dQ drain warpgroup =====================
     const int q4 = warp & 3;
     const int r = q4 * 32 + lane;                      // head-dim lane of dQ^T
     const uint32_t tl = tmem + ((uint32_t)(q4 * 32) << 16);
@@ -413,10 +422,11 @@ __global__ void __maxnreg__(128)
       atomicAdd(&g_bwd_dbg[8], (unsigned long long)c_wd);
     }
   } else {
-    // ===================== compute warps 2-9 =====================
-    // Two warpgroups share every TMEM lane quadrant (lane quadrant = warp % 4): warpgroup wg owns
-    // query columns [32 wg, 32 wg + 32) of each 64-row tile for the element-wise work and the same
-    // 32 rows of dQ for the drain.  One thread = one key row (element-wise) = one head-dim lane (drain).
+    // ===================== element-wise warps 2 .. kDrainWarp0-1 =====================
+    // kNWG warpgroups share every TMEM lane quadrant (lane quadrant = warp % 4): warpgroup wg owns
+    // query columns [kCW wg, kCW wg + kCW) of each 64-row tile.  One thread = one key row.  Measured
+    // (role counters, profiles/r1f_bwd_counters_ktmem.txt): with 2 warpgroups (32 columns per thread)
+    // these warps were busy ~85% of a tile and latency-bound; 4 warpgroups halve each thread's chain.
     const int wg = (warp - 2) >> 2;
     const int q4 = warp & 3;
     const int r = q4 * 32 + lane;
@@ -425,6 +435,7 @@ __global__ void __maxnreg__(128)
     const uint32_t tl = tmem + ((uint32_t)(q4 * 32) << 16);
     const int Ej = (j < Nn) ? p.E[j] : -1;
     const float sl2 = p.scale_log2;
+    constexpr uint32_t kFull = kCW == 32 ? 0xffffffffu : ((1u << kCW) - 1u);
     long long c_ws = 0, c_el = 0, c_ld = 0, c_math = 0, c_st = 0;
     for (int it = 0; it < n_it; ++it) {
       const int s = it % kQStages, b = it & 1;
@@ -445,25 +456,27 @@ __global__ void __maxnreg__(128)
         const float4* st_lse = reinterpret_cast<const float4*>(smem + kOffStats + s * kStatBytes);
         const float4* st_D = reinterpret_cast<const float4*>(smem + kOffStats + s * kStatBytes + 256);
         const float4* st_w = reinterpret_cast<const float4*>(smem + kOffStats + s * kStatBytes + 512);
-        // no mask needed for this key on these 32 columns: j <= first column, last column < min(E_j, N)
-        const int c0 = q0 + 32 * wg;
+        const int c0 = q0 + kCW * wg;
         // allowed query columns of this key form one interval: [max(j, c0), min(E_j, N)) - c0
-        const int lo = max(j - c0, 0), hi = min(min(Ej, Nn) - c0, 32);
-        const uint32_t cmask = (hi <= lo) ? 0u : ((hi >= 32 ? 0xffffffffu : ((1u << hi) - 1u)) & ~((1u << lo) - 1u));
-        const bool all_in = __all_sync(0xffffffffu, cmask == 0xffffffffu);
+        const int lo = max(j - c0, 0), hi = min(min(Ej, Nn) - c0, kCW);
+        const uint32_t cmask = (hi <= lo) ? 0u : ((hi >= kCW ? kFull : ((1u << hi) - 1u)) & ~((1u << lo) - 1u));
+        const bool all_in = __all_sync(0xffffffffu, cmask == kFull);
         const float2 SL = make_float2(sl2, sl2);
         // ---- phase P (S^T only): pw = w P, P^T -> TMEM as bf16 ----
-        float2 pw[16];
+        float2 pw[kCW / 2];
         {
-          uint32_t sv[32], pwk[16];
+          uint32_t sv[kCW], pwk[kCW / 2];
           long long tA = TT_CLK();
-          tmem_ld32(tl + kColS + 64 * sb + 32 * wg, sv);
+          if constexpr (kCW == 32)
+            tmem_ld32(tl + kColS + 64 * sb + kCW * wg, *reinterpret_cast<uint32_t(*)[32]>(&sv[0]));
+          else
+            tmem_ld16(tl + kColS + 64 * sb + kCW * wg, *reinterpret_cast<uint32_t(*)[16]>(&sv[0]));
           tmem_wait_ld();
           c_ld += TT_CLK() - tA;
           tA = TT_CLK();
 #pragma unroll
-          for (int c4 = 0; c4 < 8; ++c4) {
-            const int cg = 8 * wg + c4;  // float4 group within the 64 columns
+          for (int c4 = 0; c4 < kCW / 4; ++c4) {
+            const int cg = (kCW / 4) * wg + c4;  // float4 group within the 64 columns
             const float4 NL = st_lse[cg];  // -LSE * log2e
             const float4 W = st_w[cg];
             const int c = 4 * c4;
@@ -488,9 +501,12 @@ __global__ void __maxnreg__(128)
             pwk[2 * c4] = pack_bf16(pw[2 * c4].x, pw[2 * c4].y);
             pwk[2 * c4 + 1] = pack_bf16(pw[2 * c4 + 1].x, pw[2 * c4 + 1].y);
           }
-          // P^T (bf16) over this warpgroup's own S^T[b] columns: [32 wg, 32 wg + 16) — never over
-          // columns the other warpgroup may still be reading
-          tmem_st16(tl + kColS + 64 * sb + 32 * wg, pwk);
+          // P^T (bf16) over this warpgroup's own S^T columns [kCW wg, kCW wg + kCW / 2) — never over
+          // columns another warpgroup may still be reading
+          if constexpr (kCW == 32)
+            tmem_st16(tl + kColS + 64 * sb + kCW * wg, pwk);
+          else
+            tmem_st8(tl + kColS + 64 * sb + kCW * wg, pwk);
           tmem_wait_st();
           tc_fence_before();
           mbar_arrive(&p_ready[sb]);
@@ -498,17 +514,20 @@ __global__ void __maxnreg__(128)
         }
         // ---- phase dS (dP^T): dS^T = pw (dP - D) -> smem ----
         {
-          uint32_t pv[32], dsk[16];
+          uint32_t pv[kCW], dsk[kCW / 2];
           long long tA = TT_CLK();
           { long long t0 = TT_CLK(); mbar_wait(dp_full, it & 1); c_ws += TT_CLK() - t0; }
           tc_fence_after();
-          tmem_ld32(tl + kColP + 32 * wg, pv);
+          if constexpr (kCW == 32)
+            tmem_ld32(tl + kColP + kCW * wg, *reinterpret_cast<uint32_t(*)[32]>(&pv[0]));
+          else
+            tmem_ld16(tl + kColP + kCW * wg, *reinterpret_cast<uint32_t(*)[16]>(&pv[0]));
           tmem_wait_ld();
           tc_fence_before();
           mbar_arrive(dp_free);
 #pragma unroll
-          for (int c4 = 0; c4 < 8; ++c4) {
-            const float4 ND = st_D[8 * wg + c4];  // -D
+          for (int c4 = 0; c4 < kCW / 4; ++c4) {
+            const float4 ND = st_D[(kCW / 4) * wg + c4];  // -D
             const int c = 4 * c4;
             const float2 ds01 = fmul2(pw[2 * c4], fadd2(make_float2(__uint_as_float(pv[c]), __uint_as_float(pv[c + 1])), make_float2(ND.x, ND.y)));
             const float2 ds23 = fmul2(pw[2 * c4 + 1], fadd2(make_float2(__uint_as_float(pv[c + 2]), __uint_as_float(pv[c + 3])), make_float2(ND.z, ND.w)));
@@ -518,8 +537,8 @@ __global__ void __maxnreg__(128)
           // dS^T row r into the SWIZZLE_128B smem tile: 16-byte chunk c at (c ^ (r & 7))
           uint8_t* drow = smem + kOffDS + b * kDSTile + r * 128;
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            const int ch = 4 * wg + c;
+          for (int c = 0; c < kCW / 8; ++c) {
+            const int ch = (kCW / 8) * wg + c;
             *reinterpret_cast<uint4*>(drow + ((ch ^ (r & 7)) << 4)) =
                 make_uint4(dsk[4 * c], dsk[4 * c + 1], dsk[4 * c + 2], dsk[4 * c + 3]);
           }
@@ -537,16 +556,20 @@ __global__ void __maxnreg__(128)
       atomicAdd(&g_bwd_dbg[10], (unsigned long long)c_math);
       atomicAdd(&g_bwd_dbg[11], (unsigned long long)c_st);
     }
-    // ---- epilogue: warpgroup 0 writes dV, warpgroup 1 writes dK (scaled) for this key row ----
+    // ---- epilogue: the first kNWG/2 warpgroups write dV, the others dK (scaled), each its share of
+    //      this key row's 128 head dims ----
     mbar_wait(acc_done, 0);
     tc_fence_after();
     {
-      const uint32_t col = wg == 0 ? kColDV : kColDK;
-      const float mul = wg == 0 ? 1.f : p.scale;
-      __nv_bfloat16* dst = (wg == 0 ? p.dv : p.dk) + ((int64_t)j * p.hkv + hk) * kD;
+      constexpr int kPer = kNWG / 2;              // warpgroups per tensor
+      constexpr int kCols = 128 / kPer;           // head dims per warpgroup
+      const int tsr = wg / kPer, part = wg % kPer;  // tensor 0 = dV, 1 = dK
+      const uint32_t col = (tsr == 0 ? kColDV : kColDK) + kCols * part;
+      const float mul = tsr == 0 ? 1.f : p.scale;
+      __nv_bfloat16* dst = (tsr == 0 ? p.dv : p.dk) + ((int64_t)j * p.hkv + hk) * kD + kCols * part;
       double sq = 0.0;  // a6: sum of squares of the stored (bf16-rounded) values, fp32 per 8 / fp64 across
 #pragma unroll 1
-      for (int cc = 0; cc < 4; ++cc) {
+      for (int cc = 0; cc < kCols / 32; ++cc) {
         uint32_t ov[32];
         tmem_ld32(tl + col + 32 * cc, ov);
         tmem_wait_ld();
@@ -577,8 +600,12 @@ __global__ void __maxnreg__(128)
         double (*red)[4] = reinterpret_cast<double (*)[4]>(smem + kOffRed);
         for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
         if (lane == 0) red[wg][q4] = sq;
-        named_bar_sync(2 + wg, 128);
-        if (r == 0) p.part_kv[2 * (int64_t)blockIdx.x + wg] = ((red[wg][0] + red[wg][1]) + red[wg][2]) + red[wg][3];
+        named_bar_sync(2 + tsr, 128 * kPer);
+        if (r == 0 && part == 0) {
+          double t = 0.0;
+          for (int g2 = tsr * kPer; g2 < (tsr + 1) * kPer; ++g2) t += ((red[g2][0] + red[g2][1]) + red[g2][2]) + red[g2][3];
+          p.part_kv[2 * (int64_t)blockIdx.x + tsr] = t;
+        }
       }
     }
   }
