@@ -282,3 +282,34 @@ def test_bwd_fused_sqnorm(tt, dt, d, hq, hkv):
         outs.append(nrm.cpu())
     if dt == "bf16":  # dK/dV norms are bitwise reproducible (dK/dV are); dQ's follows dQ's rounding order
         assert torch.equal(outs[0][1:], outs[1][1:]) and torch.equal(outs[0][1:], outs[2][1:])
+
+
+@pytest.mark.parametrize("cfg,seed", [("agentic8k", 0), ("wide", None), ("deep32k", 1)])
+def test_full_size_tree_equals_linearised_kernels(tt, cfg, seed):
+    """SURVEY §8(d) full-scale consistency (a property at any size, checked at the BASELINE sizes and
+    bench launch configuration): the tree-packed fwd/bwd with restoration equals the same kernels run
+    on every trajectory linearised as its own sequence, outputs gathered and gradients scatter-added
+    back (Eqs. 14-16).  Not an oracle (it shares the kernels); the fp64 oracle covers sampled rows in
+    test_full_size_sampled_rows."""
+    import torch
+    t = trees.config_tree(cfg, seed)
+    c = trees.CONFIGS[cfg]
+    hq, hkv, d = c["hq"], c["hkv"], c["d"]
+    pk, (q, k, v, G, scale), (o, lse, dq, dk, dv) = _run(tt, t, hq, hkv, d, "bf16", seed=31)
+    opk = oracle.pack(t.parent, t.length)
+    paths = oracle.paths(opk)
+    idx = torch.as_tensor(np.concatenate(paths).astype(np.int64))
+    lin = tt.tt_pack([-1] * len(paths), [len(p) for p in paths])
+    qd, kd, vd, Gd = (x.cuda() for x in (q, k, v, G))
+    iq = idx.cuda()
+    lq, lk, lv, lg = (x.index_select(0, iq).contiguous() for x in (qd, kd, vd, Gd))
+    lo, llse = tt.tt_attn_fwd(lin, lq, lk, lv, scale)
+    ldq, ldk, ldv = tt.tt_attn_bwd(lin, lq, lk, lv, lo, llse, lg, restore=False, softmax_scale=scale)
+    torch.cuda.synchronize()
+    # forward: every linearised occurrence of a token equals the tree output at that token
+    assert max_abs(lo.cpu(), o[idx]) <= TOL_O_BF16
+    # backward: scatter-add of the per-branch gradients equals the restored tree gradients
+    for tree_g, lin_g, H in ((dq, ldq, hq), (dk, ldk, hkv), (dv, ldv, hkv)):
+        acc = torch.zeros(o.shape[0], H, d, dtype=torch.float32, device="cuda")
+        acc.index_add_(0, iq, lin_g.float())
+        assert rel_l2(tree_g, acc.cpu()) <= TOL_G_BF16
