@@ -568,6 +568,7 @@ struct LcArgs {
   __nv_bfloat16* dlogits;
   float *tok_loss, *ws_loss, *ws_omega;
   int32_t* d_err;
+  int nocompute;  // development ablation (TT_LOSS_NOCOMPUTE): stream the rows through without the math
 };
 
 __device__ __forceinline__ uint32_t lc_rank() { uint32_t r; asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r)); return r; }
@@ -748,6 +749,15 @@ __global__ void __launch_bounds__(kLcThreads, 1) loss_cluster_kernel(const LcArg
     const int xs_slot = it % kLcSlots;
     mbar_wait_(&mfull[b], (uint32_t)((it / NBUF) & 1));
     LcMeta M = lc_meta(meta_base, b, a.max_t);
+    if (a.nocompute) {
+      mbar_wait_(&full[b], (uint32_t)((it / NBUF) & 1));
+      bar_g();
+      if (gt == 0) {
+        mbar_arrive_(&done[b]);
+        mbar_arrive_(&mfree[b]);
+      }
+      continue;
+    }
     const int nt = M.hdr[0];
     const float Omega = reinterpret_cast<const float*>(M.hdr)[1];
     const bool bad_any = M.hdr[2] != 0;
@@ -994,6 +1004,7 @@ tt_status launch_loss(const tt_packed& pk, const __nv_bfloat16* logits, int64_t 
     LcArgs a{pk.n_tokens, logits, ld, vocab, 0, 0, tok, node_mask, boundary_mode, gamma, pk.w, pk.wr,
              pk.node, pk.node_start, pk.node_len, pk.succ_ptr, pk.succ_tok, dlogits, tok_loss, ws_loss, ws_omega, d_err};
     a.max_t = std::max(1, pk.max_succ);
+    a.nocompute = getenv("TT_LOSS_NOCOMPUTE") ? 1 : 0;
     if (variant == 1) done = try_launch_cluster<4, 3>(a, sms, st);  // fits while max_succ is small
     else if (variant == 11) done = try_launch_cluster<4, 3, 2, 0>(a, sms, st);
     else if (variant == 12) done = try_launch_cluster<4, 3, 2, 1>(a, sms, st);
