@@ -607,8 +607,10 @@ __device__ __forceinline__ LcMeta lc_meta(uint8_t* base, int slot, int max_t) {
 }
 
 // KPOLY: pairs (of 4 per 8-element vector) whose pass-2 exponentials run on the FMA pipe
-template <int CS, int NBUF, int KPOLY, int KP1, int FAST = 0>
+template <int CS, int NBUF, int KPOLY, int KP1, int FAST = 0, int NG = 2>
 __global__ void __launch_bounds__(kLcThreads, 1) loss_cluster_kernel(const LcArgs a) {
+  // NG compute groups of GT threads (2 x 256: groups alternate rows; 1 x 512: one row at a time)
+  constexpr int GT = 2 * kLcGroup / NG;
   extern __shared__ __align__(128) uint8_t lsm[];
   const int Cq = a.Cq;
   __nv_bfloat16* bufs = reinterpret_cast<__nv_bfloat16*>(lsm);                     // NBUF x Cq bf16
@@ -619,8 +621,8 @@ __global__ void __launch_bounds__(kLcThreads, 1) loss_cluster_kernel(const LcArg
   uint64_t* mfree = mfull + NBUF;                                                 // [NBUF] metadata consumed
   uint64_t* xchg = mfree + NBUF;                                                  // [kLcSlots]
   uint8_t* meta_base = reinterpret_cast<uint8_t*>(xchg + kLcSlots);
-  __shared__ float s_red[2][3][kLcGroup / 32];
-  __shared__ float s_max[2][kLcGroup / 32];
+  __shared__ float s_red[2][3][2 * kLcGroup / 32];
+  __shared__ float s_max[2][2 * kLcGroup / 32];
   __shared__ float s_lse[2];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t cr = lc_rank();
@@ -740,11 +742,11 @@ __global__ void __launch_bounds__(kLcThreads, 1) loss_cluster_kernel(const LcArg
   }
 
   // ===================== compute groups: group g takes rows it = g, g + 2, ... =====================
-  const int grp = warp / (kLcGroup / 32);
-  const int gt = tid - grp * kLcGroup, gw = gt >> 5;
-  auto bar_g = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "n"(kLcGroup) : "memory"); };
+  const int grp = warp / (GT / 32);
+  const int gt = tid - grp * GT, gw = gt >> 5;
+  auto bar_g = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "n"(GT) : "memory"); };
   int it = grp;
-  for (int64_t row = row0 + grp * rstep; row < a.N; row += 2 * rstep, it += 2) {
+  for (int64_t row = row0 + grp * rstep; row < a.N; row += NG * rstep, it += NG) {
     const int b = it % NBUF;
     const int xs_slot = it % kLcSlots;
     mbar_wait_(&mfull[b], (uint32_t)((it / NBUF) & 1));
@@ -771,7 +773,7 @@ __global__ void __launch_bounds__(kLcThreads, 1) loss_cluster_kernel(const LcArg
       // with packed f32x2 FMAs / adds — no online rescaling, ~3 issue slots per element
       __nv_bfloat162 mx = __halves2bfloat162(__ushort_as_bfloat16((unsigned short)0xff80u),
                                              __ushort_as_bfloat16((unsigned short)0xff80u));
-      for (int v = gt; v < n / 8; v += kLcGroup) {
+      for (int v = gt; v < n / 8; v += GT) {
         const uint4 q = x4[v];
         mx = __hmax2(__hmax2(mx, *reinterpret_cast<const __nv_bfloat162*>(&q.x)),
                      __hmax2(*reinterpret_cast<const __nv_bfloat162*>(&q.y), *reinterpret_cast<const __nv_bfloat162*>(&q.z)));
@@ -783,12 +785,12 @@ __global__ void __launch_bounds__(kLcThreads, 1) loss_cluster_kernel(const LcArg
       bar_g();
       tm = s_max[grp][0];
 #pragma unroll
-      for (int k = 1; k < kLcGroup / 32; ++k) tm = fmaxf(tm, s_max[grp][k]);
+      for (int k = 1; k < GT / 32; ++k) tm = fmaxf(tm, s_max[grp][k]);
       m = tm * kLog2e;  // group max, log2 units
       if (m != -INFINITY) {
         const float2 L2 = make_float2(kLog2e, kLog2e), NM = make_float2(-m, -m);
         float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
-        for (int v = gt; v < n / 8; v += kLcGroup) {
+        for (int v = gt; v < n / 8; v += GT) {
           const uint4 q = x4[v];
           const uint32_t in[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
@@ -803,7 +805,7 @@ __global__ void __launch_bounds__(kLcThreads, 1) loss_cluster_kernel(const LcArg
       }
       for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
     } else {
-      for (int v = gt; v < n / 8; v += kLcGroup) {
+      for (int v = gt; v < n / 8; v += GT) {
         const uint4 q = x4[v];
         Vec<8> r;
         r.u[0] = q.x; r.u[1] = q.y; r.u[2] = q.z; r.u[3] = q.w;
@@ -819,7 +821,7 @@ __global__ void __launch_bounds__(kLcThreads, 1) loss_cluster_kernel(const LcArg
     }
     // target logits that live in this slice (read before pass 2 overwrites them)
     float tx = 0.f;
-    for (int k = gt; k < nt; k += kLcGroup) {
+    for (int k = gt; k < nt; k += GT) {
       const int y = M.y[k];
       if (y >= off && y < off + n) {
         const float xy = __bfloat162float(xs[y - off]);
@@ -832,7 +834,7 @@ __global__ void __launch_bounds__(kLcThreads, 1) loss_cluster_kernel(const LcArg
     bar_g();
     if (gt == 0) {
       float Mx = -INFINITY, S = 0.f, TX = 0.f;
-      for (int k = 0; k < kLcGroup / 32; ++k) {
+      for (int k = 0; k < GT / 32; ++k) {
         const float m2 = s_red[grp][0][k], s2 = s_red[grp][1][k];
         const float mm = fmaxf(Mx, m2);
         S = (mm == -INFINITY) ? 0.f : S * ex2f(Mx - mm) + s2 * ex2f(m2 - mm);
@@ -877,7 +879,7 @@ __global__ void __launch_bounds__(kLcThreads, 1) loss_cluster_kernel(const LcArg
     uint4* y4 = reinterpret_cast<uint4*>(xs);
     if constexpr (FAST) {
       const float2 L2 = make_float2(kLog2e, kLog2e), NL = make_float2(-lse2, -lse2), G2 = make_float2(gO, gO);
-      for (int v = gt; v < n / 8; v += kLcGroup) {
+      for (int v = gt; v < n / 8; v += GT) {
         const uint4 q = y4[v];
         const uint32_t in[4] = {q.x, q.y, q.z, q.w};
         uint32_t o[4];
@@ -891,7 +893,7 @@ __global__ void __launch_bounds__(kLcThreads, 1) loss_cluster_kernel(const LcArg
         y4[v] = make_uint4(o[0], o[1], o[2], o[3]);
       }
     } else
-    for (int v = gt; v < n / 8; v += kLcGroup) {
+    for (int v = gt; v < n / 8; v += GT) {
       const uint4 q = y4[v];
       const uint32_t in[4] = {q.x, q.y, q.z, q.w};
       uint32_t o[4];
@@ -910,7 +912,7 @@ __global__ void __launch_bounds__(kLcThreads, 1) loss_cluster_kernel(const LcArg
     bar_g();
     // ---- fix-up of the target entries of this slice: gamma (Omega p_y - sum_{k: y_k = y} omega_k) ----
     if (!bad_any) {
-      for (int k = gt; k < nt; k += kLcGroup) {
+      for (int k = gt; k < nt; k += GT) {
         const int y = M.y[k];
         if (y < off || y >= off + n) continue;
         bool first = true;
@@ -942,13 +944,13 @@ size_t lc_smem(int Cq, int max_t) {
   return (size_t)NBUF * Cq * 2 + kLcSlots * CS * 16 + (4 * NBUF + kLcSlots) * 8 + (size_t)NBUF * (16 + (size_t)max_t * 12);
 }
 
-template <int CS, int NBUF, int KPOLY = 1, int KP1 = 0, int FAST = 0>
+template <int CS, int NBUF, int KPOLY = 1, int KP1 = 0, int FAST = 0, int NG = 2>
 bool try_launch_cluster(const LcArgs& a0, int sms, cudaStream_t st) {
   LcArgs a = a0;
   a.Cq = ((a.V + CS - 1) / CS + 7) / 8 * 8;
   const size_t smem = lc_smem<CS, NBUF>(a.Cq, a.max_t);
   if (smem + 1024 > 232448) return false;  // static shared memory + margin
-  auto kern = loss_cluster_kernel<CS, NBUF, KPOLY, KP1, FAST>;
+  auto kern = loss_cluster_kernel<CS, NBUF, KPOLY, KP1, FAST, NG>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
     cudaGetLastError();
     return false;
@@ -1013,6 +1015,7 @@ tt_status launch_loss(const tt_packed& pk, const __nv_bfloat16* logits, int64_t 
     else if (variant == 22) done = try_launch_cluster<4, 3, 2, 0, 1>(a, sms, st);
     else if (variant == 23) done = try_launch_cluster<4, 3, 2, 1, 1>(a, sms, st);
     else if (variant == 24) done = try_launch_cluster<4, 3, 1, 1, 1>(a, sms, st);
+    else if (variant == 26) done = try_launch_cluster<4, 3, 1, 1, 1, 1>(a, sms, st);
     else if (variant == 31) done = try_launch_cluster<8, 5, 1, 1, 1>(a, sms, st);
     else if (variant == 32) done = try_launch_cluster<8, 4, 1, 1, 1>(a, sms, st);
     else if (variant == 33) done = try_launch_cluster<2, 1, 1, 1, 1>(a, sms, st);
