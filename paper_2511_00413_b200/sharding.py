@@ -30,7 +30,9 @@ def lpt_partition(work: Sequence[int], world: int) -> Tuple[List[List[int]], flo
 
 
 def slot_size(n_trees: int, world: int) -> int:
-    return math.ceil(n_trees / world) * REC
+    # LPT may give one rank more than ceil(n / world) trees (many light trees vs a few heavy ones),
+    # so every slot holds all n_trees records (a few KB)
+    return n_trees * REC
 
 
 def pack_records(records, n_trees: int, world: int, device=None):

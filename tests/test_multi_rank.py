@@ -85,3 +85,21 @@ def test_reduce_is_world_size_invariant():
         slots = [sharding.pack_records([(t, recs[t]) for t in assign[r]], n_trees, world) for r in range(world)]
         totals.append(sharding.reduce_records(torch.cat(slots))[0])
     assert totals[0] == totals[1] == totals[2]
+
+
+def test_unequal_lpt_counts_fit_the_record_slot():
+    """One heavy tree and many light ones: LPT gives one rank 1 tree and the other ranks more than
+    ceil(n / world); every rank's records must still fit its all_gather slot."""
+    work = [1000] + [1] * 9
+    world = 4
+    assign, _ = sharding.lpt_partition(work, world)
+    assert max(len(a) for a in assign) > -(-len(work) // world)
+    recs = {t: _fake_record(t) for t in range(len(work))}
+    slots = [sharding.pack_records([(t, recs[t]) for t in assign[r]], len(work), world) for r in range(world)]
+    tot, n = sharding.reduce_records(torch.cat(slots))
+    assert n == len(work)
+    ref = [0.0] * 5
+    for t in range(len(work)):
+        for k, v in enumerate(recs[t]):
+            ref[k] += v
+    assert tot == ref
