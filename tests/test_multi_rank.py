@@ -88,9 +88,9 @@ def test_reduce_is_world_size_invariant():
 
 
 def test_unequal_lpt_counts_fit_the_record_slot():
-    """One heavy tree and many light ones: LPT gives one rank 1 tree and the other ranks more than
+    """Three heavy trees and many light ones: LPT gives the fourth rank all the light trees, more than
     ceil(n / world); every rank's records must still fit its all_gather slot."""
-    work = [1000] + [1] * 9
+    work = [1000, 1000, 1000] + [1] * 9
     world = 4
     assign, _ = sharding.lpt_partition(work, world)
     assert max(len(a) for a in assign) > -(-len(work) // world)
