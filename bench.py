@@ -415,11 +415,14 @@ def main():
     clocks = sampler.stop()
     step_ms = [a.elapsed_time(b) for a, b in step_ev]
     my_ms = float(sum(step_ms))
-    per_op = {}
+    per_op, per_op_med, per_op_min = {}, {}, {}
     for n in names:
         if n == "loss" and not with_loss:
             continue
-        per_op[n] = float(np.mean([sum(e[n][0].elapsed_time(e[n][1]) for e in es) for es in evs]))
+        xs = [sum(e[n][0].elapsed_time(e[n][1]) for e in es) for es in evs]
+        per_op[n] = float(np.mean(xs))
+        per_op_med[n] = round(float(np.median(xs)), 4)
+        per_op_min[n] = round(float(np.min(xs)), 4)
     flops_mine = sum(j.flops() for j in jobs) * args.steps
     t_max = my_ms
     flops_all = flops_mine
@@ -482,6 +485,10 @@ def main():
         }
         if per_op:
             result["per_op_ms"] = {k: round(v, 4) for k, v in per_op.items()}
+            result["per_op_ms_median"] = per_op_med
+            result["per_op_ms_min"] = per_op_min
+            result["step_ms_median"] = round(float(np.median(step_ms)), 4)
+            result["step_ms_min"] = round(float(np.min(step_ms)), 4)
             if len(jobs) > 1:
                 result["per_op_ms"]["note"] = f"summed over the rank's {len(jobs)} trees (rank 0)"
             attn_ms = per_op["fwd"] + per_op["bwd"]
