@@ -278,7 +278,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         tmem_wait_ld();
         // ---- mask (partial tiles; key columns past N on the ragged last block) ----
         const bool ragged = j0 + 64 > p.N;
-        if (cls == kClsPartial) {
+        if (cls == kClsPartial && !(p.dbg & 64)) {  // dbg 64: development ablation, partial tiles unmasked
           // int32 index math (N < 2^31): key c allowed iff c <= row - j0, c < N - j0, row < E_c
           const int4* Es = reinterpret_cast<const int4*>(smem + kOffE + (t % kStages) * 512) + 16 * hf;
           const int cmax = min((int)(row - j0), (int)(p.N - j0) - 1);
@@ -321,7 +321,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         //      exponentials run as a polynomial on the FMA pipe (FA4-style) ----
         const float2 SL = make_float2(sl2, sl2), NM = make_float2(-mb, -mb);
         float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
-        if (cls == kClsFull && !ragged) {
+        if ((cls == kClsFull || (p.dbg & 64)) && !ragged) {
 #pragma unroll
           for (int c = 0; c < 64; c += 4) {
             const float2 a01 = ffma2(make_float2(__uint_as_float(s[c]), __uint_as_float(s[c + 1])), SL, NM);

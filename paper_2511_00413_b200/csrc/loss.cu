@@ -549,7 +549,10 @@ __global__ void __launch_bounds__(1024) loss_sum_kernel(int64_t N, const float* 
 // for the online-rescaling passes; this form needs ~7.  25% of the exponentials of each pass run as a
 // degree-3 polynomial on the FMA pipe (relative error <= 7.5e-5 per term) to offload the MUFU unit.
 // ---------------------------------------------------------------------------------------------
-constexpr int kLcGroup = 256;                      // threads per compute group
+#ifndef TT_LOSS_GROUP
+#define TT_LOSS_GROUP 256
+#endif
+constexpr int kLcGroup = TT_LOSS_GROUP;            // threads per compute group
 constexpr int kLcThreads = 2 * kLcGroup + 64;      // 2 compute groups + producer warp + meta warp
 constexpr int kLcSlots = 4;                        // exchange slots (row it uses it % 4)
 
@@ -644,10 +647,14 @@ __global__ void __launch_bounds__(kLcThreads, 1) loss_cluster_kernel(const LcArg
 
   if (warp == 2 * kLcGroup / 32) {
     // ===================== producer warp: loads and stores of this CTA's slices =====================
-    if (lane == 0) {
+    // Lane b < NBUF owns buffer b (rows it = b, b + NBUF, ...): a lane's bulk async-groups track only
+    // its own buffer's store, so waiting for that store to have been read before reloading the
+    // buffer never waits on another buffer's store.
+    if (lane < NBUF) {
+      const int b = lane;
       uint64_t pol;
       asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-      auto load = [&](int b, int64_t row) {
+      auto load = [&](int64_t row) {
         if (n > 0) {
           mbar_expect_(&full[b], (uint32_t)n * 2);
           asm volatile(
@@ -659,14 +666,9 @@ __global__ void __launch_bounds__(kLcThreads, 1) loss_cluster_kernel(const LcArg
           mbar_arrive_(&full[b]);
         }
       };
-      for (int j = 0; j < NBUF; ++j) {
-        const int64_t row = row0 + j * rstep;
-        if (row >= a.N) break;
-        load(j, row);
-      }
-      int it = 0;
-      for (int64_t row = row0; row < a.N; row += rstep, ++it) {
-        const int b = it % NBUF;
+      if (row0 + b * rstep < a.N) load(row0 + b * rstep);
+      int it = b;
+      for (int64_t row = row0 + b * rstep; row < a.N; row += (int64_t)NBUF * rstep, it += NBUF) {
         mbar_wait_(&done[b], (uint32_t)((it / NBUF) & 1));
         if (n > 0) {
           asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(
@@ -677,8 +679,8 @@ __global__ void __launch_bounds__(kLcThreads, 1) loss_cluster_kernel(const LcArg
         }
         const int64_t nrow = row + (int64_t)NBUF * rstep;
         if (nrow < a.N) {
-          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // slice b free again
-          load(b, nrow);
+          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // this lane's slice b free again
+          load(nrow);
         }
       }
       asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
@@ -972,7 +974,8 @@ bool try_launch_cluster(const LcArgs& a0, int sms, cudaStream_t st) {
     cudaGetLastError();
     return false;
   }
-  const int64_t want = std::min<int64_t>((int64_t)ncl, a.N);
+  int64_t want = std::min<int64_t>((int64_t)ncl, a.N);
+  if (const char* mc = getenv("TT_LOSS_MAXCL")) want = std::min<int64_t>(want, std::max(1, atoi(mc)));  // dev: SM-count sweep
   if (getenv("TT_LOSS_DEBUG")) fprintf(stderr, "loss_cluster<%d,%d>: %d active clusters, Cq %d, smem %zu\n", CS, NBUF, ncl, a.Cq, smem);
   cfg.gridDim = dim3((unsigned)(want * CS));
   return cudaLaunchKernelEx(&cfg, kern, a) == cudaSuccess;
