@@ -18,7 +18,13 @@
  *   tt_restore_loss  next-token cross entropy with the tree-scale folded into every prediction
  *                    (the "gradient scaling step before the backward propagation"; R6-R8),
  *                    its gradient w.r.t. the logits, and deterministic fp64 sums.
- *   tt_grad_sqnorm   deterministic fp64 sum of squares (per-tree gradient-norm scalars).
+ *   tt_grad_sqnorm   deterministic fp64 sum of squares (per-tree gradient-norm scalars; also fused
+ *                    into tt_attn_bwd through its optional `sqnorm` output).
+ * Beyond the hot path:
+ *   tt_plan_traversals / tt_traversal_forest   capacity-constrained Tree Packing (NEXT-f1)
+ *   tt_rope / tt_restore_grad                  restored-position RoPE and the Gradient Scaler (NEXT-f2)
+ *   tt_lmhead_loss                             LM head + restoration loss without [N, V] logits (NEXT-f3)
+ *   tt_pack_weights                            real-valued per-trajectory weights (NEXT-f4)
  *
  * Conventions (all entry points):
  *   - Status: every call returns tt_status; TT_OK == 0.  On error nothing is launched and a
