@@ -340,12 +340,15 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             s[(c >> 1) + 1] = pack_bf16(p23.x, p23.y);
           }
         } else {
+          // masked / ragged tiles: masked scores are -inf; the polynomial share uses the variant that
+          // returns exactly 0 there
 #pragma unroll
           for (int c = 0; c < 64; c += 4) {
             const float2 a01 = ffma2(make_float2(__uint_as_float(s[c]), __uint_as_float(s[c + 1])), SL, NM);
             const float2 a23 = ffma2(make_float2(__uint_as_float(s[c + 2]), __uint_as_float(s[c + 3])), SL, NM);
             const float2 p01 = make_float2(ex2(a01.x), ex2(a01.y));
-            const float2 p23 = make_float2(ex2(a23.x), ex2(a23.y));
+            const float2 p23 = (TT_FWD_POLY == 2 || (TT_FWD_POLY == 1 && (c & 4))) ? exp2_poly2z(a23)
+                                                                                   : make_float2(ex2(a23.x), ex2(a23.y));
             acc0 = fadd2(acc0, p01);
             acc1 = fadd2(acc1, p23);
             s[c >> 1] = pack_bf16(p01.x, p01.y);

@@ -282,6 +282,12 @@ __device__ __forceinline__ float2 exp2_poly2(float2 x) {
                      __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
 }
 
+// exp2_poly2 that returns exactly 0 below 2^-125 (masked scores are -inf)
+__device__ __forceinline__ float2 exp2_poly2z(float2 x) {
+  const float2 e = exp2_poly2(x);
+  return make_float2(x.x < -125.f ? 0.f : e.x, x.y < -125.f ? 0.f : e.y);
+}
+
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
