@@ -249,14 +249,37 @@ def flush_l2(buf):
 
 
 # ------------------------------------------------------------------------------------ linear
+def trajectory_token_paths(pk, tree):
+    """Packed token indices of every root-to-leaf trajectory (childless nodes, or term copies),
+    from the product pack's own node_start / node_len (no oracle on this leg): the comparison input
+    of the per-branch linear runs."""
+    arr = pk.arrays()
+    start = arr["node_start"].cpu().numpy().astype(np.int64)
+    nlen = arr["node_len"].cpu().numpy().astype(np.int64)
+    par = np.asarray(tree.parent, dtype=np.int64)
+    n = len(par)
+    has_child = np.zeros(n, bool)
+    has_child[par[par >= 0]] = True
+    term = (~has_child).astype(np.int64) if tree.term is None else np.asarray(tree.term, dtype=np.int64)
+    ends = [v for v in range(n) for _ in range(int(term[v]))]
+    ends.sort(key=lambda v: (start[v], v))  # DFS pre-order of the end nodes
+    paths = []
+    for v in ends:
+        chain, u = [], v
+        while u >= 0:
+            chain.append(u)
+            u = int(par[u])
+        paths.append(np.concatenate([np.arange(start[u], start[u] + nlen[u]) for u in reversed(chain)]
+                                    + [np.zeros(0, np.int64)]))
+    return paths
+
+
 def linear_attention_time(job, reps=5):
     """Same kernels on the linearised forest (every root-to-leaf trajectory as its own root;
     untimed gather).  Returns (fwd+bwd ms, linear pairs, linear tokens)."""
     import torch
-    import oracle  # only for the trajectory paths of the comparison input (untimed setup)
     import paper_2511_00413_b200 as tt
-    opk = oracle.pack(job.tree.parent, job.tree.length)
-    paths = oracle.paths(opk)
+    paths = trajectory_token_paths(tt.tt_pack(job.tree.parent, job.tree.length, job.tree.term), job.tree)
     idx = torch.as_tensor(np.concatenate(paths).astype(np.int64), device="cuda")
     lens = [len(p) for p in paths]
     lq, lk, lv, lg = (x.index_select(0, idx).contiguous() for x in (job.q, job.k, job.v, job.g))
@@ -285,10 +308,9 @@ def linear_loss_time(job, max_rows=32768, reps=3):
     (w = 1), processed in chunks of whole trajectories (<= max_rows rows) through one in-place logits
     buffer (dlogits aliases logits), chunk times summed.  Returns (ms, linear rows)."""
     import torch
-    import oracle  # only for the trajectory lengths of the comparison input (untimed setup)
     import paper_2511_00413_b200 as tt
-    opk = oracle.pack(job.tree.parent, job.tree.length)
-    lens = [len(p) for p in oracle.paths(opk)]
+    lens = [len(p) for p in trajectory_token_paths(tt.tt_pack(job.tree.parent, job.tree.length, job.tree.term),
+                                                   job.tree)]
     chunks, cur = [], []
     for L in lens:
         if cur and sum(cur) + L > max_rows:
