@@ -19,6 +19,14 @@ the whole timed loop, max over ranks.
 
 `--impl reference` times the fp64 CPU oracle (oracle/) on the same workload/metric (bounded
 sample per step, extrapolated) — see the cpu_baseline notes in DESIGN.md.
+
+Besides the driver-contract keys the line carries: per_op_ms (+ median / min), attn_fwd_bwd_tflops,
+roofline (dominant kernel: algorithmic work per launch / event-timed duration vs MEASURED_PEAKS,
+ncu DRAM bytes and raw tensor-pipe % from profiles/ncu_traffic.json) and roofline_<other>,
+speedup_vs_linear (the same kernels on every trajectory linearised: attention vs the pair ratio,
+the loss vs the token ratio, both together), next_f1_planner, next_f2 (RoPE / Gradient Scaler
+GB/s), next_f3_lmhead (LM head + loss TFLOP/s), cpu_baseline (N = 1).  --no-linear / --no-e2e /
+--no-cpu / --no-lmhead / --no-loss skip legs (profiling runs).
 """
 from __future__ import annotations
 
