@@ -103,9 +103,33 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   const bool has1 = qa + 1 < p.nb && !(p.dbg & 16);  // dbg 16: development ablation, drop query tile 1
   const int kb_end = has1 ? qa + 2 : qa + 1;
 
+  // barriers first, so the producer can start the Q and first K/V loads before the tile-list merge
+  // (the first merged k-tile is the smaller of the two lists' first entries: both ascending)
+  if (warp == 1 && lane == 0) {
+    mbar_init(bar_q, 1);
+    for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&s_full[i], 1); mbar_init(&p_full[i], 256); mbar_init(&o_full[i], 1); }
+    mbar_fence_init();
+  }
   // ---- merged tile list of the two query blocks: kb | cls0 << 28 | cls1 << 30 ----
   for (int k = threadIdx.x; k < kb_end; k += kFwdThreads) { flags0[k] = 0; flags1[k] = 0; }
   __syncthreads();
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmQ);
+    tma_prefetch(&tmK);
+    tma_prefetch(&tmV);
+    mbar_expect_tx(bar_q, (has1 ? 2 : 1) * kTileBytes);
+    for (int i = 0; i < (has1 ? 2 : 1); ++i)
+      for (int c = 0; c < 2; ++c)
+        tma_load_3d(smem + kOffQ + i * kTileBytes + c * kChunkBytes, &tmQ, bar_q, c * 64, h, (qa + i) * 128);
+    int kb0 = p.fwd_list[tri_off(qa)] & kKbMask;
+    if (has1) kb0 = min(kb0, p.fwd_list[tri_off(qa + 1)] & kKbMask);
+    uint8_t* kd = smem + kOffKV;
+    mbar_expect_tx(&full[0], 2 * kTileBytes + 512);
+    bulk_load_1d(smem + kOffE, p.E + (int64_t)kb0 * 128, 512, &full[0]);
+    for (int c = 0; c < 2; ++c) tma_load_3d(kd + c * kChunkBytes, &tmK, &full[0], c * 64, hk, kb0 * 128);
+    for (int c = 0; c < 2; ++c) tma_load_3d(kd + kTileBytes + c * kChunkBytes, &tmV, &full[0], c * 64, hk, kb0 * 128);
+  }
   {
     const int n0 = p.fwd_cnt[qa];
     const int32_t* l0 = p.fwd_list + tri_off(qa);
@@ -128,12 +152,6 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     }
     if (lane == 0) misc[1] = cnt;
   } else if (warp == 1) {
-    if (lane == 0) {
-      mbar_init(bar_q, 1);
-      for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-      for (int i = 0; i < 2; ++i) { mbar_init(&s_full[i], 1); mbar_init(&p_full[i], 256); mbar_init(&o_full[i], 1); }
-      mbar_fence_init();
-    }
     __syncwarp();
     tmem_alloc(&misc[0], 512);
     tmem_relinquish();
@@ -146,15 +164,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 
   if (warp < 2) {
     if (warp == 0 && lane == 0) {
-      // ===================== TMA producer =====================
-      tma_prefetch(&tmQ);
-      tma_prefetch(&tmK);
-      tma_prefetch(&tmV);
-      mbar_expect_tx(bar_q, (has1 ? 2 : 1) * kTileBytes);
-      for (int i = 0; i < (has1 ? 2 : 1); ++i)
-        for (int c = 0; c < 2; ++c)
-          tma_load_3d(smem + kOffQ + i * kTileBytes + c * kChunkBytes, &tmQ, bar_q, c * 64, h, (qa + i) * 128);
-      for (int t = 0; t < T; ++t) {
+      // ===================== TMA producer (Q and k-tile 0 already issued above) =====================
+      for (int t = 1; t < T; ++t) {
         const int s = t % kStages;
         if (t >= kStages) mbar_wait(&empty[s], ((t / kStages) - 1) & 1);
         const int kb = tiles[t] & kKbMask;
