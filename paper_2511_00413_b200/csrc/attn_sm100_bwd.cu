@@ -180,14 +180,21 @@ __global__ void __maxnreg__(kNWG == 4 ? 80 : 128)  // 22 warps: 6 per SMSP x 80 
       mbar_init(k_tmem, 128);
       mbar_fence_init();
     }
-    __syncwarp();
-    tmem_alloc(&misc[0], 512);
-    tmem_relinquish();
   }
-  tc_fence_before();
+  // barriers visible to all; the producer (warp 0, which never touches TMEM) starts its loads now,
+  // while warp 1 allocates TMEM for the other warps (named barrier 5 over warps 1..)
   __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = misc[0];
+  uint32_t tmem = 0;
+  if (warp != 0) {
+    if (warp == 1) {
+      tmem_alloc(&misc[0], 512);
+      tmem_relinquish();
+    }
+    tc_fence_before();
+    named_bar_sync(5, kBwdThreads - 32);
+    tc_fence_after();
+    tmem = misc[0];
+  }
 
   if (warp == 0) {
     // ===================== producer (lane 0) =====================
