@@ -266,7 +266,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     float m = -INFINITY, l = 0.f;
     uint32_t sph = 0, par = 0;
     bool first = true;
-    long long c_ws = 0, c_cmp = 0, c_n = 0, c_bar = 0;
+    long long c_ws = 0, c_cmp = 0, c_n = 0, c_bar = 0, c_ldp = 0, c_mx = 0, c_ex = 0;
     if (i == 0 || has1) {
       for (int t = 0; t < T; ++t) {
         const int32_t e = tiles[t];
@@ -287,6 +287,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         tmem_ld32(tSh, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
         tmem_ld32(tSh + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
         tmem_wait_ld();
+        c_ldp += TT_CLK() - t_cmp;
         // ---- mask (partial tiles; key columns past N on the ragged last block) ----
         const bool ragged = j0 + 64 > p.N;
         if (cls == kClsPartial && !(p.dbg & 64)) {  // dbg 64: development ablation, partial tiles unmasked
@@ -319,6 +320,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 #pragma unroll
           for (int u = 0; u < 4; ++u) pm[u] = fmaxf(pm[u], __uint_as_float(s[c + u]));
         const float hmax = fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3]));
+        c_mx += TT_CLK() - t_cmp;
         xmax[((par * 2 + i) * 2 + hf) * 128 + r] = hmax;
         { const long long tb = TT_CLK(); named_bar_sync(1 + i, 256); c_bar += TT_CLK() - tb; }
         const float mx = fmaxf(hmax, xmax[((par * 2 + i) * 2 + (hf ^ 1)) * 128 + r]);
@@ -366,6 +368,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             s[(c >> 1) + 1] = pack_bf16(p23.x, p23.y);
           }
         }
+        c_ex += TT_CLK() - t_cmp;
         const float2 accs = fadd2(acc0, acc1);
         l = l * corr + (accs.x + accs.y);
         m = m_use;
@@ -419,6 +422,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         atomicAdd(&g_fwd_dbg[5], (unsigned long long)c_cmp);
         atomicAdd(&g_fwd_dbg[6], (unsigned long long)c_n);
         atomicAdd(&g_fwd_dbg[7], (unsigned long long)c_bar);
+        atomicAdd(&g_fwd_dbg[9], (unsigned long long)c_ldp);
+        atomicAdd(&g_fwd_dbg[10], (unsigned long long)c_mx);
+        atomicAdd(&g_fwd_dbg[11], (unsigned long long)c_ex);
       }
     }
   }

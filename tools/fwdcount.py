@@ -15,6 +15,8 @@ for cfg, seed in [("agentic8k", 0), ("deep32k", 1)]:
     n = max(n, 1)
     print(cfg, "merged tiles", T, "per-tile cycles: mma_total %.0f wait_p %.0f wait_kv %.0f | softmax(tile0,half0,r0) tiles %d: wait_s %.0f compute %.0f (of which max-exchange barrier %.0f)" %
           (b[0] / T, b[1] / T, b[2] / T, n, b[4] / n, b[5] / n, b[7] / n), flush=True)
+    print("   softmax phase ends (cumulative from S ready, per tile): tmem ld %.0f, mask+max %.0f, exp loop %.0f, total %.0f"
+          % (b[9] / n, b[10] / n, b[11] / n, b[5] / n), flush=True)
     nc = max(b[13], 1)
     print("   CTAs", b[13], "mean lifetime %.0f cycles, mean MMA loop %.0f, mean start->first K/V+Q ready %.0f, tiles/CTA %.1f" %
           (b[12] / nc, b[0] / nc, b[8] / nc, T / nc), flush=True)
