@@ -214,7 +214,8 @@ tt_status tt_attn_bwd(const tt_packed* pk, const void* q, const void* k, const v
  * Gradient-Restoration loss (R6, R7, R8, R17).  For every packed row t
  * with targets T(t) (next token inside the node, else the continuation list succ_tok; a target
  * counts iff node_loss_mask[node(target)] != 0 when the mask is given, and — boundary_mode 1 —
- * only when t has exactly one continuation), each target k with weight omega_k = w[k] (pk->wr[k]
+ * only when the trajectories through t continue to a single next token, i.e. at most one entry of
+ * the continuation list has w > 0 — subtrees carrying no trajectory are no branch), each target k with weight omega_k = w[k] (pk->wr[k]
  * when real-valued leaf weights are set, NEXT-f4):
  *   loss_t   = sum_k omega_k (lse(x_t) - x_t[tok[k]])
  *   dlogits_t = grad_scale * (Omega_t softmax(x_t) - sum_k omega_k e_{tok[k]}),  Omega_t = sum omega_k

@@ -56,7 +56,11 @@ __device__ __forceinline__ int lm_ntargets(const LmArgs& a, int64_t t, bool& las
   if (!last) return 1;
   sb = a.succ_ptr[u];
   const int se = a.succ_ptr[u + 1];
-  if (a.boundary_mode == 1 && se - sb > 1) return 0;
+  if (a.boundary_mode == 1) {  // exclude when the trajectories continue to more than one next token
+    int live = 0;
+    for (int k = sb; k < se && live < 2; ++k) live += (a.w[a.succ_tok[k]] > 0);
+    if (live > 1) return 0;
+  }
   return se - sb;
 }
 __device__ __forceinline__ int lm_target(const LmArgs& a, int64_t t, bool last, int sb, int k) {

@@ -33,6 +33,15 @@ constexpr int kMaxTargets = 1024;
 template <int W> struct Vec { uint32_t u[W / 2]; };
 
 // pass 1: streaming read that asks L2 to keep the line (it is re-read by pass 2)
+// boundary_mode 1 excludes a node's last token when the trajectories through it continue
+// to more than one next token: continuations are counted only if some trajectory passes through them
+// (w > 0: a child subtree with no trajectory end is no branch), matching the per-branch definition
+__device__ __forceinline__ bool diverges(const int32_t* succ_tok, int b, int e, const int32_t* w) {
+  int live = 0;
+  for (int k = b; k < e && live < 2; ++k) live += (w[succ_tok[k]] > 0);
+  return live > 1;
+}
+
 template <int W> __device__ __forceinline__ Vec<W> ld_keep(const __nv_bfloat16* p) {
   Vec<W> r;
   if constexpr (W == 16)
@@ -146,7 +155,7 @@ __global__ void __launch_bounds__(kLossThreads) loss_kernel(
         if (!node_mask || node_mask[node[tg]]) { s_y[0] = (int)tg; nt = 1; }
       } else {
         const int b = succ_ptr[u], e = succ_ptr[u + 1];
-        if (!(boundary_mode == 1 && e - b > 1)) {
+        if (!(boundary_mode == 1 && diverges(succ_tok, b, e, w))) {
           for (int k = b; k < e; ++k) {
             const int tg = succ_tok[k];
             if (!node_mask || node_mask[node[tg]]) s_y[nt++] = tg;
@@ -370,7 +379,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) loss_pipe_kernel(
         if (!node_mask || node_mask[node[tg]]) { s_y[0] = (int)tg; nt = 1; }
       } else {
         const int b = succ_ptr[u], e = succ_ptr[u + 1];
-        if (!(boundary_mode == 1 && e - b > 1)) {
+        if (!(boundary_mode == 1 && diverges(succ_tok, b, e, w))) {
           for (int k = b; k < e; ++k) {
             const int tg = succ_tok[k];
             if (!node_mask || node_mask[node[tg]]) s_y[nt++] = tg;
@@ -706,7 +715,7 @@ __global__ void __launch_bounds__(kLcThreads, 1) loss_cluster_kernel(const LcArg
           if (!a.node_mask || a.node_mask[a.node[tg]]) { M.y[0] = (int)tg; nt = 1; }
         } else {
           const int sb = a.succ_ptr[u], se = a.succ_ptr[u + 1];
-          if (!(a.boundary_mode == 1 && se - sb > 1)) {
+          if (!(a.boundary_mode == 1 && diverges(a.succ_tok, sb, se, a.w))) {
             for (int k = sb; k < se; ++k) {
               const int tg = a.succ_tok[k];
               if (!a.node_mask || a.node_mask[a.node[tg]]) M.y[nt++] = tg;

@@ -2,6 +2,8 @@
 [N, V] logits never materialised) against the fp64 oracle (oracle/lmhead.py: materialised logits,
 per-branch cross entropy, dH = dX W, dW = dX^T H).  Ragged vocabulary chunks, a single chunk, target-side
 node mask + boundary mode, and real-valued trajectory weights (NEXT-f4)."""
+from types import SimpleNamespace
+
 import numpy as np
 import pytest
 
@@ -26,13 +28,18 @@ CASES = [
     ("agentic700_onechunk", trees.gen_agentic(700, root_len=150, seed=3), 128, 3000, 1 << 20, {"gamma": 0.5}),
     ("wide_mask_boundary", trees.gen_wide(prefix=200, n_leaves=9), 64, 2048, 600, {"mask": True, "boundary_mode": 1}),
     ("agentic500_weights", trees.gen_agentic(500, root_len=100, seed=6), 128, 4096, 1000, {"weights": True}),
+    # explicit trajectory counts: node 1's second child carries no trajectory, so under boundary mode 1
+    # node 1's last token keeps its (single live) target while node 0's last token (two live) is excluded
+    ("term_boundary", SimpleNamespace(parent=[-1, 0, 0, 1, 1, 2, 2], length=[90, 70, 40, 130, 33, 20, 61],
+                                      term=[0, 0, 0, 1, 0, 2, 0]), 64, 1500, 512, {"boundary_mode": 1}),
 ]
 
 
 @pytest.mark.parametrize("name,t,D,V,vc,opt", CASES, ids=[c[0] for c in CASES])
 def test_lmhead_loss_matches_oracle(tt, name, t, D, V, vc, opt):
     import torch
-    pk = tt.tt_pack(t.parent, t.length)
+    term = getattr(t, "term", None)
+    pk = tt.tt_pack(t.parent, t.length, term)
     N = pk.n_tokens
     g = torch.Generator().manual_seed(11)
     H = torch.randn(N, D, generator=g).to(torch.bfloat16)
@@ -51,7 +58,7 @@ def test_lmhead_loss_matches_oracle(tt, name, t, D, V, vc, opt):
                                               node_loss_mask=mask, boundary_mode=opt.get("boundary_mode", 0),
                                               tok_loss=tl)
     torch.cuda.synchronize()
-    opk = oracle.pack(t.parent, t.length)
+    opk = oracle.pack(t.parent, t.length, term)
     r = ol.lmhead_loss(opk, to64(H), to64(W), tok.numpy(), gamma=gamma, node_loss_mask=mask,
                        boundary_mode=opt.get("boundary_mode", 0),
                        traj_weight=None if alpha is None else alpha.astype(np.float64))

@@ -5,6 +5,7 @@ path (d = 128) and the SIMT fp32 test mode (d = 64), and the restoration loss on
 with random node masks — every output compared element by element (attention O / LSE max-abs,
 gradients rel-L2, loss rows) at the north-star tolerances."""
 import math
+import os
 
 import numpy as np
 import pytest
@@ -16,6 +17,8 @@ from _util import TOL_G_BF16, TOL_G_FP32, TOL_O_BF16, TOL_O_FP32, max_abs, rel_l
 pytestmark = pytest.mark.gpu
 
 HEADS = [(1, 1), (2, 1), (4, 2), (4, 1), (3, 3), (8, 2)]
+# TT_SWEEP_SCALE=k multiplies the number of random cases (extended stress runs; default 1)
+_K = max(1, int(os.environ.get("TT_SWEEP_SCALE", "1")))
 
 
 @pytest.fixture(scope="module")
@@ -40,7 +43,7 @@ def _on_path(opk):
     return c > 0
 
 
-@pytest.mark.parametrize("seed", range(24))
+@pytest.mark.parametrize("seed", range(24 * _K))
 @pytest.mark.parametrize("mode", ["bf16_d128", "fp32_d64"])
 def test_random_attention(tt, seed, mode):
     import torch
@@ -71,7 +74,7 @@ def test_random_attention(tt, seed, mode):
             assert rel_l2(a, b) <= tol_g
 
 
-@pytest.mark.parametrize("seed", range(16))
+@pytest.mark.parametrize("seed", range(16 * _K))
 def test_random_loss(tt, seed):
     import torch
     t, rng = _forest(seed + 100)
