@@ -45,7 +45,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "tree-attn fwd+bwd effective TFLOP/s & % BF16 peak; speedup vs per-branch linear"
-LOSS_KERNEL = "loss_cluster_kernel"
+LOSS_KERNELS = ("loss_cluster_kernel", "loss_pipe_kernel")
 VOCAB = 151936
 
 
@@ -594,9 +594,13 @@ def main():
             if with_loss:
                 lb = my_rows * (4 * VOCAB + 12)
                 gbs = lb / (per_op["loss"] * 1e-3) / 1e9
-                cand["loss"] = {"bound": "hbm", "kernel": "tt_restore_loss (" + LOSS_KERNEL + " + loss_sum_kernel)" + per_launch,
+                # one launch = the clusters' rows + loss_pipe_kernel's tail rows on the SMs the clusters
+                # leave idle (side stream, joined) + the fixed-order sum; ncu bytes of both row kernels
+                ltr = [traffic.get(k) for k in LOSS_KERNELS if traffic.get(k) is not None]
+                cand["loss"] = {"bound": "hbm", "kernel": "tt_restore_loss (" + " + ".join(LOSS_KERNELS) + " + loss_sum_kernel)"
+                                + per_launch,
                                 "achieved": round(gbs, 1), "peak": peaks["hbm"], "unit": "GB/s",
-                                "frac": round(gbs / peaks["hbm"], 4), "traffic": traffic.get(LOSS_KERNEL),
+                                "frac": round(gbs / peaks["hbm"], 4), "traffic": sum(ltr) if ltr else None,
                                 "peak_source": peaks["source"] + ", HBM copy bandwidth",
                                 "algorithmic": "N (4 V + 12) bytes per launch (read + write bf16 logits row, "
                                                "token id, weight, loss)",

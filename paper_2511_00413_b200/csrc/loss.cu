@@ -18,6 +18,7 @@
 // the last token of every trajectory) skip both reads and only write zeros.
 #include <algorithm>
 #include <cstdio>
+#include <unordered_map>
 #include <cstdlib>
 
 #include "tt_internal.cuh"
@@ -324,7 +325,8 @@ __global__ void __launch_bounds__(kPipeThreads, 1) loss_pipe_kernel(
     const uint8_t* __restrict__ node_mask, int boundary_mode, float gamma, const int32_t* __restrict__ w, const float* __restrict__ wr,
     const int32_t* __restrict__ node, const int32_t* __restrict__ node_start, const int32_t* __restrict__ node_len,
     const int32_t* __restrict__ succ_ptr, const int32_t* __restrict__ succ_tok, __nv_bfloat16* dlogits,
-    float* __restrict__ tok_loss, float* __restrict__ ws_loss, float* __restrict__ ws_omega, int32_t* d_err) {
+    float* __restrict__ tok_loss, float* __restrict__ ws_loss, float* __restrict__ ws_omega, int32_t* d_err,
+    int64_t row_begin) {
   extern __shared__ __align__(128) uint8_t lsm[];
   __nv_bfloat16* ring = reinterpret_cast<__nv_bfloat16*>(lsm);            // kRing x 32 KB
   uint64_t* full = reinterpret_cast<uint64_t*>(lsm + kRing * kChunkElems * 2);
@@ -349,7 +351,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) loss_pipe_kernel(
       uint64_t pol;
       asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
       int g = 0;  // global chunk counter (ring slot = g % kRing)
-      for (int64_t row = blockIdx.x; row < N; row += gridDim.x) {
+      for (int64_t row = row_begin + blockIdx.x; row < N; row += gridDim.x) {
         const __nv_bfloat16* x = logits + row * ld;
         for (int c = 0; c < nchunk; ++c, ++g) {
           const int slot = g % kRing;
@@ -369,7 +371,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) loss_pipe_kernel(
   // ============ compute warps ============
   int g = 0;
   auto bar_c = [&]() { asm volatile("bar.sync 1, %0;" ::"n"(kPipeCompute) : "memory"); };
-  for (int64_t row = blockIdx.x; row < N; row += gridDim.x) {
+  for (int64_t row = row_begin + blockIdx.x; row < N; row += gridDim.x) {
     if (tid == 0) {
       const int32_t u = node[row];
       const bool last = row == (int64_t)node_start[u] + node_len[u] - 1;
@@ -956,6 +958,31 @@ size_t lc_smem(int Cq, int max_t) {
   return (size_t)NBUF * Cq * 2 + kLcSlots * CS * 16 + (4 * NBUF + kLcSlots) * 8 + (size_t)NBUF * (16 + (size_t)max_t * 12);
 }
 
+// The 4-CTA clusters do not tile every SM (GPCs whose SM count is not a multiple of 4: 33 clusters
+// = 132 of 148 SMs on B200).  The SMs they leave idle run loss_pipe_kernel (one CTA per SM, one row
+// at a time) over the tail rows on a side stream forked from and joined back into the caller's
+// stream; the row split follows the two kernels' measured per-SM row rates.
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+SideStream* side_stream() {
+  thread_local std::unordered_map<int, SideStream> per_dev;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  SideStream& ss = per_dev[dev];
+  if (!ss.s) {
+    if (cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming) != cudaSuccess) {
+      cudaGetLastError();
+      ss = SideStream{};
+      return nullptr;
+    }
+  }
+  return &ss;
+}
+
 template <int CS, int NBUF, int KPOLY = 1, int KP1 = 0, int FAST = 0, int NG = 2>
 bool try_launch_cluster(const LcArgs& a0, int sms, cudaStream_t st) {
   LcArgs a = a0;
@@ -988,7 +1015,36 @@ bool try_launch_cluster(const LcArgs& a0, int sms, cudaStream_t st) {
   if (const char* mc = getenv("TT_LOSS_MAXCL")) want = std::min<int64_t>(want, std::max(1, atoi(mc)));  // dev: SM-count sweep
   if (getenv("TT_LOSS_DEBUG")) fprintf(stderr, "loss_cluster<%d,%d>: %d active clusters, Cq %d, smem %zu\n", CS, NBUF, ncl, a.Cq, smem);
   cfg.gridDim = dim3((unsigned)(want * CS));
-  return cudaLaunchKernelEx(&cfg, kern, a) == cudaSuccess;
+  // tail rows for the SMs the clusters leave idle (split by per-SM row rate, pipe / cluster ~ 0.7: profiles/r1k_loss_split.txt)
+  const int idle = sms - (int)want * CS;
+  static const double ratio = [] {
+    const char* e = getenv("TT_LOSS_SPLIT");  // development A/B: 0 disables the split
+    return e ? atof(e) : 0.7;
+  }();
+  int64_t n_pipe = 0;
+  if (idle > 0 && ratio > 0 && a.N >= 8 * sms && (a.ld % 16 == 0) &&
+      ((reinterpret_cast<uintptr_t>(a.logits) | reinterpret_cast<uintptr_t>(a.dlogits)) % 32 == 0))
+    n_pipe = (int64_t)((double)a.N * idle * ratio / ((double)want * CS + idle * ratio));
+  SideStream* ss = n_pipe > 0 ? side_stream() : nullptr;
+  if (!ss) n_pipe = 0;
+  const int64_t N = a.N;
+  a.N = N - n_pipe;
+  if (ss && cudaEventRecord(ss->fork, st) != cudaSuccess) return false;
+  if (cudaLaunchKernelEx(&cfg, kern, a) != cudaSuccess) return false;
+  if (ss) {
+    // launched after the clusters so its CTAs land on the SMs they left free
+    const size_t psm = (size_t)kRing * kChunkElems * 2 + 2 * kRing * 8;
+    cudaFuncSetAttribute(loss_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm);
+    cudaStreamWaitEvent(ss->s, ss->fork, 0);
+    loss_pipe_kernel<<<(unsigned)idle, kPipeThreads, psm, ss->s>>>(
+        N, a.logits, a.ld, a.V, a.tok, a.node_mask, a.boundary_mode, a.gamma, a.w, a.wr, a.node, a.node_start,
+        a.node_len, a.succ_ptr, a.succ_tok, a.dlogits, a.tok_loss, a.ws_loss, a.ws_omega, a.d_err, N - n_pipe);
+    count_launch();
+    if (cudaGetLastError() != cudaSuccess) return false;
+    cudaEventRecord(ss->join, ss->s);
+    cudaStreamWaitEvent(st, ss->join, 0);
+  }
+  return true;
 }
 
 }  // namespace
@@ -1047,7 +1103,7 @@ tt_status launch_loss(const tt_packed& pk, const __nv_bfloat16* logits, int64_t 
     cudaFuncSetAttribute(loss_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     loss_pipe_kernel<<<(unsigned)std::min<int64_t>(pk.n_tokens, sms), kPipeThreads, smem, st>>>(
         pk.n_tokens, logits, ld, vocab, tok, node_mask, boundary_mode, gamma, pk.w, pk.wr, pk.node, pk.node_start,
-        pk.node_len, pk.succ_ptr, pk.succ_tok, dlogits, tok_loss, ws_loss, ws_omega, d_err);
+        pk.node_len, pk.succ_ptr, pk.succ_tok, dlogits, tok_loss, ws_loss, ws_omega, d_err, (int64_t)0);
   } else {
     loss_kernel<8><<<(unsigned)grid, kLossThreads, 0, st>>>(pk.n_tokens, logits, ld, vocab, tok, node_mask, boundary_mode,
                                                             gamma, pk.w, pk.wr, pk.node, pk.node_start, pk.node_len,

@@ -160,3 +160,40 @@ def test_loss_many_continuations(tt):
     g = to64(dl.cpu())
     assert np.all(np.abs(g - dx) <= 2.0 ** -8 * np.abs(dx) + 1e-5 * np.maximum(om, 1.0)[:, None])
     assert abs(sums.cpu()[0].item() - lr.sum()) <= 1e-5 * max(1.0, abs(lr.sum()))
+
+
+def test_loss_cluster_plus_tail_split(tt):
+    """>= 8 rows per SM: the 4-CTA clusters take the head rows and loss_pipe_kernel, on the SMs the
+    clusters leave idle (side stream forked from / joined into the caller's), the tail rows — every
+    row, the sums, a target-side mask and boundary mode 1 against the oracle."""
+    t = trees.gen_agentic(2400, root_len=200, seed=5)
+    mask = (np.arange(len(t.parent)) % 5 != 2).astype(np.uint8)
+    _compare(tt, t, V=4104, gamma=0.75, node_mask=mask, boundary_mode=1, inplace=True, seed=21)
+    _compare(tt, t, V=4104, gamma=1.0, seed=22)
+
+
+def test_loss_graph_capture_matches_eager(tt):
+    """tt_restore_loss captured into a CUDA graph (the side-stream fork/join is captured with it)
+    replays to the eager result bit for bit."""
+    import torch
+    t = trees.gen_agentic(2400, root_len=200, seed=5)
+    pk = tt.tt_pack(t.parent, t.length)
+    N, V = pk.n_tokens, 4104
+    x = tensors.logits_tensor(N, V, seed=31).cuda()
+    tok = tensors.token_ids(N, V, seed=32).cuda()
+    dl0 = torch.empty_like(x)
+    sums0, _, _, _ = tt.tt_restore_loss(pk, x, tok, dlogits=dl0)
+    torch.cuda.synchronize()
+    dl1 = torch.empty_like(x)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        tt.tt_restore_loss(pk, x, tok, dlogits=dl1)  # warm-up outside capture
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            sums1, _, _, _ = tt.tt_restore_loss(pk, x, tok, dlogits=dl1)
+    dl1.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(dl0, dl1)
+    assert torch.equal(sums0, sums1)

@@ -14,8 +14,8 @@ for c in deep32k wide batch64k; do
 done
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_agentic8k.csv \
   python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e --no-linear --no-lmhead > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:'tree_attn_fwd_sm100|tree_attn_bwd_sm100|loss_cluster' \
-  --launch-skip 9 --launch-count 3 -o $O/full_agentic8k -f \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:'tree_attn_fwd_sm100|tree_attn_bwd_sm100|loss_cluster|loss_pipe' \
+  --launch-skip 12 --launch-count 4 -o $O/full_agentic8k -f \
   python bench.py --steps 1 --warmup 3 --no-cpu --no-e2e --no-linear --no-lmhead > $O/ncu_full.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:'tree_attn_fwd_sm100|tree_attn_bwd_sm100' \
   --launch-skip 6 --launch-count 2 -o $O/full_deep32k -f \
