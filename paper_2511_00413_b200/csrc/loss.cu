@@ -966,12 +966,19 @@ struct SideStream {
   cudaStream_t s = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr;
 };
-SideStream* side_stream() {
+SideStream* side_stream(cudaStream_t st) {
   thread_local std::unordered_map<int, SideStream> per_dev;
   int dev = 0;
   cudaGetDevice(&dev);
   SideStream& ss = per_dev[dev];
   if (!ss.s) {
+    // never create resources inside a stream capture (the first call on this thread/device then
+    // runs without the split; later captures reuse the stream and events made outside)
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+      cudaGetLastError();
+      return nullptr;
+    }
     if (cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming) != cudaSuccess) {
@@ -1025,7 +1032,7 @@ bool try_launch_cluster(const LcArgs& a0, int sms, cudaStream_t st) {
   if (idle > 0 && ratio > 0 && a.N >= 8 * sms && (a.ld % 16 == 0) &&
       ((reinterpret_cast<uintptr_t>(a.logits) | reinterpret_cast<uintptr_t>(a.dlogits)) % 32 == 0))
     n_pipe = (int64_t)((double)a.N * idle * ratio / ((double)want * CS + idle * ratio));
-  SideStream* ss = n_pipe > 0 ? side_stream() : nullptr;
+  SideStream* ss = n_pipe > 0 ? side_stream(st) : nullptr;
   if (!ss) n_pipe = 0;
   const int64_t N = a.N;
   a.N = N - n_pipe;

@@ -197,3 +197,43 @@ def test_loss_graph_capture_matches_eager(tt):
     torch.cuda.synchronize()
     assert torch.equal(dl0, dl1)
     assert torch.equal(sums0, sums1)
+
+
+def test_loss_first_call_inside_capture(tt):
+    """On a thread that has never called tt_restore_loss, the first call happening inside a CUDA-graph
+    capture creates no stream / event (the split is skipped for it) and still replays correctly."""
+    import threading
+    import torch
+    t = trees.gen_agentic(2400, root_len=200, seed=7)
+    pk = tt.tt_pack(t.parent, t.length)
+    N, V = pk.n_tokens, 4104
+    x = tensors.logits_tensor(N, V, seed=41).cuda()
+    tok = tensors.token_ids(N, V, seed=42).cuda()
+    dl0 = torch.empty_like(x)
+    sums0, _, _, _ = tt.tt_restore_loss(pk, x, tok, dlogits=dl0)
+    torch.cuda.synchronize()
+    box = {}
+
+    def work():
+        try:
+            torch.cuda.set_device(x.device)
+            dl1 = torch.empty_like(x)
+            sums1 = torch.empty(2, dtype=torch.float64, device=x.device)
+            err = torch.zeros(1, dtype=torch.int32, device=x.device)
+            s = torch.cuda.Stream()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=s):
+                tt.tt_restore_loss(pk, x, tok, dlogits=dl1, sums=sums1, d_err=err)
+            g.replay()
+            torch.cuda.synchronize()
+            box["r"] = (dl1, sums1)
+        except Exception as e:  # surfaced in the main thread
+            box["e"] = e
+
+    th = threading.Thread(target=work)
+    th.start()
+    th.join()
+    assert "e" not in box, box.get("e")
+    dl1, sums1 = box["r"]
+    assert torch.equal(dl0, dl1)
+    assert torch.equal(sums0, sums1)
