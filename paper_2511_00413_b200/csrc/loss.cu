@@ -423,12 +423,37 @@ __global__ void __launch_bounds__(kPipeThreads, 1) loss_pipe_kernel(
       const int n = min(kChunkElems, V - c * kChunkElems);
       const uint4* src = reinterpret_cast<const uint4*>(ring + slot * kChunkElems);
       if (Omega != 0.f && !bad_any) {
-        for (int v = tid; v < n / 16; v += kPipeCompute) {  // 16 elements = 2 x uint4 per step
-          Vec<16> r;
-          const uint4 a = src[2 * v], b = src[2 * v + 1];
-          r.u[0] = a.x; r.u[1] = a.y; r.u[2] = a.z; r.u[3] = a.w;
-          r.u[4] = b.x; r.u[5] = b.y; r.u[6] = b.z; r.u[7] = b.w;
-          accum<16>(m, sum, r);
+        // per thread and chunk: max of its elements on packed bf16 pairs, at most one rescale of the
+        // running sum, then the sum of 2^(x log2e - m) with packed f32x2 FMAs / adds (the cluster
+        // kernel's FAST pass 1, thread-local so no barrier per chunk)
+        __nv_bfloat162 mx = __halves2bfloat162(__ushort_as_bfloat16((unsigned short)0xff80u),
+                                               __ushort_as_bfloat16((unsigned short)0xff80u));
+        for (int v = tid; v < n / 8; v += kPipeCompute) {
+          const uint4 q = src[v];
+          mx = __hmax2(__hmax2(mx, *reinterpret_cast<const __nv_bfloat162*>(&q.x)),
+                       __hmax2(*reinterpret_cast<const __nv_bfloat162*>(&q.y), *reinterpret_cast<const __nv_bfloat162*>(&q.z)));
+          mx = __hmax2(mx, *reinterpret_cast<const __nv_bfloat162*>(&q.w));
+        }
+        const float cm = fmaxf(__bfloat162float(mx.x), __bfloat162float(mx.y)) * kLog2e;
+        if (cm > m) {
+          sum *= ex2f(m - cm);  // m = -inf -> 0
+          m = cm;
+        }
+        if (m != -INFINITY) {
+          const float2 L2 = make_float2(kLog2e, kLog2e), NM = make_float2(-m, -m);
+          float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
+          for (int v = tid; v < n / 8; v += kPipeCompute) {
+            const uint4 q = src[v];
+            const uint32_t in[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              const float2 e2 = sm100::ffma2(bf2f(in[t]), L2, NM);
+              const float2 e = make_float2(ex2f(e2.x), ex2f(e2.y));
+              if (t & 1) acc1 = sm100::fadd2(acc1, e); else acc0 = sm100::fadd2(acc0, e);
+            }
+          }
+          const float2 acc = sm100::fadd2(acc0, acc1);
+          sum += acc.x + acc.y;
         }
       }
       __syncwarp();
@@ -480,12 +505,17 @@ __global__ void __launch_bounds__(kPipeThreads, 1) loss_pipe_kernel(
     if (lane == 0) s_red[1][warp] = lpart;
     // ---- pass 2: re-read from L2, write dlogits ----
     const float gO = gamma * Omega;
+    const float2 L2 = make_float2(kLog2e, kLog2e), NL = make_float2(-lse2, -lse2), G2 = make_float2(gO, gO);
     auto softmax16 = [&](const Vec<16>& a, __nv_bfloat16* dst) {
+      // packed f32x2 argument / scaling; 2 of every 8 pairs' exponentials as the degree-3 polynomial
+      // on the FMA pipe (as the cluster kernel's pass 2: error far below the bf16 output rounding)
       Vec<16> o;
 #pragma unroll
       for (int t = 0; t < 8; ++t) {
-        const float2 f = bf2f(a.u[t]);
-        o.u[t] = f2bf(gO * ex2f(fmaf(f.x, kLog2e, -lse2)), gO * ex2f(fmaf(f.y, kLog2e, -lse2)));
+        const float2 a2 = sm100::ffma2(bf2f(a.u[t]), L2, NL);
+        const float2 e = ((t & 3) == 3) ? sm100::exp2_poly2(a2) : make_float2(ex2f(a2.x), ex2f(a2.y));
+        const float2 r2 = sm100::fmul2(e, G2);
+        o.u[t] = f2bf(r2.x, r2.y);
       }
       st_vec<16>(dst, o);
     };
@@ -1029,7 +1059,7 @@ bool try_launch_cluster(const LcArgs& a0, int sms, cudaStream_t st) {
     return e ? atof(e) : 0.7;
   }();
   int64_t n_pipe = 0;
-  if (idle > 0 && ratio > 0 && a.N >= 8 * sms && (a.ld % 16 == 0) &&
+  if (idle > 0 && ratio > 0 && a.N >= 8 * sms && (a.V % 16 == 0) && (a.ld % 16 == 0) &&
       ((reinterpret_cast<uintptr_t>(a.logits) | reinterpret_cast<uintptr_t>(a.dlogits)) % 32 == 0))
     n_pipe = (int64_t)((double)a.N * idle * ratio / ((double)want * CS + idle * ratio));
   SideStream* ss = n_pipe > 0 ? side_stream(st) : nullptr;
@@ -1070,7 +1100,9 @@ tt_status launch_loss(const tt_packed& pk, const __nv_bfloat16* logits, int64_t 
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   // 1 CTA (1024 threads) per SM: 148 rows (~44 MB at V = 151,936) in flight, so pass 2 re-reads from L2
   const int64_t grid = std::min<int64_t>(pk.n_tokens, (int64_t)sms);
-  const bool v16 = (ld % 16 == 0) && ((reinterpret_cast<uintptr_t>(logits) | reinterpret_cast<uintptr_t>(dlogits)) % 32 == 0);
+  // loss_pipe_kernel: 16-element vectors over whole rows (V % 16 == 0) and 32-byte aligned rows
+  const bool v16 = (vocab % 16 == 0) && (ld % 16 == 0) &&
+                   ((reinterpret_cast<uintptr_t>(logits) | reinterpret_cast<uintptr_t>(dlogits)) % 32 == 0);
   static const int variant = [] {
     // development A/B: 0 ring/L2 kernel, 1 CS4x3 (else CS4x2), 3 CS8x4, 1x: poly splits, 2x: FAST passes
     // (packed-bf16 max pass + f32x2 sum pass + f32x2 dlogits), 3x: other cluster sizes

@@ -168,8 +168,15 @@ def test_loss_cluster_plus_tail_split(tt):
     row, the sums, a target-side mask and boundary mode 1 against the oracle."""
     t = trees.gen_agentic(2400, root_len=200, seed=5)
     mask = (np.arange(len(t.parent)) % 5 != 2).astype(np.uint8)
-    _compare(tt, t, V=4104, gamma=0.75, node_mask=mask, boundary_mode=1, inplace=True, seed=21)
-    _compare(tt, t, V=4104, gamma=1.0, seed=22)
+    n0 = tt.tt_launch_count()
+    _compare(tt, t, V=4096, gamma=0.75, node_mask=mask, boundary_mode=1, inplace=True, seed=21)
+    n_split = tt.tt_launch_count() - n0
+    _compare(tt, t, V=4096, gamma=1.0, seed=22)
+    # V % 16 != 0: no split (clusters only)
+    n0 = tt.tt_launch_count()
+    _compare(tt, t, V=4104, gamma=1.0, seed=23)
+    n_plain = tt.tt_launch_count() - n0
+    assert n_split == n_plain + 1  # the tail-row kernel ran in the split case (same pack launches)
 
 
 def test_loss_graph_capture_matches_eager(tt):
@@ -178,7 +185,7 @@ def test_loss_graph_capture_matches_eager(tt):
     import torch
     t = trees.gen_agentic(2400, root_len=200, seed=5)
     pk = tt.tt_pack(t.parent, t.length)
-    N, V = pk.n_tokens, 4104
+    N, V = pk.n_tokens, 4096
     x = tensors.logits_tensor(N, V, seed=31).cuda()
     tok = tensors.token_ids(N, V, seed=32).cuda()
     dl0 = torch.empty_like(x)
@@ -201,12 +208,13 @@ def test_loss_graph_capture_matches_eager(tt):
 
 def test_loss_first_call_inside_capture(tt):
     """On a thread that has never called tt_restore_loss, the first call happening inside a CUDA-graph
-    capture creates no stream / event (the split is skipped for it) and still replays correctly."""
+    capture creates no stream / event (the split is skipped for it) and still replays correctly
+    (against the eager, split result: equal up to bf16 rounding)."""
     import threading
     import torch
     t = trees.gen_agentic(2400, root_len=200, seed=7)
     pk = tt.tt_pack(t.parent, t.length)
-    N, V = pk.n_tokens, 4104
+    N, V = pk.n_tokens, 4096
     x = tensors.logits_tensor(N, V, seed=41).cuda()
     tok = tensors.token_ids(N, V, seed=42).cuda()
     dl0 = torch.empty_like(x)
@@ -235,5 +243,8 @@ def test_loss_first_call_inside_capture(tt):
     th.join()
     assert "e" not in box, box.get("e")
     dl1, sums1 = box["r"]
-    assert torch.equal(dl0, dl1)
-    assert torch.equal(sums0, sums1)
+    # the captured call ran unsplit (all rows on the clusters) while the eager one gave the tail rows
+    # to loss_pipe_kernel: same arithmetic up to fp32 rounding order, so equal to bf16 rounding
+    a, b = dl0.float(), dl1.float()
+    assert torch.all((a - b).abs() <= 2.0 ** -8 * a.abs() + 1e-6)
+    assert torch.allclose(sums0, sums1, rtol=1e-6, atol=0)

@@ -3,6 +3,8 @@ set -u
 O=gpurun_out/${1:-split}; mkdir -p $O
 python -m paper_2511_00413_b200.build > $O/build.log 2>&1
 timeout 600 python -m pytest tests/test_gpu_loss.py tests/test_gpu_weights.py tests/test_gpu_random_sweep.py -q -k "loss" > $O/pytest.txt 2>&1; echo "exit $?" >> $O/pytest.txt
+echo "== TT_LOSS_VARIANT=0 (loss_pipe_kernel alone, all rows)" >> $O/loss.txt
+TT_LOSS_VARIANT=0 timeout 120 python tools/timeloss.py >> $O/loss.txt 2>&1
 for v in ${VALS:-0 0.5 0.75 1.0 1.25}; do
   echo "== TT_LOSS_SPLIT=$v" >> $O/loss.txt
   TT_LOSS_SPLIT=$v timeout 120 python tools/timeloss.py >> $O/loss.txt 2>&1
