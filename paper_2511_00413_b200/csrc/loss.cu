@@ -293,15 +293,19 @@ __global__ void __launch_bounds__(kLossThreads) loss_kernel(
 }
 
 // ---------------------------------------------------------------------------------------------
-// Pipelined variant (V % 16 == 0, 32-byte aligned rows): warp 0 streams every row in 32 KB chunks
-// into a 4-slot shared-memory ring with TMA bulk copies (L2 evict_last policy, so pass 2 finds the
-// row in L2); 16 compute warps run pass 1 out of shared memory, then pass 2 re-reads the row from
-// L2 and writes dlogits while the producer is already prefetching the next row.
+// Pipelined variant (V % 16 == 0, 32-byte aligned rows): a producer warp streams every row in 32 KB
+// chunks into a 4-slot shared-memory ring with TMA bulk copies (L2 evict_last policy, so pass 2 finds
+// the row in L2); a meta warp resolves the targets and weights of the upcoming rows into a 2-slot
+// metadata ring; 16 compute warps run pass 1 out of shared memory (picking up the target logits on
+// the way), then pass 2 re-reads the row from L2 and writes dlogits while the producer is already
+// prefetching the next row.
 // ---------------------------------------------------------------------------------------------
 constexpr int kPipeCompute = 512;                 // compute threads
-constexpr int kPipeThreads = kPipeCompute + 32;   // + producer warp
+constexpr int kPipeThreads = kPipeCompute + 64;   // + producer warp + meta warp
 constexpr int kChunkElems = 16384;                // 32 KB of bf16
 constexpr int kRing = 4;
+constexpr int kMetaSlots = 2;                     // rows of metadata the meta warp runs ahead
+constexpr size_t kPipeSmem = (size_t)kRing * kChunkElems * 2 + (2 * kRing + 2 * kMetaSlots) * 8;
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init_(uint64_t* b, uint32_t c) {
@@ -331,16 +335,20 @@ __global__ void __launch_bounds__(kPipeThreads, 1) loss_pipe_kernel(
   __nv_bfloat16* ring = reinterpret_cast<__nv_bfloat16*>(lsm);            // kRing x 32 KB
   uint64_t* full = reinterpret_cast<uint64_t*>(lsm + kRing * kChunkElems * 2);
   uint64_t* empty = full + kRing;
-  __shared__ int s_y[kMaxTargets];
-  __shared__ float s_om[kMaxTargets];
-  __shared__ float s_xy[kMaxTargets];
-  __shared__ int s_nt;
+  uint64_t* mfull = empty + kRing;    // [kMetaSlots] row metadata ready
+  uint64_t* mfree = mfull + kMetaSlots;  // [kMetaSlots] row metadata consumed
+  __shared__ int s_y[kMetaSlots][kMaxTargets];     // target token ids (the meta warp resolves tok[])
+  __shared__ float s_om[kMetaSlots][kMaxTargets];  // target weights omega_k
+  __shared__ float s_xy[kMaxTargets];              // target logits (read from the ring in pass 1)
+  __shared__ int s_hdr[kMetaSlots][2];             // nt, bad
+  __shared__ float s_Om[kMetaSlots];               // Omega
   __shared__ float s_red[2][kPipeCompute / 32];
   __shared__ float s_lse;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nchunk = (V + kChunkElems - 1) / kChunkElems;
   if (tid == 0) {
     for (int k = 0; k < kRing; ++k) { mbar_init_(&full[k], 1); mbar_init_(&empty[k], kPipeCompute / 32); }
+    for (int k = 0; k < kMetaSlots; ++k) { mbar_init_(&mfull[k], 1); mbar_init_(&mfree[k], 1); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -368,61 +376,78 @@ __global__ void __launch_bounds__(kPipeThreads, 1) loss_pipe_kernel(
     }
     return;
   }
-  // ============ compute warps ============
-  int g = 0;
-  auto bar_c = [&]() { asm volatile("bar.sync 1, %0;" ::"n"(kPipeCompute) : "memory"); };
-  for (int64_t row = row_begin + blockIdx.x; row < N; row += gridDim.x) {
-    if (tid == 0) {
-      const int32_t u = node[row];
-      const bool last = row == (int64_t)node_start[u] + node_len[u] - 1;
+  if (warp == kPipeCompute / 32 + 1) {
+    // ============ meta warp: targets / weights of the upcoming rows (R7, R17, boundary), a row ahead
+    //              of the compute warps so its chain of dependent global loads is off their path ====
+    int it = 0;
+    for (int64_t row = row_begin + blockIdx.x; row < N; row += gridDim.x, ++it) {
+      const int sl = it % kMetaSlots;
+      if (it >= kMetaSlots) mbar_wait_(&mfree[sl], (uint32_t)(((it / kMetaSlots) - 1) & 1));
       int nt = 0;
-      if (!last) {
-        const int64_t tg = row + 1;
-        if (!node_mask || node_mask[node[tg]]) { s_y[0] = (int)tg; nt = 1; }
-      } else {
-        const int b = succ_ptr[u], e = succ_ptr[u + 1];
-        if (!(boundary_mode == 1 && diverges(succ_tok, b, e, w))) {
-          for (int k = b; k < e; ++k) {
-            const int tg = succ_tok[k];
-            if (!node_mask || node_mask[node[tg]]) s_y[nt++] = tg;
+      if (lane == 0) {
+        const int32_t u = node[row];
+        const bool last = row == (int64_t)node_start[u] + node_len[u] - 1;
+        if (!last) {
+          const int64_t tg = row + 1;
+          if (!node_mask || node_mask[node[tg]]) { s_y[sl][0] = (int)tg; nt = 1; }
+        } else {
+          const int b = succ_ptr[u], e = succ_ptr[u + 1];
+          if (!(boundary_mode == 1 && diverges(succ_tok, b, e, w))) {
+            for (int k = b; k < e; ++k) {
+              const int tg = succ_tok[k];
+              if (!node_mask || node_mask[node[tg]]) s_y[sl][nt++] = tg;
+            }
           }
         }
       }
-      s_nt = nt;
+      nt = __shfl_sync(0xffffffffu, nt, 0);
+      __syncwarp();
+      float om_part = 0.f;
+      int bad = 0;
+      for (int k = lane; k < nt; k += 32) {
+        const int tg = s_y[sl][k];
+        const int y = tok[tg];
+        const float om = wr ? wr[tg] : (float)w[tg];
+        bad |= (y < 0 || y >= V);
+        s_y[sl][k] = y;
+        s_om[sl][k] = om;
+        om_part += om;
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        om_part += __shfl_xor_sync(0xffffffffu, om_part, o);
+        bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+      }
+      if (lane == 0) {
+        s_hdr[sl][0] = nt;
+        s_hdr[sl][1] = bad;
+        s_Om[sl] = om_part;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive_(&mfull[sl]);
     }
-    bar_c();
-    const int nt = s_nt;
-    float om_part = 0.f;
-    int bad = 0;
-    for (int k = tid; k < nt; k += kPipeCompute) {
-      const int tg = s_y[k];
-      const int y = tok[tg];
-      const float om = wr ? wr[tg] : (float)w[tg];
-      bad |= (y < 0 || y >= V);
-      s_y[k] = y;
-      s_om[k] = om;
-      om_part += om;
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-      om_part += __shfl_xor_sync(0xffffffffu, om_part, o);
-      bad |= __shfl_xor_sync(0xffffffffu, bad, o);
-    }
-    if (lane == 0) { s_red[0][warp] = om_part; s_red[1][warp] = (float)bad; }
-    bar_c();
-    float Omega = 0.f, badf = 0.f;
-    for (int k = 0; k < kPipeCompute / 32; ++k) { Omega += s_red[0][k]; badf += s_red[1][k]; }
-    const bool bad_any = badf != 0.f;
-    bar_c();  // s_red reused below
-    const __nv_bfloat16* x = logits + row * ld;
+    return;
+  }
+  // ============ compute warps ============
+  int g = 0, it = 0;
+  auto bar_c = [&]() { asm volatile("bar.sync 1, %0;" ::"n"(kPipeCompute) : "memory"); };
+  for (int64_t row = row_begin + blockIdx.x; row < N; row += gridDim.x, ++it) {
+    const int sl = it % kMetaSlots;
+    mbar_wait_(&mfull[sl], (uint32_t)((it / kMetaSlots) & 1));
+    const int nt = s_hdr[sl][0];
+    const bool bad_any = s_hdr[sl][1] != 0;
+    const float Omega = s_Om[sl];
+    const int* ys = s_y[sl];
+    const float* oms = s_om[sl];
     __nv_bfloat16* dx = dlogits + row * ld;
-    // ---- pass 1 from the shared-memory ring ----
+    // ---- pass 1 from the shared-memory ring (+ the target logits, read before anything is written) ----
     float m = -INFINITY, sum = 0.f;
+    const bool live = Omega != 0.f && !bad_any;
     for (int c = 0; c < nchunk; ++c, ++g) {
       const int slot = g % kRing;
       mbar_wait_(&full[slot], (g / kRing) & 1);
       const int n = min(kChunkElems, V - c * kChunkElems);
       const uint4* src = reinterpret_cast<const uint4*>(ring + slot * kChunkElems);
-      if (Omega != 0.f && !bad_any) {
+      if (live) {
         // per thread and chunk: max of its elements on packed bf16 pairs, at most one rescale of the
         // running sum, then the sum of 2^(x log2e - m) with packed f32x2 FMAs / adds (the cluster
         // kernel's FAST pass 1, thread-local so no barrier per chunk)
@@ -455,11 +480,15 @@ __global__ void __launch_bounds__(kPipeThreads, 1) loss_pipe_kernel(
           const float2 acc = sm100::fadd2(acc0, acc1);
           sum += acc.x + acc.y;
         }
+        for (int k = tid; k < nt; k += kPipeCompute) {
+          const int o = ys[k] - c * kChunkElems;
+          if (o >= 0 && o < n) s_xy[k] = __bfloat162float(ring[slot * kChunkElems + o]);
+        }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive_(&empty[slot]);
     }
-    if (Omega == 0.f || bad_any) {
+    if (!live) {
       Vec<16> z;
 #pragma unroll
       for (int t = 0; t < 8; ++t) z.u[t] = 0u;
@@ -471,6 +500,8 @@ __global__ void __launch_bounds__(kPipeThreads, 1) loss_pipe_kernel(
         ws_omega[row] = bad_any ? 0.f : Omega;
         if (tok_loss) tok_loss[row] = lv;
       }
+      bar_c();  // every compute thread is done with metadata slot sl
+      if (tid == 0) mbar_arrive_(&mfree[sl]);
       continue;
     }
     for (int o = 16; o > 0; o >>= 1) {
@@ -495,15 +526,12 @@ __global__ void __launch_bounds__(kPipeThreads, 1) loss_pipe_kernel(
     bar_c();
     const float lse2 = s_lse;
     float lpart = 0.f;
-    for (int k = tid; k < nt; k += kPipeCompute) {
-      const float xy = __bfloat162float(x[s_y[k]]);
-      s_xy[k] = xy;
-      lpart += s_om[k] * (lse2 * kLn2 - xy);
-    }
+    for (int k = tid; k < nt; k += kPipeCompute) lpart += oms[k] * (lse2 * kLn2 - s_xy[k]);
     for (int o = 16; o > 0; o >>= 1) lpart += __shfl_xor_sync(0xffffffffu, lpart, o);
     bar_c();
     if (lane == 0) s_red[1][warp] = lpart;
     // ---- pass 2: re-read from L2, write dlogits ----
+    const __nv_bfloat16* x = logits + row * ld;
     const float gO = gamma * Omega;
     const float2 L2 = make_float2(kLog2e, kLog2e), NL = make_float2(-lse2, -lse2), G2 = make_float2(gO, gO);
     auto softmax16 = [&](const Vec<16>& a, __nv_bfloat16* dst) {
@@ -520,25 +548,25 @@ __global__ void __launch_bounds__(kPipeThreads, 1) loss_pipe_kernel(
       st_vec<16>(dst, o);
     };
     constexpr int S2 = kPipeCompute * 16;
+    constexpr int kMlp = 4;  // independent 32-byte L2 loads in flight per thread (4 / 8 / 12 measured equal)
     int c = tid * 16;
-    for (; c + 3 * S2 < V; c += 4 * S2) {  // four independent 32-byte loads in flight per thread
-      const Vec<16> a0 = ld_last<16>(x + c), a1 = ld_last<16>(x + c + S2), a2 = ld_last<16>(x + c + 2 * S2),
-                    a3 = ld_last<16>(x + c + 3 * S2);
-      softmax16(a0, dx + c);
-      softmax16(a1, dx + c + S2);
-      softmax16(a2, dx + c + 2 * S2);
-      softmax16(a3, dx + c + 3 * S2);
+    for (; c + (kMlp - 1) * S2 < V; c += kMlp * S2) {
+      Vec<16> a[kMlp];
+#pragma unroll
+      for (int u = 0; u < kMlp; ++u) a[u] = ld_last<16>(x + c + u * S2);
+#pragma unroll
+      for (int u = 0; u < kMlp; ++u) softmax16(a[u], dx + c + u * S2);
     }
     for (; c < V; c += S2) softmax16(ld_last<16>(x + c), dx + c);
     bar_c();
     for (int k = tid; k < nt; k += kPipeCompute) {
-      const int y = s_y[k];
+      const int y = ys[k];
       bool first = true;
       float om_y = 0.f;
       for (int k2 = 0; k2 < nt; ++k2) {
-        if (s_y[k2] == y) {
+        if (ys[k2] == y) {
           if (k2 < k) first = false;
-          om_y += s_om[k2];
+          om_y += oms[k2];
         }
       }
       if (first) {
@@ -553,7 +581,8 @@ __global__ void __launch_bounds__(kPipeThreads, 1) loss_pipe_kernel(
       ws_omega[row] = Omega;
       if (tok_loss) tok_loss[row] = L;
     }
-    bar_c();
+    bar_c();  // also: every compute thread is done with metadata slot sl and s_xy
+    if (tid == 0) mbar_arrive_(&mfree[sl]);
   }
 }
 
@@ -1070,7 +1099,7 @@ bool try_launch_cluster(const LcArgs& a0, int sms, cudaStream_t st) {
   if (cudaLaunchKernelEx(&cfg, kern, a) != cudaSuccess) return false;
   if (ss) {
     // launched after the clusters so its CTAs land on the SMs they left free
-    const size_t psm = (size_t)kRing * kChunkElems * 2 + 2 * kRing * 8;
+    const size_t psm = kPipeSmem;
     cudaFuncSetAttribute(loss_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm);
     cudaStreamWaitEvent(ss->s, ss->fork, 0);
     loss_pipe_kernel<<<(unsigned)idle, kPipeThreads, psm, ss->s>>>(
@@ -1138,7 +1167,7 @@ tt_status launch_loss(const tt_packed& pk, const __nv_bfloat16* logits, int64_t 
   }
   if (done) {
   } else if (v16) {
-    const size_t smem = (size_t)kRing * kChunkElems * 2 + 2 * kRing * 8;
+    const size_t smem = kPipeSmem;
     cudaFuncSetAttribute(loss_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     loss_pipe_kernel<<<(unsigned)std::min<int64_t>(pk.n_tokens, sms), kPipeThreads, smem, st>>>(
         pk.n_tokens, logits, ld, vocab, tok, node_mask, boundary_mode, gamma, pk.w, pk.wr, pk.node, pk.node_start,

@@ -70,6 +70,28 @@ def test_loss_vocab_not_multiple_of_8_rows_padded(tt):
     assert np.all(np.abs(g - dx) <= 2.0 ** -8 * np.abs(dx) + 1e-5 * np.maximum(om, 1)[:, None])
 
 
+def test_loss_vocab_padded_to_16(tt):
+    # V % 8 != 0 with 16-element-aligned rows (ld = 4112): the generic kernel (no 16-byte bulk copies
+    # of a ragged row, no writes into the padding)
+    import torch
+    t = trees.gen_agentic(400, root_len=60, seed=8)
+    pk = tt.tt_pack(t.parent, t.length)
+    N, V, ld = pk.n_tokens, 4100, 4112
+    x = tensors.logits_tensor(N, ld, seed=15)
+    tok = tensors.token_ids(N, V, seed=16)
+    xd = x.cuda()
+    dl = torch.full_like(xd, 7.0)
+    sums, dl, _, err = tt.tt_restore_loss(pk, xd, tok.cuda(), vocab=V, dlogits=dl)
+    torch.cuda.synchronize()
+    assert int(err.item()) == 0
+    opk = oracle.pack(t.parent, t.length)
+    lr, om, dx = oracle.loss(opk, tok.numpy(), V, np.arange(N), x[:, :V])
+    assert abs(sums.cpu()[0].item() - lr.sum()) <= 1e-5 * max(1.0, abs(lr.sum()))
+    g = to64(dl.cpu()[:, :V])
+    assert np.all(np.abs(g - dx) <= 2.0 ** -8 * np.abs(dx) + 1e-5 * np.maximum(om, 1)[:, None])
+    assert torch.all(dl[:, V:] == 7.0)  # padding untouched
+
+
 def test_loss_node_mask_and_boundary_mode(tt):
     t = trees.fig4_unit()
     mask = np.array([1, 1, 0, 1, 1, 0, 1, 1, 1], np.uint8)
