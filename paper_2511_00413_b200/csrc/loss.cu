@@ -347,8 +347,8 @@ __global__ void __launch_bounds__(kPipeThreads, 1) loss_pipe_kernel(
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nchunk = (V + kChunkElems - 1) / kChunkElems;
   if (tid == 0) {
-    for (int k = 0; k < kRing; ++k) { mbar_init_(&full[k], 1); mbar_init_(&empty[k], kPipeCompute / 32); }
-    for (int k = 0; k < kMetaSlots; ++k) { mbar_init_(&mfull[k], 1); mbar_init_(&mfree[k], 1); }
+    for (int k = 0; k < kRing; ++k) { mbar_init_(&full[k], 1); mbar_init_(&empty[k], kPipeCompute); }
+    for (int k = 0; k < kMetaSlots; ++k) { mbar_init_(&mfull[k], 32); mbar_init_(&mfree[k], 1); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -422,8 +422,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) loss_pipe_kernel(
         s_hdr[sl][1] = bad;
         s_Om[sl] = om_part;
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive_(&mfull[sl]);
+      mbar_arrive_(&mfull[sl]);  // every lane, after its own writes of this slot
     }
     return;
   }
@@ -485,8 +484,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) loss_pipe_kernel(
           if (o >= 0 && o < n) s_xy[k] = __bfloat162float(ring[slot * kChunkElems + o]);
         }
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive_(&empty[slot]);
+      mbar_arrive_(&empty[slot]);  // every compute thread: its reads of this slot are done
     }
     if (!live) {
       Vec<16> z;
