@@ -31,7 +31,9 @@
  *     thread-local message is available from tt_last_error().
  *   - Memory: the CALLER owns every buffer.  The library never allocates device memory, never
  *     frees, never synchronises a stream, and keeps no global state except the thread-local
- *     error string and a cached per-device attribute query.
+ *     error string, a cached per-device attribute query, and lazily created per-thread,
+ *     per-device handles: a cuBLASLt handle (tt_lmhead_loss) and one side stream + two events
+ *     (tt_restore_loss; never created while `stream` is capturing).
  *   - Host vs device: pointers documented as HOST are read synchronously during the call;
  *     all others are DEVICE pointers and are accessed asynchronously on `stream`.
  *   - Layout "thd": Q/O/dO/dQ are [N, Hq, d], K/V/dK/dV are [N, Hkv, d], contiguous, row major,
@@ -225,6 +227,11 @@ tt_status tt_attn_bwd(const tt_packed* pk, const void* q, const void* k, const v
  * (sum_t loss_t, sum_t Omega_t), reduced in a fixed order (bitwise reproducible).
  * d_err (device int32, nullable) is set to 1 if a target token id is outside [0, vocab); that
  * row's loss is NaN.  ws: >= tt_restore_loss_workspace() bytes.
+ * Execution: when vocab % 16 == 0, rows are 32-byte aligned and N >= 8 rows per SM, the call forks
+ * a library-owned side stream from `stream` (event record + wait) for the tail rows, which run on
+ * the SMs the 4-CTA clusters leave idle, and joins it back into `stream` before the final sum:
+ * the call stays stream-ordered on `stream` and may be captured into a CUDA graph.
+ * Row results do not depend on which kernel computed a row beyond fp32 rounding order.
  * -------------------------------------------------------------------------------------- */
 size_t tt_restore_loss_workspace(const tt_packed* pk);
 tt_status tt_restore_loss(const tt_packed* pk, const void* logits, int64_t ld, int32_t vocab, const int32_t* tok,
