@@ -2,7 +2,7 @@ import torch, sys
 sys.path.insert(0, '/root/repo')
 import paper_2511_00413_b200 as tt
 from workloads import trees
-for cfg, seed in [("agentic8k", 0), ("wide", None)]:
+for cfg, seed in [(c, 0 if c != "wide" else None) for c in (sys.argv[1:] or ["agentic8k", "wide"])]:
     t = trees.config_tree(cfg, seed); pk = tt.tt_pack(t.parent, t.length); N = pk.n_tokens; V = 151936
     g = torch.Generator(device="cuda").manual_seed(0)
     x = torch.empty(N, V, device="cuda", dtype=torch.bfloat16)
