@@ -82,11 +82,13 @@ def test_unit_weights_equal_integer_restore(tt):
 
 
 @pytest.mark.parametrize("kind", ["advantage", "positive"])
-def test_weighted_loss(tt, kind):
+@pytest.mark.parametrize("size,V", [(600, 1000), (2400, 4096)], ids=["clusters", "clusters_plus_tail"])
+def test_weighted_loss(tt, kind, size, V):
+    """(2400, 4096): >= 8 rows per SM and V % 16 == 0, so the tail rows run in loss_pipe_kernel."""
     import torch
-    t = trees.gen_agentic(600, root_len=100, seed=3)
+    t = trees.gen_agentic(size, root_len=100, seed=3)
     pk = tt.tt_pack(t.parent, t.length)
-    N, V = pk.n_tokens, 1000
+    N = pk.n_tokens
     alpha = _alpha(pk.info["n_traj"], 5, kind)
     tt.tt_pack_weights(pk, alpha)
     x = tensors.logits_tensor(N, V, seed=4)
