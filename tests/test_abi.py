@@ -83,3 +83,14 @@ def test_deep_chain_plan(tt):
     info = tt.tt_pack_plan(t.parent, t.length)
     assert info["n_tokens"] == 10000
     assert info["n_pairs"] == 10000 * 10001 // 2
+
+
+def test_missing_library_fails_loudly(monkeypatch):
+    """No fallback: with libtt.so absent every entry point raises instead of computing elsewhere."""
+    from paper_2511_00413_b200 import binding
+    monkeypatch.setattr(binding, "_SO", "/nonexistent/libtt.so")
+    monkeypatch.setattr(binding, "_lib", None)
+    with pytest.raises(ImportError):
+        binding.lib()
+    with pytest.raises(ImportError):
+        binding.tt_pack_plan([-1, 0], [3, 2])
