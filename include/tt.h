@@ -32,8 +32,9 @@
  *   - Memory: the CALLER owns every buffer.  The library never allocates device memory, never
  *     frees, never synchronises a stream, and keeps no global state except the thread-local
  *     error string, a cached per-device attribute query, and lazily created per-thread,
- *     per-device handles: a cuBLASLt handle (tt_lmhead_loss) and one side stream + two events
- *     (tt_restore_loss; never created while `stream` is capturing).
+ *     per-device handles: a cuBLASLt handle (tt_lmhead_loss), one side stream + two events
+ *     (tt_restore_loss; never created while `stream` is capturing) and a ring of 4 pinned host
+ *     staging buffers + events (tt_pack / tt_pack_weights; released at thread exit).
  *   - Host vs device: pointers documented as HOST are read synchronously during the call;
  *     all others are DEVICE pointers and are accessed asynchronously on `stream`.
  *   - Layout "thd": Q/O/dO/dQ are [N, Hq, d], K/V/dK/dV are [N, Hkv, d], contiguous, row major,
@@ -77,6 +78,12 @@ const char* tt_status_string(tt_status s);
 const char* tt_last_error(void);
 /* ABI version (major * 100 + minor). */
 int32_t tt_version(void);
+/* Build flags of the loaded library: bit 0 (TT_BUILD_DEV) set only in a development build
+ * (-DTT_DEV, `python -m paper_2511_00413_b200.build --dev`), whose kernels read A/B switches from
+ * environment variables (ablations that skip work).  The shipped build returns 0 and ignores every
+ * such variable; bench.py refuses to time a development build. */
+#define TT_BUILD_DEV 1
+int32_t tt_build_flags(void);
 
 /* --------------------------------------------------------------------------------------
  * Tree Packing ("merge trajectories into a tree"; Eq. 13 P:395-400 "X_ours =
@@ -152,7 +159,11 @@ tt_status tt_pack_plan(const int32_t* parent, const int32_t* len, const int32_t*
 
 /* Pack: host validation + O(n) node DFS, one async H2D copy of the node tables, then device
  * kernels that fill the per-token arrays and the tile metadata into d_ws (ws_bytes >=
- * info.ws_bytes).  `out` receives device pointers into d_ws.  `info` may be NULL. */
+ * info.ws_bytes).  `out` receives device pointers into d_ws.  `info` may be NULL.
+ * The node tables are staged through a per-thread ring of 4 pinned host buffers (the copy never
+ * synchronises the stream; a slot is reused once its previous copy has completed, so the host may
+ * wait for a pack issued 4 calls earlier).  Not capturable: a capturing `stream` returns
+ * TT_ERR_INVALID_ARGUMENT (pack outside the capture and capture the fwd / loss / bwd calls). */
 tt_status tt_pack(const int32_t* parent, const int32_t* len, const int32_t* term, int32_t n_nodes,
                   void* d_ws, size_t ws_bytes, tt_packed* out, tt_pack_info* info, tt_stream_t stream);
 
@@ -171,7 +182,7 @@ tt_status tt_pack(const int32_t* parent, const int32_t* len, const int32_t* term
  * parent/len/term/n_nodes: exactly the forest pk was packed from (checked: n_nodes, N).
  * wr: DEVICE [n_blk * 128] fp32, 16-byte aligned, caller-owned; W per token (fp64 subtree sums
  *   rounded once to fp32), 0 in the padding.  On success pk->wr = wr.  Host work O(n + N), one
- *   async H2D copy on `stream` (the host image is staged before return).
+ *   async H2D copy on `stream` through the same pinned staging ring as tt_pack (not capturable).
  * -------------------------------------------------------------------------------------- */
 tt_status tt_pack_weights(const int32_t* parent, const int32_t* len, const int32_t* term, int32_t n_nodes,
                           const float* traj_weight, tt_packed* pk, float* wr, tt_stream_t stream);

@@ -357,6 +357,99 @@ int oracle_attn_bwd(int64_t N, int32_t hq, int32_t hkv, int32_t d, double scale,
   const int g = hq / hkv;
   const bool filt = want_q || want_k;
   std::vector<std::vector<double>> dk_h(hq), dv_h(hq);
+  if (filt) {
+    // Sampled mode: only the wanted outputs, each by the same arithmetic and in the same summation
+    // order as the full mode below (bq[p] over keys j ascending; bk[j] / bv[j] over rows p
+    // ascending within a branch; branches in trajectory order), so a wanted value is bitwise the
+    // full mode's.  The work is split over rows (forward rows, dq rows) or keys (dk/dv), never
+    // over the terms of one sum, so the result does not depend on the thread count.
+    for (int64_t i = 0; i < N * hq * d; ++i) dq[i] = 0.0;
+    std::vector<const double*> kr, vr;
+    std::vector<double> O, LSE, Dv, bq, bk, bv;
+    std::vector<int64_t> rows_q, keys;
+    for (int h = 0; h < hq; ++h) {
+      const int hk = h / g;
+      dk_h[h].assign((size_t)N * d, 0.0);
+      dv_h[h].assign((size_t)N * d, 0.0);
+      for (int64_t t = 0; t < n_traj; ++t) {
+        const int32_t* idx = path_idx + path_ptr[t];
+        const int64_t L = path_ptr[t + 1] - path_ptr[t];
+        if (L == 0) continue;
+        int64_t p_min = L;
+        if (want_k) {
+          for (int64_t p = 0; p < L; ++p) if (want_k[idx[p]]) { p_min = p; break; }
+        }
+        rows_q.clear(); keys.clear();
+        std::vector<char> need(L, 0);
+        for (int64_t p = 0; p < L; ++p) {
+          const bool wq = want_q && want_q[idx[p]];
+          need[p] = wq || p >= p_min;
+          if (wq) rows_q.push_back(p);
+          if (want_k && want_k[idx[p]]) keys.push_back(p);
+        }
+        kr.resize(L); vr.resize(L);
+        for (int64_t p = 0; p < L; ++p) {
+          kr[p] = k + ((int64_t)idx[p] * hkv + hk) * d;
+          vr[p] = v + ((int64_t)idx[p] * hkv + hk) * d;
+        }
+        O.assign((size_t)L * d, 0.0); LSE.assign(L, 0.0); Dv.assign(L, 0.0);
+        bq.assign((size_t)L * d, 0.0); bk.assign((size_t)L * d, 0.0); bv.assign((size_t)L * d, 0.0);
+        // forward rows + D_p (same arithmetic as the full mode)
+        run_threads((int)L, nthreads, [&](int p) {
+          if (!need[p]) return;
+          std::vector<double> s;
+          const double* gp = gup + ((int64_t)idx[p] * hq + h) * d;
+          attn_row(q + ((int64_t)idx[p] * hq + h) * d, kr.data(), vr.data(), p + 1, d, scale, s, &O[(size_t)p * d],
+                   &LSE[p]);
+          double D = 0.0;
+          for (int c = 0; c < d; ++c) D += gp[c] * O[(size_t)p * d + c];
+          Dv[p] = D;
+        });
+        // dq of the wanted rows: sum over keys j <= p ascending
+        run_threads((int)rows_q.size(), nthreads, [&](int r) {
+          const int64_t p = rows_q[r];
+          const double* qp = q + ((int64_t)idx[p] * hq + h) * d;
+          const double* gp = gup + ((int64_t)idx[p] * hq + h) * d;
+          for (int64_t j = 0; j <= p; ++j) {
+            double acc = 0.0;
+            for (int c = 0; c < d; ++c) acc += qp[c] * kr[j][c];
+            double P = std::exp(scale * acc - LSE[p]);
+            double dP = 0.0;
+            for (int c = 0; c < d; ++c) dP += gp[c] * vr[j][c];
+            double dS = P * (dP - Dv[p]);
+            for (int c = 0; c < d; ++c) bq[p * d + c] += scale * dS * kr[j][c];
+          }
+        });
+        // dk / dv of the wanted keys: sum over rows p >= j ascending
+        run_threads((int)keys.size(), nthreads, [&](int r) {
+          const int64_t j = keys[r];
+          for (int64_t p = j; p < L; ++p) {
+            const double* qp = q + ((int64_t)idx[p] * hq + h) * d;
+            const double* gp = gup + ((int64_t)idx[p] * hq + h) * d;
+            double acc = 0.0;
+            for (int c = 0; c < d; ++c) acc += qp[c] * kr[j][c];
+            double P = std::exp(scale * acc - LSE[p]);
+            double dP = 0.0;
+            for (int c = 0; c < d; ++c) dP += gp[c] * vr[j][c];
+            double dS = P * (dP - Dv[p]);
+            for (int c = 0; c < d; ++c) {
+              bk[j * d + c] += scale * dS * qp[c];
+              bv[j * d + c] += P * gp[c];
+            }
+          }
+        });
+        const double a = traj_weight ? traj_weight[t] : 1.0;
+        for (int64_t p = 0; p < L; ++p) {
+          const int64_t i = idx[p];
+          for (int c = 0; c < d; ++c) {
+            dq[(i * hq + h) * d + c] += a * bq[p * d + c];
+            dk_h[h][i * d + c] += a * bk[p * d + c];
+            dv_h[h][i * d + c] += a * bv[p * d + c];
+          }
+        }
+      }
+    }
+  } else
   run_threads(hq, nthreads, [&](int h) {
     const int hk = h / g;
     dk_h[h].assign((size_t)N * d, 0.0);

@@ -74,6 +74,8 @@ def lib():
             L.tt_last_error.restype = C.c_char_p
             L.tt_last_error.argtypes = []
             L.tt_version.restype = C.c_int32
+            L.tt_build_flags.restype = C.c_int32
+            L.tt_build_flags.argtypes = []
             L.tt_pack_plan.argtypes = [i32p, i32p, i32p, C.c_int32, C.POINTER(TTPackInfo)]
             L.tt_pack.argtypes = [i32p, i32p, i32p, C.c_int32, vp, sz, C.POINTER(TTPacked), C.POINTER(TTPackInfo), st]
             L.tt_attn_fwd.argtypes = [C.POINTER(TTPacked), vp, vp, vp, C.c_int, C.c_int32, C.c_int32, C.c_int32,
@@ -151,11 +153,27 @@ def _p(t):
     return None if t is None else C.c_void_p(t.data_ptr())
 
 
-def _need(t, dtype, name):
-    """Checks a caller-supplied output's dtype (the C ABI takes typed pointers: a mismatched torch
-    dtype would be silently reinterpreted)."""
-    if t is not None and t.dtype != dtype:
+def _need(t, dtype, name, device=None, contiguous=False):
+    """Checks a caller-supplied tensor's dtype (the C ABI takes typed pointers: a mismatched torch
+    dtype would be silently reinterpreted), and optionally its device and contiguity."""
+    if t is None:
+        return
+    if t.dtype != dtype:
         raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if device is not None and t.device != device:
+        raise ValueError(f"{name} must be on {device}, got {t.device}")
+    if contiguous and not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+
+
+def _ws_stream(stream):
+    """Context for allocating temporaries: on the stream the kernels run on, so the caching allocator
+    never hands a still-in-use workspace to another stream (explicit stream= callers)."""
+    import contextlib
+    import torch
+    if stream is None or not hasattr(stream, "cuda_stream"):
+        return contextlib.nullcontext()
+    return torch.cuda.stream(stream)
 
 
 def tt_launch_count() -> int:
@@ -292,13 +310,22 @@ def tt_attn_bwd(pk: PackedTree, q, k, v, o, lse, dout, restore=True, softmax_sca
     import torch
     N, hq, d = q.shape
     hkv = k.shape[1]
-    dq = torch.empty_like(q) if dq is None else dq
-    dk = torch.empty_like(k) if dk is None else dk
-    dv = torch.empty_like(v) if dv is None else dv
-    need = tt_attn_bwd_workspace(pk, hq, hkv, d, q.dtype)
-    if ws is None or ws.numel() < need:
-        ws = torch.empty(need, dtype=torch.uint8, device=q.device)
-    _need(sqnorm, torch.float64, "sqnorm")
+    with _ws_stream(stream):
+        dq = torch.empty_like(q) if dq is None else dq
+        dk = torch.empty_like(k) if dk is None else dk
+        dv = torch.empty_like(v) if dv is None else dv
+        need = tt_attn_bwd_workspace(pk, hq, hkv, d, q.dtype)
+        if ws is None or ws.numel() < need:
+            ws = torch.empty(need, dtype=torch.uint8, device=q.device)
+    for name, t in (("k", k), ("v", v), ("o", o), ("dout", dout), ("dq", dq), ("dk", dk), ("dv", dv)):
+        _need(t, q.dtype, name, q.device, contiguous=True)
+    _need(q, q.dtype, "q", q.device, contiguous=True)
+    _need(lse, torch.float32, "lse", q.device, contiguous=True)
+    if tuple(o.shape) != tuple(q.shape) or tuple(dout.shape) != tuple(q.shape) or tuple(dq.shape) != tuple(q.shape):
+        raise ValueError("o, dout, dq must have q's shape [N, hq, d]")
+    if tuple(v.shape) != tuple(k.shape) or tuple(dk.shape) != tuple(k.shape) or tuple(dv.shape) != tuple(k.shape):
+        raise ValueError("v, dk, dv must have k's shape [N, hkv, d]")
+    _need(sqnorm, torch.float64, "sqnorm", q.device)
     _check("tt_attn_bwd", lib().tt_attn_bwd(C.byref(pk.c), _p(q), _p(k), _p(v), _p(o), _p(lse), _p(dout),
                                             int(bool(restore)), _dt(q), hq, hkv, d, _scale(softmax_scale, d),
                                             _p(dq), _p(dk), _p(dv), _p(sqnorm), _p(ws), int(ws.numel()),
@@ -311,21 +338,37 @@ def tt_restore_loss(pk: PackedTree, logits, tok, grad_scale=1.0, node_loss_mask=
     """Returns (sums [2] fp64 device: (sum loss, sum Omega), dlogits, tok_loss, d_err).
     Pass dlogits=logits for the in-place (aliasing) form."""
     import torch
-    N, ld = logits.shape
-    vocab = ld if vocab is None else int(vocab)
-    dlogits = torch.empty_like(logits) if dlogits is None else dlogits
-    sums = torch.zeros(2, dtype=torch.float64, device=logits.device) if sums is None else sums
-    d_err = torch.zeros(1, dtype=torch.int32, device=logits.device) if d_err is None else d_err
-    L = lib()
-    need = int(L.tt_restore_loss_workspace(C.byref(pk.c)))
-    if ws is None or ws.numel() < need:
-        ws = torch.empty(need, dtype=torch.uint8, device=logits.device)
-    if node_loss_mask is not None and not isinstance(node_loss_mask, torch.Tensor):
-        node_loss_mask = torch.as_tensor(np.asarray(node_loss_mask, dtype=np.uint8), device=logits.device)
-    _need(tok_loss, torch.float32, "tok_loss")
-    _need(sums, torch.float64, "sums")
-    _need(d_err, torch.int32, "d_err")
-    _need(tok, torch.int32, "tok")
+    if logits.dim() != 2 or logits.dtype != torch.bfloat16 or logits.stride(1) != 1:
+        raise ValueError("logits must be a bf16 [N, V] tensor with unit column stride")
+    N = logits.shape[0]
+    ld = logits.stride(0)  # row stride in elements (a column-sliced view keeps its parent's stride)
+    vocab = logits.shape[1] if vocab is None else int(vocab)
+    if vocab > logits.shape[1]:
+        raise ValueError(f"vocab {vocab} exceeds the logits width {logits.shape[1]}")
+    dev = logits.device
+    with _ws_stream(stream):
+        dlogits = torch.empty_like(logits) if dlogits is None else dlogits
+        sums = torch.zeros(2, dtype=torch.float64, device=dev) if sums is None else sums
+        d_err = torch.zeros(1, dtype=torch.int32, device=dev) if d_err is None else d_err
+        L = lib()
+        need = int(L.tt_restore_loss_workspace(C.byref(pk.c)))
+        if ws is None or ws.numel() < need:
+            ws = torch.empty(need, dtype=torch.uint8, device=dev)
+        if node_loss_mask is not None and not isinstance(node_loss_mask, torch.Tensor):
+            node_loss_mask = torch.as_tensor(np.asarray(node_loss_mask, dtype=np.uint8), device=dev)
+    if dlogits.dtype != torch.bfloat16 or tuple(dlogits.shape) != tuple(logits.shape) or dlogits.stride() != logits.stride():
+        raise ValueError("dlogits must be bf16 with logits' shape and strides (or logits itself, in place)")
+    if dlogits.device != dev:
+        raise ValueError("dlogits must be on logits' device")
+    if N != pk.n_tokens:
+        raise ValueError(f"logits has {N} rows, the pack {pk.n_tokens} tokens")
+    _need(tok, torch.int32, "tok", dev, contiguous=True)
+    if tok.numel() < N:
+        raise ValueError("tok must hold one token id per packed token")
+    _need(node_loss_mask, torch.uint8, "node_loss_mask", dev, contiguous=True)
+    _need(tok_loss, torch.float32, "tok_loss", dev, contiguous=True)
+    _need(sums, torch.float64, "sums", dev, contiguous=True)
+    _need(d_err, torch.int32, "d_err", dev)
     _check("tt_restore_loss", L.tt_restore_loss(C.byref(pk.c), _p(logits), int(ld), vocab, _p(tok),
                                                 _p(node_loss_mask), int(boundary_mode), float(grad_scale),
                                                 _p(dlogits), _p(tok_loss), _p(sums), _p(d_err), _p(ws),

@@ -26,10 +26,15 @@ SO = os.path.join(HERE, "libtt.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-Xptxas", "-warn-spills", "-I", os.path.join(ROOT, "include")]
+# Development builds (--dev, or TT_DEV=1 in the environment): -DTT_DEV compiles in the environment
+# A/B switches (ablations / variant sweeps, csrc/tt_internal.cuh dev_getenv) and, with
+# TT_PROFILE_COUNTERS, per-role cycle counters; TT_EXTRA_NVCC_FLAGS adds compile-time variants.  The
+# library reports it through tt_build_flags() and bench.py refuses to time it.
+DEV_FLAGS = ["-DTT_DEV"]
 if os.environ.get("TT_PROFILE_COUNTERS"):
-    FLAGS += ["-DTT_PROFILE_COUNTERS"]  # development cycle counters in the tensor-core kernels
+    DEV_FLAGS += ["-DTT_PROFILE_COUNTERS"]
 if os.environ.get("TT_EXTRA_NVCC_FLAGS"):
-    FLAGS += os.environ["TT_EXTRA_NVCC_FLAGS"].split()  # development A/B of compile-time variants
+    DEV_FLAGS += os.environ["TT_EXTRA_NVCC_FLAGS"].split()
 
 
 def nvcc() -> str:
@@ -44,8 +49,14 @@ def _deps_mtime(src: str) -> float:
     return max([os.path.getmtime(src)] + [os.path.getmtime(h) for h in hdrs])
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, dev: bool = False) -> str:
+    dev = dev or bool(os.environ.get("TT_DEV"))
+    flags = FLAGS + (DEV_FLAGS if dev else [])
     os.makedirs(OBJ, exist_ok=True)
+    stamp = os.path.join(OBJ, "flags.txt")
+    if not os.path.exists(stamp) or open(stamp).read() != " ".join(flags):
+        force = True  # release <-> dev switch: rebuild every object
+    
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     jobs = []
     for s in srcs:
@@ -55,7 +66,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     def comp(so):
         s, o = so
-        cmd = [nvcc()] + ARCH + FLAGS + ["-c", s, "-o", o]
+        cmd = [nvcc()] + ARCH + flags + ["-c", s, "-o", o]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {os.path.basename(s)}:\n{r.stderr}")
@@ -77,6 +88,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")
+    with open(stamp, "w") as f:
+        f.write(" ".join(flags))
     return SO
 
 
@@ -84,5 +97,6 @@ if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--force", action="store_true")
     ap.add_argument("-v", "--verbose", action="store_true")
+    ap.add_argument("--dev", action="store_true", help="development build (-DTT_DEV): env A/B switches compiled in")
     a = ap.parse_args()
-    print(build(force=a.force, verbose=a.verbose))
+    print(build(force=a.force, verbose=a.verbose, dev=a.dev))

@@ -1,4 +1,4 @@
-// attn_sm100.cu — placeholder dispatch for bf16 d=128 until the tcgen05 kernels land.
+// attn_sm100.cu — device capability check for the sm_100a tensor-core attention path (bf16, d = 128).
 #include "tt_internal.cuh"
 
 namespace tt {

@@ -217,7 +217,7 @@ __global__ void __maxnreg__(kNWG == 4 ? 80 : 128)  // 22 warps: 6 per SMSP x 80 
         const int q0 = (qt0 + it % nq) * kBQ;
         uint8_t* qd = smem + kOffQS + s * 2 * kQTile;
         uint8_t* st = smem + kOffStats + s * kStatBytes;
-        if ((p.dbg & 2) && it >= kQStages) {
+        if ((dev_dbg(p.dbg) & 2) && it >= kQStages) {
           mbar_arrive(&q_full[s]);
           continue;
         }
@@ -340,7 +340,7 @@ __global__ void __maxnreg__(kNWG == 4 ? 80 : 128)  // 22 warps: 6 per SMSP x 80 
         }
       }
       mma_commit_w(acc_done);
-      if ((p.dbg & 8) && lane == 0) {
+      if ((dev_dbg(p.dbg) & 8) && lane == 0) {
         atomicAdd(&g_bwd_dbg[0], (unsigned long long)(TT_CLK() - t_start));
         atomicAdd(&g_bwd_dbg[1], (unsigned long long)w_sm);
         atomicAdd(&g_bwd_dbg[2], (unsigned long long)w_dq);
@@ -388,8 +388,8 @@ __global__ void __maxnreg__(kNWG == 4 ? 80 : 128)  // 22 warps: 6 per SMSP x 80 
       tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(&dq_free[0]);
-      if (p.dbg & 1) continue;
-      if (p.dbg & 16) {
+      if (dev_dbg(p.dbg) & 1) continue;
+      if (dev_dbg(p.dbg) & 16) {
         // variant: coalesced fp32 REDs straight from registers (a warp instruction covers 32
         // consecutive head dims of one query row = 128 contiguous bytes); no shared-memory staging
         float* base = p.dq_acc + ((int64_t)q0 * p.hq + h) * kD + r;
@@ -424,7 +424,7 @@ __global__ void __maxnreg__(kNWG == 4 ? 80 : 128)  // 22 warps: 6 per SMSP x 80 
       c_dr += TT_CLK() - t_dr;
     }
     if (r == 0) bulk_wait<0>();
-    if ((p.dbg & 8) && r == 0) {
+    if ((dev_dbg(p.dbg) & 8) && r == 0) {
       atomicAdd(&g_bwd_dbg[7], (unsigned long long)c_dr);
       atomicAdd(&g_bwd_dbg[8], (unsigned long long)c_wd);
     }
@@ -451,7 +451,7 @@ __global__ void __maxnreg__(kNWG == 4 ? 80 : 128)  // 22 warps: 6 per SMSP x 80 
       { long long t0 = TT_CLK(); mbar_wait(&s_full[sb], kKT ? (it & 1) : ((it >> 1) & 1)); c_ws += TT_CLK() - t0; }
       tc_fence_after();
       long long t_el = TT_CLK();
-      if (p.dbg & 4) {
+      if (dev_dbg(p.dbg) & 4) {
         tc_fence_before();
         mbar_arrive(&p_ready[sb]);
         mbar_wait(dp_full, it & 1);
@@ -556,7 +556,7 @@ __global__ void __maxnreg__(kNWG == 4 ? 80 : 128)  // 22 warps: 6 per SMSP x 80 
       }
       c_el += TT_CLK() - t_el;
     }
-    if ((p.dbg & 8) && r == 0 && wg == 0) {
+    if ((dev_dbg(p.dbg) & 8) && r == 0 && wg == 0) {
       atomicAdd(&g_bwd_dbg[5], (unsigned long long)c_ws);
       atomicAdd(&g_bwd_dbg[6], (unsigned long long)c_el);
       atomicAdd(&g_bwd_dbg[9], (unsigned long long)c_ld);
@@ -622,7 +622,7 @@ __global__ void __maxnreg__(kNWG == 4 ? 80 : 128)  // 22 warps: 6 per SMSP x 80 
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
-  if ((p.dbg & 8) && threadIdx.x == 0) {
+  if ((dev_dbg(p.dbg) & 8) && threadIdx.x == 0) {
     atomicAdd(&g_bwd_dbg[12], (unsigned long long)(TT_CLK() - t_kernel0));
     atomicAdd(&g_bwd_dbg[13], 1ull);
   }
@@ -729,9 +729,9 @@ tt_status sm100_attn_bwd(const tt_packed& pk, const void* q, const void* k, cons
   prm.nb = pk.n_blk;
   prm.restore = restore ? 1 : 0;
   {
-    const char* e = getenv("TT_DEBUG_BWD");
+    const char* e = dev_getenv("TT_DEBUG_BWD");
     prm.dbg = e ? atoi(e) : 0;
-    const char* o = getenv("TT_CTA_ORDER");  // development A/B: bit 1 = bwd head-major
+    const char* o = dev_getenv("TT_CTA_ORDER");  // development A/B: bit 1 = bwd head-major
     prm.head_major = o ? ((atoi(o) >> 1) & 1) : 0;  // measured: head-major loses the global heavy-first order (8K -10%, wide -12%)
   }
   prm.scale = scale;

@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
                              : (int)(blockIdx.x % p.hq);
   const int hk = h / (p.hq / p.hkv);
   const int qa = 2 * pair;
-  const bool has1 = qa + 1 < p.nb && !(p.dbg & 16);  // dbg 16: development ablation, drop query tile 1
+  const bool has1 = qa + 1 < p.nb && !(dev_dbg(p.dbg) & 16);  // dbg 16: development ablation, drop query tile 1
   const int kb_end = has1 ? qa + 2 : qa + 1;
 
   // barriers first, so the producer can start the Q and first K/V loads before the tile-list merge
@@ -203,7 +203,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       mbar_wait(bar_q, 0);
       if (T > 0) {
         mbar_wait(&full[0], 0);
-        if ((p.dbg & 8) && lane == 0) atomicAdd(&g_fwd_dbg[8], (unsigned long long)(TT_CLK() - t_kernel0));
+        if ((dev_dbg(p.dbg) & 8) && lane == 0) atomicAdd(&g_fwd_dbg[8], (unsigned long long)(TT_CLK() - t_kernel0));
         tc_fence_after();
 #pragma unroll
         for (int i = 0; i < 2; ++i)
@@ -238,7 +238,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         }
         mma_commit_w(&empty[s]);
       }
-      if ((p.dbg & 8) && lane == 0) {
+      if ((dev_dbg(p.dbg) & 8) && lane == 0) {
         atomicAdd(&g_fwd_dbg[0], (unsigned long long)(TT_CLK() - t_beg));
         atomicAdd(&g_fwd_dbg[1], (unsigned long long)w_p);
         atomicAdd(&g_fwd_dbg[2], (unsigned long long)w_kv);
@@ -278,7 +278,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         const long long t_cmp = TT_CLK();
         sph ^= 1;
         tc_fence_after();
-        if (p.dbg & 32) {  // development ablation: no softmax work (MMA pipeline alone)
+        if (dev_dbg(p.dbg) & 32) {  // development ablation: no softmax work (MMA pipeline alone)
           tc_fence_before();
           mbar_arrive(&p_full[i]);
           continue;
@@ -290,7 +290,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         c_ldp += TT_CLK() - t_cmp;
         // ---- mask (partial tiles; key columns past N on the ragged last block) ----
         const bool ragged = j0 + 64 > p.N;
-        if (cls == kClsPartial && !(p.dbg & 64)) {  // dbg 64: development ablation, partial tiles unmasked
+        if (cls == kClsPartial && !(dev_dbg(p.dbg) & 64)) {  // dbg 64: development ablation, partial tiles unmasked
           // int32 index math (N < 2^31): key c allowed iff c <= row - j0, c < N - j0, row < E_c
           const int4* Es = reinterpret_cast<const int4*>(smem + kOffE + (t % kStages) * 512) + 16 * hf;
           const int cmax = min((int)(row - j0), (int)(p.N - j0) - 1);
@@ -334,7 +334,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         //      exponentials run as a polynomial on the FMA pipe (FA4-style) ----
         const float2 SL = make_float2(sl2, sl2), NM = make_float2(-mb, -mb);
         float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
-        if ((cls == kClsFull || (p.dbg & 64)) && !ragged) {
+        if ((cls == kClsFull || (dev_dbg(p.dbg) & 64)) && !ragged) {
 #pragma unroll
           for (int c = 0; c < 64; c += 4) {
             const float2 a01 = ffma2(make_float2(__uint_as_float(s[c]), __uint_as_float(s[c + 1])), SL, NM);
@@ -417,7 +417,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         }
       }
       if (hf == 0 && row < p.N) p.lse[(int64_t)h * p.N + row] = (m + __log2f(lt)) * kLn2;
-      if ((p.dbg & 8) && r == 0 && i == 0 && hf == 0) {
+      if ((dev_dbg(p.dbg) & 8) && r == 0 && i == 0 && hf == 0) {
         atomicAdd(&g_fwd_dbg[4], (unsigned long long)c_ws);
         atomicAdd(&g_fwd_dbg[5], (unsigned long long)c_cmp);
         atomicAdd(&g_fwd_dbg[6], (unsigned long long)c_n);
@@ -434,7 +434,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
-  if ((p.dbg & 8) && threadIdx.x == 0) {
+  if ((dev_dbg(p.dbg) & 8) && threadIdx.x == 0) {
     atomicAdd(&g_fwd_dbg[12], (unsigned long long)(TT_CLK() - t_kernel0));
     atomicAdd(&g_fwd_dbg[13], 1ull);
   }
@@ -502,9 +502,9 @@ tt_status sm100_attn_fwd(const tt_packed& pk, const void* q, const void* k, cons
   prm.npairs = (nb + 1) / 2;
   prm.scale_log2 = scale * kLog2e;
   {
-    const char* e = getenv("TT_DEBUG_FWD");
+    const char* e = dev_getenv("TT_DEBUG_FWD");
     prm.dbg = e ? atoi(e) : 0;
-    const char* o = getenv("TT_CTA_ORDER");  // development A/B: bit 0 = fwd head-major
+    const char* o = dev_getenv("TT_CTA_ORDER");  // development A/B: bit 0 = fwd head-major
     prm.head_major = o ? (atoi(o) & 1) : 0;
   }
   prm.E = pk.E;

@@ -640,7 +640,7 @@ struct LcArgs {
   __nv_bfloat16* dlogits;
   float *tok_loss, *ws_loss, *ws_omega;
   int32_t* d_err;
-  int nocompute;  // development ablation (TT_LOSS_NOCOMPUTE): stream the rows through without the math
+  int nocompute;  // development ablation (TT_DEV builds only) (TT_LOSS_NOCOMPUTE): stream the rows through without the math
 };
 
 __device__ __forceinline__ uint32_t lc_rank() { uint32_t r; asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r)); return r; }
@@ -822,7 +822,7 @@ __global__ void __launch_bounds__(kLcThreads, 1) loss_cluster_kernel(const LcArg
     const int xs_slot = it % kLcSlots;
     mbar_wait_(&mfull[b], (uint32_t)((it / NBUF) & 1));
     LcMeta M = lc_meta(meta_base, b, a.max_t);
-    if (a.nocompute) {
+    if (kDevBuild && a.nocompute) {
       mbar_wait_(&full[b], (uint32_t)((it / NBUF) & 1));
       bar_g();
       if (gt == 0) {
@@ -1047,16 +1047,23 @@ SideStream* side_stream(cudaStream_t st) {
   return &ss;
 }
 
+// Outcome of a cluster launch attempt: kNotLaunched leaves the stream untouched (the caller may try
+// another kernel); once the cluster kernel is enqueued the attempt is final (kLaunched / kFailed), so
+// a failure after that point is reported, never retried over rows that may already hold dlogits
+// (in-place mode).
+enum class LcLaunch { kNotLaunched, kLaunched, kFailed };
+
 template <int CS, int NBUF, int KPOLY = 1, int KP1 = 0, int FAST = 0, int NG = 2>
-bool try_launch_cluster(const LcArgs& a0, int sms, cudaStream_t st) {
+LcLaunch try_launch_cluster(const LcArgs& a0, int sms, cudaStream_t st) {
   LcArgs a = a0;
   a.Cq = ((a.V + CS - 1) / CS + 7) / 8 * 8;
   const size_t smem = lc_smem<CS, NBUF>(a.Cq, a.max_t);
-  if (smem + 1024 > 232448) return false;  // static shared memory + margin
+  if (smem + 1024 > 232448) return LcLaunch::kNotLaunched;  // static shared memory + margin
   auto kern = loss_cluster_kernel<CS, NBUF, KPOLY, KP1, FAST, NG>;
+  cudaGetLastError();  // a stale error of an earlier call must not be taken for this launch's
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
     cudaGetLastError();
-    return false;
+    return LcLaunch::kNotLaunched;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(CS * std::max(1, sms / CS)));
@@ -1073,42 +1080,63 @@ bool try_launch_cluster(const LcArgs& a0, int sms, cudaStream_t st) {
   int ncl = 0;
   if (cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg) != cudaSuccess || ncl <= 0) {
     cudaGetLastError();
-    return false;
+    return LcLaunch::kNotLaunched;
   }
   int64_t want = std::min<int64_t>((int64_t)ncl, a.N);
-  if (const char* mc = getenv("TT_LOSS_MAXCL")) want = std::min<int64_t>(want, std::max(1, atoi(mc)));  // dev: SM-count sweep
-  if (getenv("TT_LOSS_DEBUG")) fprintf(stderr, "loss_cluster<%d,%d>: %d active clusters, Cq %d, smem %zu\n", CS, NBUF, ncl, a.Cq, smem);
+  if (const char* mc = dev_getenv("TT_LOSS_MAXCL")) want = std::min<int64_t>(want, std::max(1, atoi(mc)));  // dev: SM-count sweep
+  if (dev_getenv("TT_LOSS_DEBUG")) fprintf(stderr, "loss_cluster<%d,%d>: %d active clusters, Cq %d, smem %zu\n", CS, NBUF, ncl, a.Cq, smem);
   cfg.gridDim = dim3((unsigned)(want * CS));
   // tail rows for the SMs the clusters leave idle (split by per-SM row rate, pipe / cluster ~ 0.7: profiles/r1k_loss_split.txt)
   const int idle = sms - (int)want * CS;
-  static const double ratio = [] {
-    const char* e = getenv("TT_LOSS_SPLIT");  // development A/B: 0 disables the split
-    return e ? atof(e) : 0.7;
-  }();
+  double ratio = 0.7;
+  if (const char* e = dev_getenv("TT_LOSS_SPLIT")) ratio = atof(e);  // development A/B: 0 disables the split
   int64_t n_pipe = 0;
   if (idle > 0 && ratio > 0 && a.N >= 8 * sms && (a.V % 16 == 0) && (a.ld % 16 == 0) &&
       ((reinterpret_cast<uintptr_t>(a.logits) | reinterpret_cast<uintptr_t>(a.dlogits)) % 32 == 0))
     n_pipe = (int64_t)((double)a.N * idle * ratio / ((double)want * CS + idle * ratio));
   SideStream* ss = n_pipe > 0 ? side_stream(st) : nullptr;
+  if (ss && cudaFuncSetAttribute(loss_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPipeSmem) != cudaSuccess) {
+    cudaGetLastError();
+    ss = nullptr;
+  }
   if (!ss) n_pipe = 0;
   const int64_t N = a.N;
   a.N = N - n_pipe;
-  if (ss && cudaEventRecord(ss->fork, st) != cudaSuccess) return false;
-  if (cudaLaunchKernelEx(&cfg, kern, a) != cudaSuccess) return false;
+  if (ss && cudaEventRecord(ss->fork, st) != cudaSuccess) {
+    cudaGetLastError();
+    ss = nullptr;
+    n_pipe = 0;
+    a.N = N;
+  }
+  if (cudaLaunchKernelEx(&cfg, kern, a) != cudaSuccess) {
+    cudaGetLastError();
+    if (!ss) return LcLaunch::kNotLaunched;
+    // the fork event was recorded on st: keep the side stream joined (capture stays balanced)
+    cudaStreamWaitEvent(ss->s, ss->fork, 0);
+    cudaEventRecord(ss->join, ss->s);
+    cudaStreamWaitEvent(st, ss->join, 0);
+    return LcLaunch::kNotLaunched;
+  }
+  count_launch();
+  LcLaunch res = LcLaunch::kLaunched;
   if (ss) {
     // launched after the clusters so its CTAs land on the SMs they left free
-    const size_t psm = kPipeSmem;
-    cudaFuncSetAttribute(loss_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm);
     cudaStreamWaitEvent(ss->s, ss->fork, 0);
-    loss_pipe_kernel<<<(unsigned)idle, kPipeThreads, psm, ss->s>>>(
+    loss_pipe_kernel<<<(unsigned)idle, kPipeThreads, kPipeSmem, ss->s>>>(
         N, a.logits, a.ld, a.V, a.tok, a.node_mask, a.boundary_mode, a.gamma, a.w, a.wr, a.node, a.node_start,
         a.node_len, a.succ_ptr, a.succ_tok, a.dlogits, a.tok_loss, a.ws_loss, a.ws_omega, a.d_err, N - n_pipe);
-    count_launch();
-    if (cudaGetLastError() != cudaSuccess) return false;
+    const cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) {
+      count_launch();
+    } else {
+      set_error("loss_pipe_kernel (tail rows %lld..%lld): %s", (long long)(N - n_pipe), (long long)N, cudaGetErrorString(e));
+      res = LcLaunch::kFailed;
+    }
+    // always join, even after a failed tail launch
     cudaEventRecord(ss->join, ss->s);
     cudaStreamWaitEvent(st, ss->join, 0);
   }
-  return true;
+  return res;
 }
 
 }  // namespace
@@ -1130,55 +1158,62 @@ tt_status launch_loss(const tt_packed& pk, const __nv_bfloat16* logits, int64_t 
   // loss_pipe_kernel: 16-element vectors over whole rows (V % 16 == 0) and 32-byte aligned rows
   const bool v16 = (vocab % 16 == 0) && (ld % 16 == 0) &&
                    ((reinterpret_cast<uintptr_t>(logits) | reinterpret_cast<uintptr_t>(dlogits)) % 32 == 0);
-  static const int variant = [] {
-    // development A/B: 0 ring/L2 kernel, 1 CS4x3 (else CS4x2), 3 CS8x4, 1x: poly splits, 2x: FAST passes
-    // (packed-bf16 max pass + f32x2 sum pass + f32x2 dlogits), 3x: other cluster sizes
-    const char* e = getenv("TT_LOSS_VARIANT");
-    // CS4 x 3 buffers, FAST passes, 25% polynomial exponentials in pass 2 only (variant 24 also put
-    // 25% of pass 1's on the polynomial, ~1% faster, but its 7.5e-5 relative error per term moves the
-    // lse by up to ~2e-5 and broke the dlogits tolerance on a small-vocabulary random case)
-    return e ? atoi(e) : 21;
-  }();
-  bool done = false;
-  if (variant != 0 && vocab % 8 == 0) {
+  LcLaunch lc = LcLaunch::kNotLaunched;
+  if (vocab % 8 == 0) {
     LcArgs a{pk.n_tokens, logits, ld, vocab, 0, 0, tok, node_mask, boundary_mode, gamma, pk.w, pk.wr,
-             pk.node, pk.node_start, pk.node_len, pk.succ_ptr, pk.succ_tok, dlogits, tok_loss, ws_loss, ws_omega, d_err};
+             pk.node, pk.node_start, pk.node_len, pk.succ_ptr, pk.succ_tok, dlogits, tok_loss, ws_loss, ws_omega, d_err, 0};
     a.max_t = std::max(1, pk.max_succ);
-    a.nocompute = getenv("TT_LOSS_NOCOMPUTE") ? 1 : 0;
-    if (variant == 1) done = try_launch_cluster<4, 3>(a, sms, st);  // fits while max_succ is small
-    else if (variant == 11) done = try_launch_cluster<4, 3, 2, 0>(a, sms, st);
-    else if (variant == 12) done = try_launch_cluster<4, 3, 2, 1>(a, sms, st);
-    else if (variant == 13) done = try_launch_cluster<4, 3, 1, 1>(a, sms, st);
-    else if (variant == 21) done = try_launch_cluster<4, 3, 1, 0, 1>(a, sms, st);
-    else if (variant == 22) done = try_launch_cluster<4, 3, 2, 0, 1>(a, sms, st);
-    else if (variant == 23) done = try_launch_cluster<4, 3, 2, 1, 1>(a, sms, st);
-    else if (variant == 24) done = try_launch_cluster<4, 3, 1, 1, 1>(a, sms, st);
-    else if (variant == 26) done = try_launch_cluster<4, 3, 1, 1, 1, 1>(a, sms, st);
-    else if (variant == 31) done = try_launch_cluster<8, 5, 1, 1, 1>(a, sms, st);
-    else if (variant == 32) done = try_launch_cluster<8, 4, 1, 1, 1>(a, sms, st);
-    else if (variant == 33) done = try_launch_cluster<2, 1, 1, 1, 1>(a, sms, st);
-    else if (variant == 34) done = try_launch_cluster<8, 5, 2, 1, 1>(a, sms, st);
-    else if (variant == 35) done = try_launch_cluster<3, 2, 1, 1, 1>(a, sms, st);
-    else if (variant == 36) done = try_launch_cluster<6, 4, 1, 1, 1>(a, sms, st);
-    else if (variant == 3) done = try_launch_cluster<8, 4>(a, sms, st);
-    if (!done) done = try_launch_cluster<4, 2>(a, sms, st);
+    // shipped kernel: 4-CTA clusters x 3 buffers, FAST passes, 25% polynomial exponentials in pass 2
+    // only (25% in pass 1 too was ~1% faster, but its 7.5e-5 relative error per term moves the lse by
+    // up to ~2e-5 and broke the dlogits tolerance on a small-vocabulary random case); 2 buffers when
+    // many continuation targets do not leave room for 3
+    int variant = 21;
+#ifdef TT_DEV
+    // development A/B: 0 ring/L2 kernel, 1 CS4x3, 3 CS8x4, 1x: poly splits, 2x: FAST passes, 3x: other
+    // cluster sizes; TT_LOSS_NOCOMPUTE streams the rows through without the math
+    if (const char* e = dev_getenv("TT_LOSS_VARIANT")) variant = atoi(e);
+    a.nocompute = dev_getenv("TT_LOSS_NOCOMPUTE") ? 1 : 0;
+    if (variant == 0) lc = LcLaunch::kNotLaunched;
+    else if (variant == 1) lc = try_launch_cluster<4, 3>(a, sms, st);
+    else if (variant == 11) lc = try_launch_cluster<4, 3, 2, 0>(a, sms, st);
+    else if (variant == 12) lc = try_launch_cluster<4, 3, 2, 1>(a, sms, st);
+    else if (variant == 13) lc = try_launch_cluster<4, 3, 1, 1>(a, sms, st);
+    else if (variant == 22) lc = try_launch_cluster<4, 3, 2, 0, 1>(a, sms, st);
+    else if (variant == 23) lc = try_launch_cluster<4, 3, 2, 1, 1>(a, sms, st);
+    else if (variant == 24) lc = try_launch_cluster<4, 3, 1, 1, 1>(a, sms, st);
+    else if (variant == 26) lc = try_launch_cluster<4, 3, 1, 1, 1, 1>(a, sms, st);
+    else if (variant == 31) lc = try_launch_cluster<8, 5, 1, 1, 1>(a, sms, st);
+    else if (variant == 32) lc = try_launch_cluster<8, 4, 1, 1, 1>(a, sms, st);
+    else if (variant == 33) lc = try_launch_cluster<2, 1, 1, 1, 1>(a, sms, st);
+    else if (variant == 34) lc = try_launch_cluster<8, 5, 2, 1, 1>(a, sms, st);
+    else if (variant == 35) lc = try_launch_cluster<3, 2, 1, 1, 1>(a, sms, st);
+    else if (variant == 36) lc = try_launch_cluster<6, 4, 1, 1, 1>(a, sms, st);
+    else if (variant == 3) lc = try_launch_cluster<8, 4>(a, sms, st);
+#endif
+    if (variant == 21) lc = try_launch_cluster<4, 3, 1, 0, 1>(a, sms, st);
+    if (variant != 0 && lc == LcLaunch::kNotLaunched) lc = try_launch_cluster<4, 2, 1, 0, 1>(a, sms, st);
   }
-  if (done) {
-  } else if (v16) {
-    const size_t smem = kPipeSmem;
-    cudaFuncSetAttribute(loss_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    loss_pipe_kernel<<<(unsigned)std::min<int64_t>(pk.n_tokens, sms), kPipeThreads, smem, st>>>(
-        pk.n_tokens, logits, ld, vocab, tok, node_mask, boundary_mode, gamma, pk.w, pk.wr, pk.node, pk.node_start,
-        pk.node_len, pk.succ_ptr, pk.succ_tok, dlogits, tok_loss, ws_loss, ws_omega, d_err, (int64_t)0);
-  } else {
-    loss_kernel<8><<<(unsigned)grid, kLossThreads, 0, st>>>(pk.n_tokens, logits, ld, vocab, tok, node_mask, boundary_mode,
-                                                            gamma, pk.w, pk.wr, pk.node, pk.node_start, pk.node_len,
-                                                            pk.succ_ptr, pk.succ_tok, dlogits, tok_loss, ws_loss,
-                                                            ws_omega, d_err);
+  if (lc == LcLaunch::kFailed) return TT_ERR_CUDA;  // message set by try_launch_cluster
+  if (lc == LcLaunch::kNotLaunched) {
+    if (v16) {
+      const size_t smem = kPipeSmem;
+      if (cudaFuncSetAttribute(loss_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+        set_error("loss_pipe_kernel: smem attribute: %s", cudaGetErrorString(cudaGetLastError()));
+        return TT_ERR_CUDA;
+      }
+      loss_pipe_kernel<<<(unsigned)std::min<int64_t>(pk.n_tokens, sms), kPipeThreads, smem, st>>>(
+          pk.n_tokens, logits, ld, vocab, tok, node_mask, boundary_mode, gamma, pk.w, pk.wr, pk.node, pk.node_start,
+          pk.node_len, pk.succ_ptr, pk.succ_tok, dlogits, tok_loss, ws_loss, ws_omega, d_err, (int64_t)0);
+    } else {
+      loss_kernel<8><<<(unsigned)grid, kLossThreads, 0, st>>>(pk.n_tokens, logits, ld, vocab, tok, node_mask, boundary_mode,
+                                                              gamma, pk.w, pk.wr, pk.node, pk.node_start, pk.node_len,
+                                                              pk.succ_ptr, pk.succ_tok, dlogits, tok_loss, ws_loss,
+                                                              ws_omega, d_err);
+    }
+    count_launch();
+    tt_status s = check_launch("loss_kernel");
+    if (s) return s;
   }
-  count_launch();
-  tt_status s = check_launch("loss_kernel");
-  if (s) return s;
   loss_sum_kernel<<<1, 1024, 0, st>>>(pk.n_tokens, ws_loss, ws_omega, sums);
   count_launch();
   return check_launch("loss_sum_kernel");

@@ -212,6 +212,7 @@ const char* tt_status_string(tt_status s) {
 
 const char* tt_last_error(void) { return g_err.c_str(); }
 int32_t tt_version(void) { return 100; }
+int32_t tt_build_flags(void) { return tt::kDevBuild ? TT_BUILD_DEV : 0; }
 int64_t tt_launch_count(void) { return g_launches; }
 void tt_launch_count_reset(void) { g_launches = 0; }
 
@@ -235,6 +236,64 @@ tt_status tt_pack_plan(const int32_t* parent, const int32_t* len, const int32_t*
   info->n_pairs = H.pairs;
   info->n_linear_pairs = H.lin_pairs;
   info->ws_bytes = L.total;
+  return TT_OK;
+}
+
+// Host -> device copy of a host-built image through a per-thread ring of pinned staging buffers
+// (a copy from pageable memory would synchronise the stream).  A slot is rewritten only after the
+// event recorded behind its previous copy has completed.  Staging a host image is not capturable
+// (a graph would replay whatever the slot holds then), so a capturing stream is refused.
+static tt_status stage_h2d(void* dst, const void* src, size_t bytes, cudaStream_t st, const char* who) {
+  struct Slot { void* buf = nullptr; size_t cap = 0; cudaEvent_t ev = nullptr; bool used = false; };
+  struct Ring {
+    Slot slot[4];
+    int next = 0;
+    ~Ring() {
+      // thread exit: release what this thread staged through (errors ignored at process teardown)
+      for (Slot& s : slot) {
+        if (s.ev) { cudaEventSynchronize(s.ev); cudaEventDestroy(s.ev); }
+        if (s.buf) cudaFreeHost(s.buf);
+      }
+      cudaGetLastError();
+    }
+  };
+  thread_local Ring ring;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+    cudaGetLastError();
+    set_error("%s: stages host data and cannot be captured into a CUDA graph (call it outside the capture)", who);
+    return TT_ERR_INVALID_ARGUMENT;
+  }
+  Slot& s = ring.slot[ring.next];
+  ring.next = (ring.next + 1) % 4;
+  if (s.used && cudaEventSynchronize(s.ev) != cudaSuccess) {
+    set_error("%s: staging event: %s", who, cudaGetErrorString(cudaGetLastError()));
+    return TT_ERR_CUDA;
+  }
+  if (s.cap < bytes) {
+    if (s.buf) cudaFreeHost(s.buf);
+    s.buf = nullptr;
+    s.cap = 0;
+    const size_t cap = std::max<size_t>(bytes, 1 << 16);
+    if (cudaHostAlloc(&s.buf, cap, cudaHostAllocDefault) != cudaSuccess) {
+      set_error("%s: pinned staging buffer (%zu bytes): %s", who, cap, cudaGetErrorString(cudaGetLastError()));
+      return TT_ERR_CUDA;
+    }
+    s.cap = cap;
+  }
+  if (!s.ev && cudaEventCreateWithFlags(&s.ev, cudaEventDisableTiming) != cudaSuccess) {
+    set_error("%s: staging event: %s", who, cudaGetErrorString(cudaGetLastError()));
+    return TT_ERR_CUDA;
+  }
+  std::memcpy(s.buf, src, bytes);
+  cudaError_t e = cudaMemcpyAsync(dst, s.buf, bytes, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaEventRecord(s.ev, st);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    set_error("%s: H2D copy failed: %s", who, cudaGetErrorString(e));
+    return TT_ERR_CUDA;
+  }
+  s.used = true;
   return TT_OK;
 }
 
@@ -266,8 +325,7 @@ tt_status tt_pack(const int32_t* parent, const int32_t* len, const int32_t* term
   img.insert(img.end(), H.order_start.begin(), H.order_start.end());
   int32_t* nb = reinterpret_cast<int32_t*>(base + L.off_nodeblk);
   cudaStream_t st = as_cuda(stream);
-  cudaError_t e = cudaMemcpyAsync(nb, img.data(), img.size() * 4, cudaMemcpyHostToDevice, st);
-  if (e != cudaSuccess) { set_error("tt_pack: H2D copy failed: %s", cudaGetErrorString(e)); return TT_ERR_CUDA; }
+  if ((s = stage_h2d(nb, img.data(), img.size() * 4, st, "tt_pack"))) return s;
   tt_packed P{};
   P.pos = reinterpret_cast<int32_t*>(base + L.off_pos);
   P.w = reinterpret_cast<int32_t*>(base + L.off_w);
@@ -342,8 +400,7 @@ tt_status tt_pack_weights(const int32_t* parent, const int32_t* len, const int32
     const float wu = (float)W[u];
     for (int32_t i = H.start[u]; i < H.start[u] + H.len[u]; ++i) img[i] = wu;
   }
-  cudaError_t e = cudaMemcpyAsync(wr, img.data(), img.size() * 4, cudaMemcpyHostToDevice, as_cuda(stream));
-  if (e != cudaSuccess) { set_error("tt_pack_weights: H2D copy failed: %s", cudaGetErrorString(e)); return TT_ERR_CUDA; }
+  if (tt_status s2 = stage_h2d(wr, img.data(), img.size() * 4, as_cuda(stream), "tt_pack_weights")) return s2;
   pk->wr = wr;
   return TT_OK;
 }

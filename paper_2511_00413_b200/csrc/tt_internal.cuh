@@ -7,6 +7,7 @@
 
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <string>
 
 #include <cuda.h>
@@ -14,6 +15,21 @@
 #include "../../include/tt.h"
 
 namespace tt {
+
+// Development A/B switches (ablations, variant sweeps, CTA orders, cycle counters) exist only in a
+// build compiled with -DTT_DEV (python -m paper_2511_00413_b200.build --dev).  In the shipped
+// library dev_getenv() is always null and dev_dbg() a constant 0, so no environment variable can
+// change what a kernel computes or skip work (tests/test_abi.py checks the release build ignores
+// them).
+#ifdef TT_DEV
+inline const char* dev_getenv(const char* name) { return getenv(name); }
+__host__ __device__ constexpr int dev_dbg(int d) { return d; }
+constexpr bool kDevBuild = true;
+#else
+inline const char* dev_getenv(const char*) { return nullptr; }
+__host__ __device__ constexpr int dev_dbg(int) { return 0; }
+constexpr bool kDevBuild = false;
+#endif
 
 void set_error(const char* fmt, ...);
 void clear_error();

@@ -94,3 +94,14 @@ def test_missing_library_fails_loudly(monkeypatch):
         binding.lib()
     with pytest.raises(ImportError):
         binding.tt_pack_plan([-1, 0], [3, 2])
+
+
+def test_release_build_has_no_dev_switches(tt):
+    """The shipped libtt.so is a release build: tt_build_flags() reports no TT_DEV, and none of the
+    development A/B environment variables (ablations that skip work, variant sweeps, CTA orders) is
+    even referenced by the binary, so a stray variable on a bench box cannot change the timed work."""
+    assert tt.lib().tt_build_flags() & 1 == 0
+    blob = open(tt.lib_path(), "rb").read()
+    for name in (b"TT_DEBUG_FWD", b"TT_DEBUG_BWD", b"TT_CTA_ORDER", b"TT_LOSS_VARIANT", b"TT_LOSS_NOCOMPUTE",
+                 b"TT_LOSS_SPLIT", b"TT_LOSS_MAXCL", b"TT_LOSS_DEBUG"):
+        assert name not in blob, name

@@ -313,3 +313,57 @@ def test_full_size_tree_equals_linearised_kernels(tt, cfg, seed):
         acc = torch.zeros(o.shape[0], H, d, dtype=torch.float32, device="cuda")
         acc.index_add_(0, iq, lin_g.float())
         assert rel_l2(tree_g, acc.cpu()) <= TOL_G_BF16
+
+
+def _root_key_case(tt, t, hq, hkv, seed, n_rows, key_blocks, full=False):
+    """Tree whose first key blocks are seen by every query row (>= 256 query blocks of 128 rows):
+    dK/dV of those root blocks accumulate over every q-tile x GQA head of the tree in one CTA, and
+    dQ rows along the whole range receive ~N/128 key-block contributions.  Compared with the fp64
+    oracle directly (rel-L2 per tensor and per head), not with the linearised kernels."""
+    pk, (q, k, v, G, scale), (o, lse, dq, dk, dv) = _run(tt, t, hq, hkv, 128, "bf16", seed=seed)
+    opk = oracle.pack(t.parent, t.length)
+    N = opk["n_tokens"]
+    assert N >= 256 * 128 and opk["E"][0] == N  # the root key block sees >= 256 query blocks
+    rng = np.random.default_rng(seed)
+    if full:
+        wq = wk = None
+        mq = mk = np.ones(N, bool)
+    else:
+        wq = np.zeros(N, np.uint8)
+        wq[np.linspace(0, N - 1, n_rows).astype(np.int64)] = 1   # spread along the whole range
+        wq[rng.choice(N, n_rows // 4, replace=False)] = 1
+        wk = np.zeros(N, np.uint8)
+        for kb in key_blocks:
+            wk[kb * 128:min(N, kb * 128 + 128)] = 1
+        mq, mk = wq.astype(bool), wk.astype(bool)
+    oo, olse = oracle.attn_fwd(opk, q, k, v, scale, want=wq, check_invariant=False)
+    assert max_abs(o[mq], oo[mq]) <= TOL_O_BF16
+    assert max_abs(lse[:, mq], olse[:, mq]) <= TOL_O_BF16
+    odq, odk, odv = oracle.attn_bwd(opk, q, k, v, G, scale, want_q=wq, want_k=wk)
+    assert rel_l2(dq[mq], odq[mq]) <= TOL_G_BF16
+    assert rel_l2(dk[mk], odk[mk]) <= TOL_G_BF16
+    assert rel_l2(dv[mk], odv[mk]) <= TOL_G_BF16
+    for h in range(hq):
+        assert rel_l2(dq[mq][:, h], odq[mq][:, h]) <= TOL_G_BF16
+    for h in range(hkv):
+        assert rel_l2(dk[mk][:, h], odk[mk][:, h]) <= TOL_G_BF16
+        assert rel_l2(dv[mk][:, h], odv[mk][:, h]) <= TOL_G_BF16
+    # each root key block on its own (its 128 keys x heads), so a bad block cannot hide in the sum
+    for kb in ([0, 1] if full else key_blocks):
+        s = slice(kb * 128, kb * 128 + 128)
+        assert rel_l2(dk[s], odk[s]) <= TOL_G_BF16 and rel_l2(dv[s], odv[s]) <= TOL_G_BF16
+
+
+def test_root_keys_deep_prefix_vs_oracle(tt):
+    """Deep shape (16K shared prefix, two 8.2K continuations, N = 32,768, GQA 4/1): the root key
+    blocks walk all 256 query blocks x 4 heads (1,024 dK/dV accumulation steps of 128 rows) — the
+    heaviest backward work of deep32k / batch64k, checked against the oracle."""
+    t = trees.Tree([-1, 0, 0], [16384, 8192, 8192], name="deep_root")
+    _root_key_case(tt, t, 4, 1, seed=41, n_rows=64, key_blocks=[0, 1, 63, 127, 128, 191, 255])
+
+
+def test_root_keys_star_full_vs_oracle(tt):
+    """Wide shape (256-token root + 255 leaves of 128, N = 32,896, GQA 8/2): the root key blocks see
+    all 257 query blocks x 4 heads; every dQ / dK / dV element is compared with the oracle."""
+    t = trees.star(256, [128] * 255)
+    _root_key_case(tt, t, 8, 2, seed=43, n_rows=0, key_blocks=[], full=True)

@@ -270,3 +270,45 @@ def test_loss_first_call_inside_capture(tt):
     a, b = dl0.float(), dl1.float()
     assert torch.all((a - b).abs() <= 2.0 ** -8 * a.abs() + 1e-6)
     assert torch.allclose(sums0, sums1, rtol=1e-6, atol=0)
+
+
+@pytest.mark.parametrize("cfg", ["agentic8k", "wide"])
+def test_loss_full_vocab_every_row(tt, cfg):
+    """Qwen3 vocabulary (V = 151,936) at a BASELINE config's full size, in place as in the bench: the
+    per-token loss of EVERY row (cluster-kernel rows and the tail rows the idle SMs take) against the
+    oracle, and dlogits element-wise on 192 rows (96 spread over the whole range, 96 from the last
+    30%, where the tail-row kernel works), plus the fp64 sums."""
+    import torch
+    t = trees.config_tree(cfg, 0 if cfg == "agentic8k" else None)
+    V = 151936
+    pk = tt.tt_pack(t.parent, t.length, t.term)
+    N = pk.n_tokens
+    x = tensors.logits_tensor(N, V, seed=19)
+    tok = tensors.token_ids(N, V, seed=20)
+    xd = x.cuda()
+    tl = torch.empty(N, dtype=torch.float32, device="cuda")
+    sums, dl, _, err = tt.tt_restore_loss(pk, xd, tok.cuda(), dlogits=xd, tok_loss=tl)
+    torch.cuda.synchronize()
+    assert int(err.item()) == 0
+    opk = oracle.pack(t.parent, t.length, t.term)
+    rng = np.random.default_rng(5)
+    sample = np.unique(np.concatenate([np.linspace(0, N - 1, 96).astype(np.int64),
+                                       rng.choice(np.arange(int(0.7 * N), N), 96, replace=False)]))
+    tl_all = to64(tl.cpu())
+    lsum = 0.0
+    osum = 0.0
+    for r0 in range(0, N, 1024):
+        rows = np.arange(r0, min(N, r0 + 1024))
+        lr, om, dx = oracle.loss(opk, tok.numpy(), V, rows, x[r0:rows[-1] + 1])
+        assert np.allclose(tl_all[rows], lr, rtol=1e-5, atol=1e-4 * max(1.0, om.max())), r0
+        lsum += lr.sum()
+        osum += om.sum()
+        pick = sample[(sample >= r0) & (sample <= rows[-1])]
+        if len(pick):
+            g = to64(dl[torch.as_tensor(pick)].cpu())
+            ref = dx[pick - r0]
+            tol = 2.0 ** -8 * np.abs(ref) + 1e-5 * np.maximum(om[pick - r0], 1.0)[:, None]
+            assert np.all(np.abs(g - ref) <= tol), r0
+    s = sums.cpu().numpy()
+    assert abs(s[0] - lsum) <= 1e-5 * abs(lsum)
+    assert s[1] == osum

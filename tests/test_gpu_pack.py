@@ -83,3 +83,30 @@ def test_pack_successor_lists(tt):
         if len(idx) > 3:
             nxt.add(int(idx[3]))
     assert sorted(st[sp[0]:sp[1]].tolist()) == sorted(nxt)
+
+
+def test_pack_refuses_graph_capture_and_explicit_stream():
+    """tt_pack stages its node tables through pinned host buffers: inside a CUDA-graph capture it
+    returns TT_ERR_INVALID_ARGUMENT instead of recording a host copy; on an explicit side stream it
+    packs exactly what the default stream does."""
+    import numpy as np
+    import torch
+    import paper_2511_00413_b200 as tt
+    from workloads import trees
+    t = trees.gen_agentic(2000, root_len=300, seed=2)
+    ref = tt.tt_pack(t.parent, t.length)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        pk = tt.tt_pack(t.parent, t.length, stream=s)
+    s.synchronize()
+    for key in ("pos", "w", "E", "node", "fwd_cnt"):
+        assert torch.equal(pk.arrays()[key], ref.arrays()[key]), key
+    g = torch.cuda.CUDAGraph()
+    with pytest.raises(tt.TTError) as ei:
+        with torch.cuda.graph(g, stream=s):
+            tt.tt_pack(t.parent, t.length, stream=s)
+    assert ei.value.code == 1
+    # many packs in a row reuse the 4 staging slots (each waits only for its slot's previous copy)
+    outs = [tt.tt_pack(t.parent, t.length) for _ in range(9)]
+    torch.cuda.synchronize()
+    assert all(torch.equal(o.arrays()["E"], ref.arrays()["E"]) for o in outs)

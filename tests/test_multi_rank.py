@@ -103,3 +103,52 @@ def test_unequal_lpt_counts_fit_the_record_slot():
         for k, v in enumerate(recs[t]):
             ref[k] += v
     assert tot == ref
+
+
+def _bench_worker(rank, world, port, n_trees, work, out_q):
+    """bench.py's own step aggregation (bench.aggregate) on gloo: LPT partition, fixed-size record
+    all_gather, tree-id-ordered reduction, max-over-ranks time and summed FLOPs."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    assign, _ = sharding.lpt_partition(work, world)
+    recs = [(t, torch.tensor(_fake_record(t), dtype=torch.float64)) for t in assign[rank]]
+    my_ms = 10.0 + rank
+    my_flops = float(sum(work[t] for t in assign[rank]))
+    tot, n, t_max, flops = bench.aggregate(recs, my_ms, my_flops, n_trees, dist, world, device=None)
+    out_q.put((world, rank, tot, n, t_max, flops))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_bench_aggregate_world_sizes_bitwise():
+    """the totals bench.py prints are bitwise identical at world sizes 1, 2 and 4 (the
+    same per-tree records, gathered and summed in tree-id order), the job time is the max over
+    ranks and the FLOPs are summed over ranks."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    n_trees = 13
+    work = [int(x) for x in torch.randint(1, 10 ** 6, (n_trees,), generator=torch.Generator().manual_seed(5))]
+    recs1 = [(t, torch.tensor(_fake_record(t), dtype=torch.float64)) for t in range(n_trees)]
+    ref, n1, t1, f1 = bench.aggregate(recs1, 10.0, float(sum(work)), n_trees)
+    assert n1 == n_trees and t1 == 10.0 and f1 == float(sum(work))
+    ctx = mp.get_context("spawn")
+    for world in (2, 4):
+        q = ctx.Queue()
+        port = _free_port()
+        procs = [ctx.Process(target=_bench_worker, args=(r, world, port, n_trees, work, q)) for r in range(world)]
+        for p in procs:
+            p.start()
+        res = [q.get(timeout=180) for _ in range(world)]
+        for p in procs:
+            p.join(timeout=60)
+            assert p.exitcode == 0
+        for w, rank, tot, n, t_max, flops in res:
+            assert n == n_trees
+            assert tot == ref, (world, rank)          # bitwise
+            assert t_max == 10.0 + world - 1          # max over ranks
+            assert flops == float(sum(work))

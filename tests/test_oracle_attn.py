@@ -208,3 +208,25 @@ def test_want_rows_subset_matches_full():
     mk = wk.astype(bool)
     assert np.array_equal(dq2[m], dq[m])
     assert np.array_equal(dk2[mk], dk[mk]) and np.array_equal(dv2[mk], dv[mk])
+
+
+def test_want_subset_thread_count_and_single_filters():
+    """The sampled backward splits work over rows / keys only: identical bits at any thread count,
+    and with only one of want_q / want_k given (the other outputs stay 0)."""
+    t = trees.gen_agentic(500, root_len=120, seed=6)
+    pk = oracle.pack(t.parent, t.length)
+    N = pk["n_tokens"]
+    q, k, v, G = _rand(N, 4, 2, 8, seed=4)
+    dq, dk, dv = oracle.attn_bwd(pk, q, k, v, G, 0.3)
+    rng = np.random.default_rng(3)
+    wq = np.zeros(N, np.uint8)
+    wq[rng.choice(N, 30, replace=False)] = 1
+    wk = np.zeros(N, np.uint8)
+    wk[:5] = 1                      # root keys: every row of every branch contributes
+    wk[rng.choice(N, 10, replace=False)] = 1
+    mq, mk = wq.astype(bool), wk.astype(bool)
+    for nt in (1, 3, 8):
+        a = oracle.attn_bwd(pk, q, k, v, G, 0.3, want_q=wq, nthreads=nt)
+        assert np.array_equal(a[0][mq], dq[mq]) and not a[1].any()
+        b = oracle.attn_bwd(pk, q, k, v, G, 0.3, want_k=wk, nthreads=nt)
+        assert np.array_equal(b[1][mk], dk[mk]) and np.array_equal(b[2][mk], dv[mk]) and not b[0].any()
