@@ -518,10 +518,21 @@ def time_forest_pack(trees_list, reps=5):
         torch.cuda.synchronize()
         if r:
             ts.append(a.elapsed_time(b))
-    return float(np.median(ts)), pk.n_tokens, pk.n_blk, int(pk.info["n_fwd_tiles"])
+    tiles = int(pk.arrays()["fwd_cnt"].sum().item())
+    return float(np.median(ts)), pk.n_tokens, pk.n_blk, tiles
 
 
 # ------------------------------------------------------------------------------------ main
+def run_leg(out, name, fn):
+    """An extra measurement after the timed step: a failure is recorded in the line, never loses it."""
+    import traceback
+    try:
+        fn()
+    except Exception as e:  # noqa: BLE001
+        out.setdefault("leg_errors", {})[name] = f"{type(e).__name__}: {e}"
+        traceback.print_exc()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -748,7 +759,7 @@ def main():
         if e2e:
             result["e2e"] = e2e
         out = result
-    if rank == 0 and not args.no_extras:
+    def leg_pack():
         # a1 over the rank's whole batch in one launch; per-step packs above are per tree
         pms, pN, pnb, ptiles = time_forest_pack([j.tree for j in jobs])
         pbytes = 16 * pN + 12 * pnb + 4 * ptiles
@@ -760,8 +771,10 @@ def main():
                                 "algorithmic": "16 B/token written (pos, w, E, node) + 12 B/block (min/max E, tile count) "
                                                "+ 4 B per non-empty tile",
                                 "tokens": pN, "ms": round(pms, 4), "peak_source": peaks["source"] + ", HBM copy bandwidth"}
+    if rank == 0 and not args.no_extras:
+        run_leg(out, "pack", leg_pack)
     # ---- per-branch linear comparison (same kernels, untimed w.r.t. the step; rank 0's first tree) ----
-    if rank == 0 and not args.no_linear:
+    def leg_linear():
         j0 = jobs[0]
         tree_ms = (per_op["fwd"] + per_op["bwd"]) / len(jobs) if len(jobs) == 1 else None
         if tree_ms is None:
@@ -785,7 +798,9 @@ def main():
                 "loss_speedup": round(ll_ms / t_loss, 3),
                 "loss_frac_of_token_ratio": round(ll_ms / t_loss / tr, 3),
                 "attn_plus_loss_speedup": round((lin_ms + ll_ms) / (tree_ms + t_loss), 3)})
-    if rank == 0 and not args.no_extras:
+    if rank == 0 and not args.no_linear:
+        run_leg(out, "linear", leg_linear)
+    def leg_next():
         # NEXT-f1: capacity-constrained Tree Packing of this rank's tree at a budget forcing a split
         # (C = max(longest trajectory, tree tokens / 2)); host planner timing + effective reuse
         t_ = jobs[0].tree
@@ -856,7 +871,9 @@ def main():
                                      "workspace_bytes": int(wsl.numel()),
                                      "materialised_logits_bytes_avoided": int(2 * 2 * Nl * VOCAB)}
             del Hh, Wl, dHl, dWl, wsl
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and not args.no_extras:
+        run_leg(out, "next", leg_next)
+    def leg_cpu():
         dt, share, ntraj, cores = oracle_sample(jobs[0].tree, cfg, budget_s=args.cpu_budget)
         full_s = dt / share
         out["cpu_baseline"] = {"value": round(jobs[0].flops() / full_s / 1e12, 6), "unit": "TFLOP/s", "cores": cores,
@@ -867,6 +884,8 @@ def main():
                                          f"tree's effective FLOPs / the measured time",
                                "extrapolated_full_tree_s": round(full_s, 1), "cpu_model": cpu_model(),
                                "host_cpus": os.cpu_count()}
+    if rank == 0 and world == 1 and not args.no_cpu:
+        run_leg(out, "cpu", leg_cpu)
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:

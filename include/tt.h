@@ -24,6 +24,7 @@
  *   tt_plan_traversals / tt_traversal_forest   capacity-constrained Tree Packing (NEXT-f1)
  *   tt_rope / tt_restore_grad                  restored-position RoPE and the Gradient Scaler (NEXT-f2)
  *   tt_lmhead_loss                             LM head + restoration loss without [N, V] logits (NEXT-f3)
+ *   tt_gemm                                    its tcgen05 GEMM (CTA pairs, fused epilogues)
  *   tt_pack_weights                            real-valued per-trajectory weights (NEXT-f4)
  *
  * Conventions (all entry points):
@@ -32,7 +33,7 @@
  *   - Memory: the CALLER owns every buffer.  The library never allocates device memory, never
  *     frees, never synchronises a stream, and keeps no global state except the thread-local
  *     error string, a cached per-device attribute query, and lazily created per-thread,
- *     per-device handles: a cuBLASLt handle (tt_lmhead_loss), one side stream + two events
+ *     per-device handles: one side stream + two events
  *     (tt_restore_loss; never created while `stream` is capturing) and a ring of 4 pinned host
  *     staging buffers + events (tt_pack / tt_pack_weights; released at thread exit).
  *   - Host vs device: pointers documented as HOST are read synchronously during the call;
@@ -300,15 +301,17 @@ tt_status tt_traversal_forest(const int32_t* parent, const int32_t* len, const i
  * X = H W^T computed and kept in fp32):
  *   loss_t = sum_k omega_k (lse(x_t) - x_t[y_k]),   G_t = gamma (Omega_t softmax(x_t) - sum_k omega_k e_{y_k})
  *   dH = G W  [N, hidden],   dW = G^T H  [vocab, hidden]
- * The vocabulary is processed in chunks of vocab_chunk columns (largest temporary [N, vocab_chunk]
- * fp32 + bf16); logits are computed twice (sweep 1: lse, sweep 2: G), G is rounded to bf16 once as
- * the operand of the dH / dW GEMMs.  The four GEMMs per chunk are plain cuBLASLt calls (bf16 in,
- * fp32 compute); the cross-entropy steps are libtt kernels.
+ * Every contraction is the library's own tcgen05 GEMM (tt_gemm below) with the cross-entropy steps
+ * fused into its epilogues: sweep 1 is ONE GEMM over the whole vocabulary whose epilogue keeps only
+ * per-row (max, sum-exp) partials of each 128-column slice and the target logits (the [N, vocab]
+ * logits are never written); sweep 2 recomputes X per chunk of vocab_chunk columns with an epilogue
+ * that writes G in bf16 (largest temporary [N, vocab_chunk] bf16 + the fp32 dH accumulator), then
+ * dH (+)= G_c W_c and dW_c = G_c^T H.
  * h: DEVICE [N, hidden] bf16; w: DEVICE [vocab, hidden] bf16 (row-major, the LM-head weight);
  * tok / node_loss_mask / boundary_mode / grad_scale / tok_loss / sums / d_err: as tt_restore_loss.
  * dh: DEVICE [N, hidden] bf16 (written); dw: DEVICE [vocab, hidden] bf16 (written).
  * d_ws: DEVICE workspace of tt_lmhead_loss_workspace bytes (16-byte aligned), caller-owned.
- * hidden % 8 == 0.  Errors: as tt_restore_loss; TT_ERR_CUDA if a cuBLASLt call fails.
+ * hidden % 8 == 0.  Errors: as tt_restore_loss; TT_ERR_CUDA if a launch fails.
  * -------------------------------------------------------------------------------------- */
 tt_status tt_lmhead_loss_workspace(const tt_packed* pk, int32_t hidden, int32_t vocab, int32_t vocab_chunk,
                                    size_t* bytes);
@@ -316,6 +319,18 @@ tt_status tt_lmhead_loss(const tt_packed* pk, const void* h, const void* w, int3
                          int32_t vocab_chunk, const int32_t* tok, const uint8_t* node_loss_mask, int32_t boundary_mode,
                          float grad_scale, void* dh, void* dw, float* tok_loss, double* sums, int32_t* d_err,
                          void* d_ws, size_t ws_bytes, tt_stream_t stream);
+
+/* --------------------------------------------------------------------------------------
+ * GEMM building block of tt_lmhead_loss, exposed for direct testing:
+ *   D[M, N] (=|+=) A[M, K] . B[K, N]     bf16 operands, fp32 accumulation (tcgen05, CTA pairs)
+ * a: DEVICE bf16, stored row-major [M, K] (a_mn = 0) or [K, M] (a_mn = 1), row stride lda elements;
+ * b: DEVICE bf16, stored row-major [N, K] (b_mn = 0) or [K, N] (b_mn = 1), row stride ldb elements;
+ * d: DEVICE [M, ldd] row-major, bf16 (d_dt = TT_BF16, written) or fp32 (TT_FP32; accumulate = 1
+ *    adds into it).  Strides and base pointers 16-byte aligned.  M, N, K > 0.
+ * -------------------------------------------------------------------------------------- */
+tt_status tt_gemm(int32_t M, int32_t N, int32_t K, const void* a, int64_t lda, int32_t a_mn, const void* b,
+                  int64_t ldb, int32_t b_mn, void* d, int64_t ldd, tt_dtype d_dt, int32_t accumulate,
+                  tt_stream_t stream);
 
 /* --------------------------------------------------------------------------------------
  * Position-embedding correction (Eq. 23):

@@ -102,6 +102,8 @@ def lib():
                                          C.c_float, vp, vp, vp, vp, vp, vp, sz, st]
             L.tt_rope.argtypes = [C.POINTER(TTPacked), vp, C.c_int, C.c_int32, C.c_int32, C.c_double, C.c_int32, st]
             L.tt_restore_grad.argtypes = [C.POINTER(TTPacked), vp, C.c_int, C.c_int64, st]
+            L.tt_gemm.argtypes = [C.c_int32, C.c_int32, C.c_int32, vp, C.c_int64, C.c_int32, vp, C.c_int64, C.c_int32,
+                                  vp, C.c_int64, C.c_int, C.c_int32, st]
             L.tt_launch_count.restype = C.c_int64
             L.tt_launch_count.argtypes = []
             L.tt_launch_count_reset.argtypes = []
@@ -109,7 +111,7 @@ def lib():
             for fn in ("tt_pack_plan", "tt_pack", "tt_attn_fwd", "tt_attn_bwd_workspace", "tt_attn_bwd",
                        "tt_restore_loss", "tt_grad_sqnorm", "tt_grad_sqnorm3", "tt_plan_traversals",
                        "tt_traversal_forest", "tt_rope", "tt_restore_grad", "tt_lmhead_loss_workspace",
-                       "tt_lmhead_loss"):
+                       "tt_lmhead_loss", "tt_gemm"):
                 getattr(L, fn).restype = C.c_int
             _lib = L
     return _lib
@@ -439,6 +441,29 @@ def tt_lmhead_loss(pk: PackedTree, h, w, tok, grad_scale=1.0, vocab_chunk=16384,
                                                   float(grad_scale), _p(dh), _p(dw), _p(tok_loss), _p(sums),
                                                   _p(d_err), _p(ws), int(ws.numel()), _stream(stream)))
     return sums, dh, dw, tok_loss, d_err
+
+
+def tt_gemm(a, b, a_mn=False, b_mn=False, out=None, out_dtype=None, accumulate=False, stream=None):
+    """D = A . B on the library's tcgen05 GEMM.  a: bf16 [M, K] (a_mn=False) or [K, M] (a_mn=True);
+    b: bf16 [N, K] (b_mn=False) or [K, N] (b_mn=True); unit column stride, row stride = stride(0).
+    out: [M, N] bf16 or fp32 (accumulate=True adds into an fp32 out)."""
+    import torch
+    for t, n in ((a, "a"), (b, "b")):
+        if t.dim() != 2 or t.dtype != torch.bfloat16 or t.stride(1) != 1:
+            raise ValueError(f"{n} must be a bf16 matrix with unit column stride")
+    M, K = (a.shape[1], a.shape[0]) if a_mn else (a.shape[0], a.shape[1])
+    N, K2 = (b.shape[1], b.shape[0]) if b_mn else (b.shape[0], b.shape[1])
+    if K != K2:
+        raise ValueError(f"inner dimensions differ: {K} vs {K2}")
+    if out is None:
+        out = torch.zeros(M, N, dtype=out_dtype or torch.float32, device=a.device)
+    if out.dim() != 2 or out.shape[0] != M or out.shape[1] != N or out.stride(1) != 1:
+        raise ValueError("out must be [M, N] with unit column stride")
+    if b.device != a.device or out.device != a.device:
+        raise ValueError("a, b, out must share a device")
+    _check("tt_gemm", lib().tt_gemm(M, N, K, _p(a), a.stride(0), int(bool(a_mn)), _p(b), b.stride(0), int(bool(b_mn)),
+                                    _p(out), out.stride(0), _dt(out), int(bool(accumulate)), _stream(stream)))
+    return out
 
 
 def tt_rope(pk: PackedTree, x, base=1.0e6, inverse=False, stream=None):

@@ -80,10 +80,7 @@ def build(force: bool = False, verbose: bool = False, dev: bool = False) -> str:
     objs = [os.path.join(OBJ, os.path.basename(s)[:-3] + ".o") for s in srcs]
     if force or jobs or not os.path.exists(SO) or os.path.getmtime(SO) < max(os.path.getmtime(o) for o in objs):
         cuda_lib = os.path.join(os.path.dirname(os.path.dirname(os.path.realpath(nvcc()))), "lib64")
-        # cuBLASLt (plain library GEMMs of tt_lmhead_loss, NEXT-f3): dynamic, found via rpath or an
-        # already-loaded libcublasLt.so.12 (torch's)
-        cmd = [nvcc()] + ARCH + ["-shared", "-o", SO] + objs + ["-L" + cuda_lib, "-lcublasLt", "-Xlinker",
-                                                               "-rpath=" + cuda_lib, "-lcudart_static", "-ldl",
+        cmd = [nvcc()] + ARCH + ["-shared", "-o", SO] + objs + ["-L" + cuda_lib, "-lcudart_static", "-ldl",
                                                                "-lrt", "-lpthread"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:

@@ -537,7 +537,7 @@ tt_status tt_lmhead_loss_workspace(const tt_packed* pk, int32_t hidden, int32_t 
                                    size_t* bytes) {
   clear_error();
   if (!pk || !bytes || hidden <= 0 || vocab <= 0 || vocab_chunk <= 0) { set_error("tt_lmhead_loss_workspace: bad argument"); return TT_ERR_INVALID_ARGUMENT; }
-  *bytes = lmhead_ws_bytes(pk->n_tokens, hidden, vocab, vocab_chunk);
+  *bytes = lmhead_ws_bytes(pk->n_tokens, hidden, vocab, vocab_chunk, pk->max_succ);
   return TT_OK;
 }
 
@@ -555,10 +555,29 @@ tt_status tt_lmhead_loss(const tt_packed* pk, const void* h, const void* w, int3
     set_error("tt_lmhead_loss: tensors must be 16-byte aligned"); return TT_ERR_ALIGNMENT;
   }
   if (pk->n_tokens > INT32_MAX) { set_error("tt_lmhead_loss: too many rows"); return TT_ERR_TOO_LARGE; }
-  if (ws_bytes < lmhead_ws_bytes(pk->n_tokens, hidden, vocab, vocab_chunk)) { set_error("tt_lmhead_loss: workspace too small"); return TT_ERR_WORKSPACE; }
+  if (ws_bytes < lmhead_ws_bytes(pk->n_tokens, hidden, vocab, vocab_chunk, pk->max_succ)) { set_error("tt_lmhead_loss: workspace too small"); return TT_ERR_WORKSPACE; }
   return launch_lmhead_loss(*pk, static_cast<const __nv_bfloat16*>(h), static_cast<const __nv_bfloat16*>(w), hidden, vocab,
                             vocab_chunk, tok, node_loss_mask, boundary_mode, grad_scale, static_cast<__nv_bfloat16*>(dh),
                             static_cast<__nv_bfloat16*>(dw), tok_loss, sums, d_err, d_ws, as_cuda(stream));
+}
+
+tt_status tt_gemm(int32_t M, int32_t N, int32_t K, const void* a, int64_t lda, int32_t a_mn, const void* b,
+                  int64_t ldb, int32_t b_mn, void* d, int64_t ldd, tt_dtype d_dt, int32_t accumulate,
+                  tt_stream_t stream) {
+  clear_error();
+  if (M <= 0 || N <= 0 || K <= 0 || !a || !b || !d) { set_error("tt_gemm: bad argument"); return TT_ERR_INVALID_ARGUMENT; }
+  if (d_dt != TT_BF16 && d_dt != TT_FP32) { set_error("tt_gemm: bad output dtype"); return TT_ERR_INVALID_ARGUMENT; }
+  if (d_dt == TT_BF16 && accumulate) { set_error("tt_gemm: accumulate needs an fp32 output"); return TT_ERR_UNSUPPORTED; }
+  if (lda < (a_mn ? M : K) || ldb < (b_mn ? N : K) || ldd < N) { set_error("tt_gemm: leading dimension too small"); return TT_ERR_INVALID_ARGUMENT; }
+  if (!aligned16(a) || !aligned16(b) || !aligned16(d) || (lda % 8) || (ldb % 8)) {
+    set_error("tt_gemm: operands must be 16-byte aligned with row strides a multiple of 8 elements"); return TT_ERR_ALIGNMENT;
+  }
+  gemm::GemmEpilogue ep{};
+  ep.out = d;
+  ep.ldo = ldd;
+  ep.beta = accumulate ? 1 : 0;
+  return gemm::gemm_run(d_dt == TT_BF16 ? gemm::kEpiStoreBF16 : gemm::kEpiAccF32, M, N, K, a, lda, a_mn ? 1 : 0, b, ldb,
+                        b_mn ? 1 : 0, ep, as_cuda(stream));
 }
 
 tt_status tt_rope(const tt_packed* pk, void* x, tt_dtype dt, int32_t n_heads, int32_t d, double base,

@@ -93,7 +93,29 @@ tt_status launch_sqnorm(const void* const* xs, const int64_t* ns, int count, tt_
                         double* partials, cudaStream_t st);
 
 tt_status launch_loss_sums(int64_t N, const float* ws_loss, const float* ws_omega, double* sums, cudaStream_t st);
-size_t lmhead_ws_bytes(int64_t N, int D, int V, int Vc);
+size_t lmhead_ws_bytes(int64_t N, int D, int V, int Vc, int max_t);
+
+// tcgen05 GEMM of gemm_sm100.cu (CTA pairs): D[M, N] = A . B, epilogue selected by `epi`
+namespace gemm {
+enum { kEpiStoreBF16 = 0, kEpiAccF32 = 1, kEpiLsePartial = 2, kEpiDlogits = 3 };
+struct GemmEpilogue {
+  void* out = nullptr;       // bf16 (kEpiStoreBF16, kEpiDlogits) / fp32 (kEpiAccF32) [M, ldo]
+  int64_t ldo = 0;
+  int beta = 0;              // kEpiAccF32: accumulate
+  int col_offset = 0, vocab = 0;
+  void* part = nullptr;      // float2 [2 ceil(N / 256)][M]
+  int max_t = 1;
+  const int* tgt_cnt = nullptr;
+  const int* tgt_y = nullptr;
+  const float* tgt_w = nullptr;
+  float* tgt_x = nullptr;
+  const float* lse2 = nullptr;
+  const float* g_omega = nullptr;
+  float gamma = 1.f;
+};
+tt_status gemm_run(int epi, int M, int N, int K, const void* A, int64_t lda, int a_mn, const void* B, int64_t ldb,
+                   int b_mn, const GemmEpilogue& ep, cudaStream_t st);
+}  // namespace gemm
 tt_status launch_lmhead_loss(const tt_packed& pk, const __nv_bfloat16* H, const __nv_bfloat16* W, int D, int V, int Vc,
                              const int32_t* tok, const uint8_t* node_mask, int boundary_mode, float gamma,
                              __nv_bfloat16* dH, __nv_bfloat16* dW, float* tok_loss, double* sums, int32_t* d_err,
