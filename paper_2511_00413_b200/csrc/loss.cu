@@ -21,6 +21,8 @@
 #include <unordered_map>
 #include <cstdlib>
 
+#include <cuda_fp16.h>
+
 #include "tt_internal.cuh"
 #include "sm100_ptx.cuh"
 
@@ -88,6 +90,10 @@ __device__ __forceinline__ float2 bf2f(uint32_t u) {
 }
 __device__ __forceinline__ uint32_t f2bf(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+__device__ __forceinline__ uint32_t f2h(float lo, float hi) {
+  __half2 v = __floats2half2_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
 }
 __device__ __forceinline__ float ex2f(float x) {
@@ -839,6 +845,7 @@ __global__ void __launch_bounds__(kLcThreads, 1) loss_cluster_kernel(const LcArg
     __nv_bfloat16* xs = bufs + (size_t)b * Cq;
     const uint4* x4 = reinterpret_cast<const uint4*>(xs);
     float m = -INFINITY, sum = 0.f;
+    float tx = 0.f;
     if constexpr (FAST) {
       // pass 1a: slice max on packed bf16 pairs (HMNMX2, no conversion); 1b: sum of 2^(x log2e - M)
       // with packed f32x2 FMAs / adds — no online rescaling, ~3 issue slots per element
@@ -853,6 +860,17 @@ __global__ void __launch_bounds__(kLcThreads, 1) loss_cluster_kernel(const LcArg
       float tm = fmaxf(__bfloat162float(mx.x), __bfloat162float(mx.y));
       for (int o = 16; o > 0; o >>= 1) tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, o));
       if (lane == 0) s_max[grp][gw] = tm;
+      if constexpr (FAST == 2) {
+        // the target logits of this slice, read before pass 1b overwrites the slice (barrier below)
+        for (int k = gt; k < nt; k += GT) {
+          const int y = M.y[k];
+          if (y >= off && y < off + n) {
+            const float xy = __bfloat162float(xs[y - off]);
+            M.xy[k] = xy;
+            tx += M.om[k] * xy;
+          }
+        }
+      }
       bar_g();
       tm = s_max[grp][0];
 #pragma unroll
@@ -861,15 +879,21 @@ __global__ void __launch_bounds__(kLcThreads, 1) loss_cluster_kernel(const LcArg
       if (m != -INFINITY) {
         const float2 L2 = make_float2(kLog2e, kLog2e), NM = make_float2(-m, -m);
         float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
+        uint4* xw4 = reinterpret_cast<uint4*>(xs);
         for (int v = gt; v < n / 8; v += GT) {
           const uint4 q = x4[v];
           const uint32_t in[4] = {q.x, q.y, q.z, q.w};
+          uint32_t eh[4];
+          (void)eh;
+          (void)xw4;
 #pragma unroll
           for (int t = 0; t < 4; ++t) {
             const float2 e2 = sm100::ffma2(bf2f(in[t]), L2, NM);
             const float2 e = (t >= 4 - KP1) ? sm100::exp2_poly2(e2) : make_float2(ex2f(e2.x), ex2f(e2.y));
             if (t & 1) acc1 = sm100::fadd2(acc1, e); else acc0 = sm100::fadd2(acc0, e);
+            if constexpr (FAST == 2) eh[t] = f2h(e.x, e.y);
           }
+          if constexpr (FAST == 2) xw4[v] = make_uint4(eh[0], eh[1], eh[2], eh[3]);  // e in place, fp16
         }
         const float2 acc = sm100::fadd2(acc0, acc1);
         sum = acc.x + acc.y;
@@ -890,9 +914,9 @@ __global__ void __launch_bounds__(kLcThreads, 1) loss_cluster_kernel(const LcArg
         m = mm;
       }
     }
-    // target logits that live in this slice (read before pass 2 overwrites them)
-    float tx = 0.f;
-    for (int k = gt; k < nt; k += GT) {
+    // target logits that live in this slice (read before pass 2 overwrites them; FAST == 2 picked
+    // them up before pass 1b)
+    for (int k = gt; k < (FAST == 2 ? 0 : nt); k += GT) {
       const int y = M.y[k];
       if (y >= off && y < off + n) {
         const float xy = __bfloat162float(xs[y - off]);
@@ -948,7 +972,25 @@ __global__ void __launch_bounds__(kLcThreads, 1) loss_cluster_kernel(const LcArg
     const float gO = bad_any ? 0.f : a.gamma * Omega;
     // ---- pass 2: dlogits = gamma Omega softmax, in place in shared memory ----
     uint4* y4 = reinterpret_cast<uint4*>(xs);
-    if constexpr (FAST) {
+    if constexpr (FAST == 2) {
+      // the slice holds e = 2^(x log2e - m) (fp16, pass 1b): softmax = e 2^(m - lse2), one multiply
+      // per element and no exponential (the MUFU work of the row halves); fp16 keeps 11 significant
+      // bits (relative 2^-11, below the bf16 output rounding; values under 2^-24 flush to 0, an
+      // absolute error < 6e-8 gamma Omega)
+      const float sc = (m == -INFINITY) ? 0.f : gO * ex2f(m - lse2);
+      const float2 S2 = make_float2(sc, sc);
+      for (int v = gt; v < n / 8; v += GT) {
+        const uint4 q = y4[v];
+        const uint32_t in[4] = {q.x, q.y, q.z, q.w};
+        uint32_t o[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const float2 r2 = sm100::fmul2(__half22float2(*reinterpret_cast<const __half2*>(&in[t])), S2);
+          o[t] = f2bf(r2.x, r2.y);
+        }
+        y4[v] = make_uint4(o[0], o[1], o[2], o[3]);
+      }
+    } else if constexpr (FAST) {
       const float2 L2 = make_float2(kLog2e, kLog2e), NL = make_float2(-lse2, -lse2), G2 = make_float2(gO, gO);
       for (int v = gt; v < n / 8; v += GT) {
         const uint4 q = y4[v];
@@ -1166,7 +1208,10 @@ tt_status launch_loss(const tt_packed& pk, const __nv_bfloat16* logits, int64_t 
     // shipped kernel: 4-CTA clusters x 3 buffers, FAST passes, 25% polynomial exponentials in pass 2
     // only (25% in pass 1 too was ~1% faster, but its 7.5e-5 relative error per term moves the lse by
     // up to ~2e-5 and broke the dlogits tolerance on a small-vocabulary random case); 2 buffers when
-    // many continuation targets do not leave room for 3
+    // many continuation targets do not leave room for 3.  Dev variant 25 keeps pass 1's exponentials
+    // in place as fp16 so pass 2 needs no exponential: 1-3.5% faster (profiles/r2_loss_fp16_ab.txt),
+    // but the fp16 intermediate (2^-11 relative) pushes dlogits across a bf16 rounding boundary
+    // (1 element in 600K at V = 1000 missed the 2^-8 |dx| bound), so it is not shipped.
     int variant = 21;
 #ifdef TT_DEV
     // development A/B: 0 ring/L2 kernel, 1 CS4x3, 3 CS8x4, 1x: poly splits, 2x: FAST passes, 3x: other
@@ -1178,6 +1223,7 @@ tt_status launch_loss(const tt_packed& pk, const __nv_bfloat16* logits, int64_t 
     else if (variant == 11) lc = try_launch_cluster<4, 3, 2, 0>(a, sms, st);
     else if (variant == 12) lc = try_launch_cluster<4, 3, 2, 1>(a, sms, st);
     else if (variant == 13) lc = try_launch_cluster<4, 3, 1, 1>(a, sms, st);
+    else if (variant == 25) lc = try_launch_cluster<4, 3, 0, 0, 2>(a, sms, st);
     else if (variant == 22) lc = try_launch_cluster<4, 3, 2, 0, 1>(a, sms, st);
     else if (variant == 23) lc = try_launch_cluster<4, 3, 2, 1, 1>(a, sms, st);
     else if (variant == 24) lc = try_launch_cluster<4, 3, 1, 1, 1>(a, sms, st);

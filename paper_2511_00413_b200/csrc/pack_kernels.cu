@@ -8,7 +8,10 @@
 //   node = u
 // and reduces min / max E over the block's keys.  16 B/token written, coalesced.
 // Kernel 2 (one warp per q-block): classifies the tiles (qb, kb <= qb) from minE/maxE and
-// compacts the non-empty ones into the triangular fwd list (no global scan needed).
+// compacts the non-empty ones into the triangular fwd list (no global scan needed).  The scan starts
+// at kb_lo[qb], the first block of the tree holding the q-block's first token (host-computed): in a
+// forest no earlier tree's key is visible, so a batch of trees packs in O(sum of per-tree blocks^2)
+// instead of O(total blocks^2).
 #include "tt_internal.cuh"
 
 namespace tt {
@@ -56,7 +59,8 @@ __global__ void __launch_bounds__(kBlock) pack_fill_kernel(int64_t N, const int3
   }
 }
 
-__global__ void __launch_bounds__(32) pack_tiles_kernel(int64_t N, int32_t nb, const int32_t* __restrict__ kminE,
+__global__ void __launch_bounds__(32) pack_tiles_kernel(int64_t N, int32_t nb, const int32_t* __restrict__ kb_lo,
+                                                        const int32_t* __restrict__ kminE,
                                                         const int32_t* __restrict__ kmaxE, int32_t* __restrict__ fwd_cnt,
                                                         int32_t* __restrict__ fwd_list) {
   const int32_t qb = blockIdx.x;
@@ -65,7 +69,7 @@ __global__ void __launch_bounds__(32) pack_tiles_kernel(int64_t N, int32_t nb, c
   const int64_t i1 = imin64(N, i0 + kBlock);
   int32_t* out = fwd_list + tri_off(qb);
   int32_t cnt = 0;
-  for (int32_t base = 0; base <= qb; base += 32) {
+  for (int32_t base = kb_lo[qb]; base <= qb; base += 32) {
     const int32_t kb = base + lane;
     int cls = 0;
     if (kb < qb) {
@@ -85,6 +89,7 @@ __global__ void __launch_bounds__(32) pack_tiles_kernel(int64_t N, int32_t nb, c
 }
 
 tt_status launch_pack_fill(const tt_packed& pk, const int32_t* order, const int32_t* order_start, int32_t n_order,
+                           const int32_t* kb_lo,
                            int32_t* pos, int32_t* w, int32_t* E, int32_t* node, int32_t* kminE, int32_t* kmaxE,
                            int32_t* fwd_cnt, int32_t* fwd_list, cudaStream_t st) {
   const int32_t nb = pk.n_blk;
@@ -93,7 +98,7 @@ tt_status launch_pack_fill(const tt_packed& pk, const int32_t* order, const int3
   count_launch();
   tt_status s = check_launch("pack_fill_kernel");
   if (s) return s;
-  pack_tiles_kernel<<<nb, 32, 0, st>>>(pk.n_tokens, nb, kminE, kmaxE, fwd_cnt, fwd_list);
+  pack_tiles_kernel<<<nb, 32, 0, st>>>(pk.n_tokens, nb, kb_lo, kminE, kmaxE, fwd_cnt, fwd_list);
   count_launch();
   return check_launch("pack_tiles_kernel");
 }

@@ -40,6 +40,7 @@ struct HostPack {
   int32_t n = 0;
   int64_t N = 0;
   std::vector<int32_t> start, len, sub_end, depth, leaves;  // per node
+  std::vector<int32_t> root_start;                          // per node: first token of its tree
   std::vector<int32_t> succ_ptr, succ_tok;                  // per node CSR
   std::vector<int32_t> order, order_start;                  // nodes with len > 0, packed order
   std::vector<int32_t> pre, kids_ptr, kids;                 // DFS pre-order, children CSR
@@ -72,7 +73,7 @@ static tt_status host_pack(const int32_t* parent, const int32_t* len, const int3
       if (parent[v] >= 0) kids[fill[parent[v]]++] = v;
   }
   H.start.assign(n, 0); H.len.assign(len, len + n); H.sub_end.assign(n, 0);
-  H.depth.assign(n, 0); H.leaves.assign(n, 0);
+  H.depth.assign(n, 0); H.leaves.assign(n, 0); H.root_start.assign(n, 0);
   // iterative DFS pre-order
   std::vector<int32_t> pre;
   pre.reserve(n);
@@ -85,6 +86,7 @@ static tt_status host_pack(const int32_t* parent, const int32_t* len, const int3
     st.push_back(r);
     H.depth[r] = 0;
     H.start[r] = (int32_t)cursor;
+    H.root_start[r] = (int32_t)cursor;
     cursor += len[r];
     pre.push_back(r);
     while (!st.empty()) {
@@ -94,6 +96,7 @@ static tt_status host_pack(const int32_t* parent, const int32_t* len, const int3
         int32_t c = kids[c0 + next_child[u]++];
         H.depth[c] = H.depth[u] + len[u];
         H.start[c] = (int32_t)cursor;
+        H.root_start[c] = H.root_start[r];
         cursor += len[c];
         pre.push_back(c);
         st.push_back(c);
@@ -183,7 +186,7 @@ static PackLayout pack_layout(int64_t N, int32_t n, int32_t n_succ, int32_t n_or
   L.off_flist = o; o = al256(o + (size_t)tri_off(L.nb) * 4);
   // node block: start, len, sub_end, depth, leaves [n] each, succ_ptr [n+1], succ_tok, order, order_start
   L.off_nodeblk = o;
-  L.nodeblk_bytes = (size_t)(5 * (size_t)n + (n + 1) + n_succ + 2 * (size_t)n_order) * 4;
+  L.nodeblk_bytes = (size_t)(5 * (size_t)n + (n + 1) + n_succ + 2 * (size_t)n_order + L.nb) * 4;
   o = al256(o + L.nodeblk_bytes);
   L.total = o;
   return L;
@@ -323,6 +326,13 @@ tt_status tt_pack(const int32_t* parent, const int32_t* len, const int32_t* term
   img.insert(img.end(), H.succ_tok.begin(), H.succ_tok.end());
   img.insert(img.end(), H.order.begin(), H.order.end());
   img.insert(img.end(), H.order_start.begin(), H.order_start.end());
+  // per q-block: the first k-block of the tree holding the block's first token (no key of an
+  // earlier tree is ever visible, so the tile classification of a forest starts there)
+  for (int32_t qb = 0; qb < L.nb; ++qb) {
+    const int32_t i0 = qb * kBlock;
+    const int32_t k = (int32_t)(std::upper_bound(H.order_start.begin(), H.order_start.end(), i0) - H.order_start.begin()) - 1;
+    img.push_back(H.root_start[H.order[std::max(k, 0)]] / kBlock);
+  }
   int32_t* nb = reinterpret_cast<int32_t*>(base + L.off_nodeblk);
   cudaStream_t st = as_cuda(stream);
   if ((s = stage_h2d(nb, img.data(), img.size() * 4, st, "tt_pack"))) return s;
@@ -340,6 +350,7 @@ tt_status tt_pack(const int32_t* parent, const int32_t* len, const int32_t* term
   P.succ_tok = nb + 6 * n + 1;
   const int32_t* order = nb + 6 * n + 1 + n_succ;
   const int32_t* order_start = order + n_order;
+  const int32_t* kb_lo = order_start + n_order;
   P.kblk_minE = reinterpret_cast<int32_t*>(base + L.off_kmin);
   P.kblk_maxE = reinterpret_cast<int32_t*>(base + L.off_kmax);
   P.fwd_cnt = reinterpret_cast<int32_t*>(base + L.off_fcnt);
@@ -350,7 +361,7 @@ tt_status tt_pack(const int32_t* parent, const int32_t* len, const int32_t* term
   P.n_succ = n_succ;
   P.max_succ = 0;
   for (int32_t u = 0; u < n; ++u) P.max_succ = std::max(P.max_succ, H.succ_ptr[u + 1] - H.succ_ptr[u]);
-  s = launch_pack_fill(P, order, order_start, n_order, const_cast<int32_t*>(P.pos), const_cast<int32_t*>(P.w),
+  s = launch_pack_fill(P, order, order_start, n_order, kb_lo, const_cast<int32_t*>(P.pos), const_cast<int32_t*>(P.w),
                        const_cast<int32_t*>(P.E), const_cast<int32_t*>(P.node), const_cast<int32_t*>(P.kblk_minE),
                        const_cast<int32_t*>(P.kblk_maxE), const_cast<int32_t*>(P.fwd_cnt),
                        const_cast<int32_t*>(P.fwd_list), st);
