@@ -706,15 +706,16 @@ def main():
             my_pairs = sum(j.info["n_pairs"] for j in jobs)
             my_rows = sum(j.info["n_tokens"] for j in jobs)
             result["attn_fwd_bwd_tflops"] = round(my_flops / (attn_ms * 1e-3) / 1e12, 2)
-            traffic, util = {}, {}
+            traffic, util, dens = {}, {}, {}
             prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
             if os.path.exists(prof):
                 try:
                     pj = json.load(open(prof))
                     traffic = pj.get(args.config, {})
                     util = pj.get("bf16_mma_ops_pct", {}).get(args.config, {})
+                    dens = pj.get("tile_density", {}).get(args.config, {})
                 except Exception:
-                    traffic, util = {}, {}
+                    traffic, util, dens = {}, {}, {}
             per_launch = "" if len(jobs) == 1 else f" (mean over the rank's {len(jobs)} launches)"
 
             def tensor_roof(name, kernel, fl_per_pair, ms, main_kernel):
@@ -726,11 +727,10 @@ def main():
                      "algorithmic": f"{fl_per_pair} d Hq A FLOPs per launch (A = ancestor pairs: only unmasked pairs)",
                      "ms": round(ms, 4)}
                 if raw is not None:
-                    # ncu's bf16 MMA-op utilisation counts every tile the kernel multiplies (masked
-                    # elements of partial tiles included); raw / effective = tile density
-                    eff_pct = 100.0 * ach / peaks["bf16"]
+                    # raw tensor-core utilisation from ncu (every multiplied tile element, masked ones
+                    # included) and the tile density = effective / raw FLOPs of the captured launch
                     r["ncu_bf16_mma_ops_pct"] = raw
-                    r["tile_density"] = round(eff_pct / raw, 3) if raw else None
+                    r["tile_density"] = dens.get(main_kernel)
                 return r
 
             cand = {"bwd": tensor_roof("bwd", "tt_attn_bwd (bwd_pre + tree_attn_bwd_sm100 + dq_convert)", 10,

@@ -114,6 +114,7 @@ struct BwdParams {
   int restore;
   int head_major;  // CTA order: 1 = all k-blocks of kv head 0, then head 1, ... (dQ rows of one
                    // head group stay L2-resident); 0 = heads fastest
+  int walk;  // query-tile walk (TT_BWD_WALK, dev A/B): bit 0 descending from maxE, bit 1 heads inner
   int dbg;  // development ablations (TT_DEBUG_BWD): 1 skip dQ reduce, 2 reuse Q/dO stage (no reload), 4 skip elementwise math
   float scale, scale_log2;
   const int32_t* E;
@@ -128,6 +129,15 @@ struct BwdParams {
   double* part_kv;  // nullable: [grid][2] fp64 partial sums of squares of this CTA's dV (0) / dK (1) rows
   const __nv_bfloat16* kmat;  // K [N, hkv, 128] (KTMEM: rows copied into TMEM by the drain warpgroup)
 };
+
+// work item `it` of a CTA -> (q head, first query row of the 64-row tile)
+__device__ __forceinline__ void bwd_item(const BwdParams& p, int it, int nq, int qt0, int hk, int& h, int& q0) {
+  const int w = dev_dbg(p.walk);
+  const int qi = (w & 2) ? it / p.g : it % nq;
+  const int hi = (w & 2) ? it % p.g : it / nq;
+  h = hk * p.g + hi;
+  q0 = ((w & 1) ? (qt0 + nq - 1 - qi) : (qt0 + qi)) * kBQ;
+}
 
 __global__ void __maxnreg__(kNWG == 4 ? 80 : 128)  // 22 warps: 6 per SMSP x 80 regs x 32 fit its 16K registers
     tree_attn_bwd_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
@@ -213,8 +223,8 @@ __global__ void __maxnreg__(kNWG == 4 ? 80 : 128)  // 22 warps: 6 per SMSP x 80 
       for (int it = 0; it < n_it; ++it) {
         const int s = it % kQStages;
         if (it >= kQStages) mbar_wait(&q_empty[s], ((it / kQStages) - 1) & 1);
-        const int h = hk * p.g + it / nq;
-        const int q0 = (qt0 + it % nq) * kBQ;
+        int h, q0;
+        bwd_item(p, it, nq, qt0, hk, h, q0);
         uint8_t* qd = smem + kOffQS + s * 2 * kQTile;
         uint8_t* st = smem + kOffStats + s * kStatBytes;
         if ((dev_dbg(p.dbg) & 2) && it >= kQStages) {
@@ -377,8 +387,8 @@ __global__ void __maxnreg__(kNWG == 4 ? 80 : 128)  // 22 warps: 6 per SMSP x 80 
       mbar_arrive(k_tmem);
     }
     for (int it = 0; it < n_it; ++it) {
-      const int h = hk * p.g + it / nq;
-      const int q0 = (qt0 + it % nq) * kBQ;
+      int h, q0;
+      bwd_item(p, it, nq, qt0, hk, h, q0);
       { long long t0 = TT_CLK(); mbar_wait(&dq_full[0], it & 1); c_wd += TT_CLK() - t0; }
       long long t_dr = TT_CLK();
       tc_fence_after();
@@ -446,7 +456,8 @@ __global__ void __maxnreg__(kNWG == 4 ? 80 : 128)  // 22 warps: 6 per SMSP x 80 
     long long c_ws = 0, c_el = 0, c_ld = 0, c_math = 0, c_st = 0;
     for (int it = 0; it < n_it; ++it) {
       const int s = it % kQStages, b = it & 1;
-      const int q0 = (qt0 + it % nq) * kBQ;
+      int h_unused, q0;
+      bwd_item(p, it, nq, qt0, hk, h_unused, q0);
       const int sb = kKT ? 0 : b;
       { long long t0 = TT_CLK(); mbar_wait(&s_full[sb], kKT ? (it & 1) : ((it >> 1) & 1)); c_ws += TT_CLK() - t0; }
       tc_fence_after();
@@ -732,6 +743,8 @@ tt_status sm100_attn_bwd(const tt_packed& pk, const void* q, const void* k, cons
     const char* e = dev_getenv("TT_DEBUG_BWD");
     prm.dbg = e ? atoi(e) : 0;
     const char* o = dev_getenv("TT_CTA_ORDER");  // development A/B: bit 1 = bwd head-major
+    const char* wk = dev_getenv("TT_BWD_WALK");
+    prm.walk = wk ? atoi(wk) : 0;
     prm.head_major = o ? ((atoi(o) >> 1) & 1) : 0;  // measured: head-major loses the global heavy-first order (8K -10%, wide -12%)
   }
   prm.scale = scale;
