@@ -114,6 +114,7 @@ struct BwdParams {
   int restore;
   int head_major;  // CTA order: 1 = all k-blocks of kv head 0, then head 1, ... (dQ rows of one
                    // head group stay L2-resident); 0 = heads fastest
+  int wait;  // dev A/B (TT_WAIT_HINT): suspend-hint waits, bit 0 producer, 1 consumers, 2 epilogue
   int walk;  // query-tile walk (TT_BWD_WALK, dev A/B): bit 0 descending from maxE, bit 1 heads inner
   int dbg;  // development ablations (TT_DEBUG_BWD): 1 skip dQ reduce, 2 reuse Q/dO stage (no reload), 4 skip elementwise math
   float scale, scale_log2;
@@ -222,7 +223,7 @@ __global__ void __maxnreg__(kNWG == 4 ? 80 : 128)  // 22 warps: 6 per SMSP x 80 
     if (lane == 0) {
       for (int it = 0; it < n_it; ++it) {
         const int s = it % kQStages;
-        if (it >= kQStages) mbar_wait(&q_empty[s], ((it / kQStages) - 1) & 1);
+        if (it >= kQStages) mbar_wait_role(&q_empty[s], ((it / kQStages) - 1) & 1, dev_dbg(p.wait) & 1);
         int h, q0;
         bwd_item(p, it, nq, qt0, hk, h, q0);
         uint8_t* qd = smem + kOffQS + s * 2 * kQTile;
@@ -389,7 +390,7 @@ __global__ void __maxnreg__(kNWG == 4 ? 80 : 128)  // 22 warps: 6 per SMSP x 80 
     for (int it = 0; it < n_it; ++it) {
       int h, q0;
       bwd_item(p, it, nq, qt0, hk, h, q0);
-      { long long t0 = TT_CLK(); mbar_wait(&dq_full[0], it & 1); c_wd += TT_CLK() - t0; }
+      { long long t0 = TT_CLK(); mbar_wait_role(&dq_full[0], it & 1, dev_dbg(p.wait) & 2); c_wd += TT_CLK() - t0; }
       long long t_dr = TT_CLK();
       tc_fence_after();
       uint32_t v0[32], v1[32];
@@ -459,7 +460,7 @@ __global__ void __maxnreg__(kNWG == 4 ? 80 : 128)  // 22 warps: 6 per SMSP x 80 
       int h_unused, q0;
       bwd_item(p, it, nq, qt0, hk, h_unused, q0);
       const int sb = kKT ? 0 : b;
-      { long long t0 = TT_CLK(); mbar_wait(&s_full[sb], kKT ? (it & 1) : ((it >> 1) & 1)); c_ws += TT_CLK() - t0; }
+      { long long t0 = TT_CLK(); mbar_wait_role(&s_full[sb], kKT ? (it & 1) : ((it >> 1) & 1), dev_dbg(p.wait) & 2); c_ws += TT_CLK() - t0; }
       tc_fence_after();
       long long t_el = TT_CLK();
       if (dev_dbg(p.dbg) & 4) {
@@ -534,7 +535,7 @@ __global__ void __maxnreg__(kNWG == 4 ? 80 : 128)  // 22 warps: 6 per SMSP x 80 
         {
           uint32_t pv[kCW], dsk[kCW / 2];
           long long tA = TT_CLK();
-          { long long t0 = TT_CLK(); mbar_wait(dp_full, it & 1); c_ws += TT_CLK() - t0; }
+          { long long t0 = TT_CLK(); mbar_wait_role(dp_full, it & 1, dev_dbg(p.wait) & 2); c_ws += TT_CLK() - t0; }
           tc_fence_after();
           if constexpr (kCW == 32)
             tmem_ld32(tl + kColP + kCW * wg, *reinterpret_cast<uint32_t(*)[32]>(&pv[0]));
@@ -576,7 +577,7 @@ __global__ void __maxnreg__(kNWG == 4 ? 80 : 128)  // 22 warps: 6 per SMSP x 80 
     }
     // ---- epilogue: the first kNWG/2 warpgroups write dV, the others dK (scaled), each its share of
     //      this key row's 128 head dims ----
-    mbar_wait(acc_done, 0);
+    mbar_wait_role(acc_done, 0, dev_dbg(p.wait) & 4);
     tc_fence_after();
     {
       constexpr int kPer = kNWG / 2;              // warpgroups per tensor
@@ -745,6 +746,8 @@ tt_status sm100_attn_bwd(const tt_packed& pk, const void* q, const void* k, cons
     const char* o = dev_getenv("TT_CTA_ORDER");  // development A/B: bit 1 = bwd head-major
     const char* wk = dev_getenv("TT_BWD_WALK");
     prm.walk = wk ? atoi(wk) : 0;
+    const char* wh = dev_getenv("TT_WAIT_HINT");
+    prm.wait = wh ? atoi(wh) : 0;
     prm.head_major = o ? ((atoi(o) >> 1) & 1) : 0;  // measured: head-major loses the global heavy-first order (8K -10%, wide -12%)
   }
   prm.scale = scale;

@@ -62,6 +62,7 @@ struct FwdParams {
   float scale_log2;
   int head_major;  // CTA order: 1 = kv-head groups outermost (K/V of one group L2-resident)
   int dbg;
+  int wait;  // dev A/B (TT_WAIT_HINT): suspend-hint waits, bit 0 producer, 1 softmax, 2 epilogue
   const int32_t* E;
   const int32_t* fwd_cnt;
   const int32_t* fwd_list;
@@ -167,7 +168,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       // ===================== TMA producer (Q and k-tile 0 already issued above) =====================
       for (int t = 1; t < T; ++t) {
         const int s = t % kStages;
-        if (t >= kStages) mbar_wait(&empty[s], ((t / kStages) - 1) & 1);
+        if (t >= kStages) mbar_wait_role(&empty[s], ((t / kStages) - 1) & 1, dev_dbg(p.wait) & 1);
         const int kb = tiles[t] & kKbMask;
         uint8_t* kd = smem + kOffKV + s * 2 * kTileBytes;
         mbar_expect_tx(&full[s], 2 * kTileBytes + 512);
@@ -274,7 +275,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         if (!cls) continue;
         const int kb = e & kKbMask;
         const int64_t j0 = (int64_t)kb * 128 + 64 * hf;  // first key of this half
-        { const long long t0 = TT_CLK(); mbar_wait(&s_full[i], sph); c_ws += TT_CLK() - t0; }
+        { const long long t0 = TT_CLK(); mbar_wait_role(&s_full[i], sph, dev_dbg(p.wait) & 2); c_ws += TT_CLK() - t0; }
         const long long t_cmp = TT_CLK();
         sph ^= 1;
         tc_fence_after();
@@ -394,7 +395,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         first = false;
       }
       // ---- epilogue: O / l -> bf16 (this half's 64 columns), LSE (half 0) ----
-      mbar_wait(&o_full[i], 0);
+      mbar_wait_role(&o_full[i], 0, dev_dbg(p.wait) & 4);
       tc_fence_after();
       xl[(i * 2 + hf) * 128 + r] = l;
       named_bar_sync(1 + i, 256);
@@ -506,6 +507,8 @@ tt_status sm100_attn_fwd(const tt_packed& pk, const void* q, const void* k, cons
     prm.dbg = e ? atoi(e) : 0;
     const char* o = dev_getenv("TT_CTA_ORDER");  // development A/B: bit 0 = fwd head-major
     prm.head_major = o ? (atoi(o) & 1) : 0;
+    const char* wh = dev_getenv("TT_WAIT_HINT");
+    prm.wait = wh ? atoi(wh) : 0;
   }
   prm.E = pk.E;
   prm.fwd_cnt = pk.fwd_cnt;

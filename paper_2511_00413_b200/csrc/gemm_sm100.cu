@@ -43,6 +43,7 @@ constexpr uint32_t kOffBar = kStages * kStageBytes;   // 192 KB of stages
 constexpr uint32_t kSmemBytes = kOffBar + 256;
 static_assert(kSmemBytes <= 232448, "GEMM exceeds 227 KB of shared memory");
 constexpr uint32_t kPeerMask = 0xFEFFFFFFu;           // shared::cluster address -> the leader CTA's copy
+constexpr int kGemmWaitDefault = 0;
 
 struct Args {
   int M, N, K;
@@ -62,7 +63,16 @@ struct Args {
   const float* lse2;       // [M] log2-domain lse (kEpiDlogits)
   const float* g_omega;    // [M] gamma * Omega (0 for rows without a prediction)
   float gamma;
+  int wait_mode;           // dev A/B (TT_GEMM_WAIT): 0 spin try_wait, 1 suspend-time hint, 2 nanosleep back-off
 };
+
+// barrier wait of the long-waiting roles (epilogue for the accumulator, producer for a free stage)
+__device__ __forceinline__ void wait_long(const Args& p, uint64_t* bar, uint32_t parity) {
+  const int m = kDevBuild ? p.wait_mode : kGemmWaitDefault;
+  if (m == 1) mbar_wait_hint(bar, parity, 20000);
+  else if (m == 2) mbar_wait_sleep(bar, parity);
+  else mbar_wait(bar, parity);
+}
 
 __device__ __forceinline__ uint32_t cta_rank() {
   uint32_t r;
@@ -163,7 +173,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int m0 = tm * 256 + 128 * (int)rank, n0 = tn * 256 + 128 * (int)rank;
         for (int kb = 0; kb < nk; ++kb, ++it) {
           const int s = it % kStages;
-          if (it >= kStages) mbar_wait(&empty[s], ((it / kStages) - 1) & 1);
+          if (it >= kStages) wait_long(p, &empty[s], ((it / kStages) - 1) & 1);
           if (leader) expect_tx(&full[s], 2 * kStageBytes);
           const uint32_t fb = smem_u32(&full[s]) & kPeerMask;
           const uint32_t a_dst = sbase + s * kStageBytes, b_dst = a_dst + kHalfBytes;
@@ -230,7 +240,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int row = tm * 256 + 128 * (int)rank + rl;
       const int c_base = tn * 256 + 128 * half;          // first column of this thread's 128
       const bool rv = row < p.M;
-      mbar_wait(&acc_full[b], (tc >> 1) & 1);
+      wait_long(p, &acc_full[b], (tc >> 1) & 1);
       tc_fence_after();
       float m_run = -INFINITY, s_run = 0.f;
       int nt = 0;
@@ -447,6 +457,8 @@ tt_status gemm_run(int epi, int M, int N, int K, const void* A, int64_t lda, int
   a.col_offset = ep.col_offset; a.vocab = ep.vocab; a.part = reinterpret_cast<float2*>(ep.part);
   a.max_t = ep.max_t; a.tgt_cnt = ep.tgt_cnt; a.tgt_y = ep.tgt_y; a.tgt_w = ep.tgt_w; a.tgt_x = ep.tgt_x;
   a.lse2 = ep.lse2; a.g_omega = ep.g_omega; a.gamma = ep.gamma;
+  a.wait_mode = 0;
+  if (const char* w = dev_getenv("TT_GEMM_WAIT")) a.wait_mode = atoi(w);
   switch (epi) {
     case kEpiStoreBF16: return launch<kEpiStoreBF16>(ma, mb, a, st);
     case kEpiAccF32: return launch<kEpiAccF32>(ma, mb, a, st);

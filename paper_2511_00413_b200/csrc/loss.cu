@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <unordered_map>
+#include <utility>
 #include <cstdlib>
 
 #include <cuda_fp16.h>
@@ -1064,6 +1065,22 @@ size_t lc_smem(int Cq, int max_t) {
 struct SideStream {
   cudaStream_t s = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr;
+  SideStream() = default;
+  SideStream(const SideStream&) = delete;
+  SideStream& operator=(const SideStream&) = delete;
+  SideStream(SideStream&& o) noexcept : s(o.s), fork(o.fork), join(o.join) { o.s = nullptr; o.fork = o.join = nullptr; }
+  SideStream& operator=(SideStream&& o) noexcept {
+    std::swap(s, o.s); std::swap(fork, o.fork); std::swap(join, o.join);
+    return *this;
+  }
+  ~SideStream() {
+    // thread exit: release the side stream and its events (work still queued on them completes
+    // first: cudaStreamDestroy / cudaEventDestroy defer the release; errors at teardown ignored)
+    if (join) cudaEventDestroy(join);
+    if (fork) cudaEventDestroy(fork);
+    if (s) cudaStreamDestroy(s);
+    cudaGetLastError();
+  }
 };
 SideStream* side_stream(cudaStream_t st) {
   thread_local std::unordered_map<int, SideStream> per_dev;
@@ -1082,7 +1099,7 @@ SideStream* side_stream(cudaStream_t st) {
         cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming) != cudaSuccess) {
       cudaGetLastError();
-      ss = SideStream{};
+      ss = SideStream{};  // the moved-from temporary releases whatever was created
       return nullptr;
     }
   }

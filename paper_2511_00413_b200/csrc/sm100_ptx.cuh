@@ -40,6 +40,40 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// Wait with a suspend-time hint: the thread is descheduled (up to ~hint ns) instead of re-issuing
+// the try_wait, so idle warps stop burning issue slots and power while the barrier is pending.
+__device__ __forceinline__ void mbar_wait_hint(uint64_t* bar, uint32_t parity, uint32_t hint_ns) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAITH_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "@!p bra WAITH_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(hint_ns)
+      : "memory");
+}
+// Role-dependent wait: `hint` != 0 selects the suspend-hint form (development A/B of idle-warp power)
+__device__ __forceinline__ void mbar_wait_role(uint64_t* bar, uint32_t parity, int hint) {
+  if (hint) mbar_wait_hint(bar, parity, 20000);
+  else mbar_wait(bar, parity);
+}
+// Wait with exponential __nanosleep back-off between polls (for warps that wait a long time).
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  uint32_t ns = 32;
+  while (true) {
+    uint32_t ok;
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (ok) return;
+    __nanosleep(ns);
+    ns = ns < 1024 ? 2 * ns : ns;
+  }
+}
+
 // ------------------------------------------------------------------------------ TMA
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap* m) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(m) : "memory");
