@@ -862,14 +862,48 @@ def main():
             tokl = torch.randint(0, VOCAB, (Nl,), device="cuda", dtype=torch.int32, generator=g2)
             wsl = torch.empty(tt.tt_lmhead_loss_workspace(pkl, D_h, VOCAB, vc), dtype=torch.uint8, device="cuda")
             dHl, dWl = torch.empty_like(Hh), torch.empty_like(Wl)
+            # measured from an idle GPU (3 s cool-down after the timed step and the other legs, which
+            # leave the board at its power cap), SM clocks sampled during the leg
+            torch.cuda.synchronize()
+            time.sleep(3.0)
+            smp = ClockSampler(local)
+            smp.start()
             lm_ms = _t(lambda: tt.tt_lmhead_loss(pkl, Hh, Wl, tokl, vocab_chunk=vc, dh=dHl, dw=dWl, ws=wsl), reps=3)
+            # context: one vocabulary chunk's four contractions on the library GEMM vs cuBLAS (torch.matmul)
+            Wc = Wl[:vc]
+            Gc = torch.randn(Nl, vc, device="cuda", generator=g2).to(torch.bfloat16)
+            Xc = torch.empty(Nl, vc, device="cuda", dtype=torch.bfloat16)
+            dHa = torch.zeros(Nl, D_h, device="cuda", dtype=torch.float32)
+            dWc = torch.empty(vc, D_h, device="cuda", dtype=torch.bfloat16)
+            dHb = torch.empty(Nl, D_h, device="cuda", dtype=torch.bfloat16)
+
+            def mine():
+                tt.tt_gemm(Hh, Wc, out=Xc)
+                tt.tt_gemm(Hh, Wc, out=Xc)
+                tt.tt_gemm(Gc, Wc, b_mn=True, out=dHa, accumulate=True)
+                tt.tt_gemm(Gc, Hh, a_mn=True, b_mn=True, out=dWc)
+
+            def cublas():
+                torch.matmul(Hh, Wc.t(), out=Xc)
+                torch.matmul(Hh, Wc.t(), out=Xc)
+                torch.matmul(Gc, Wc, out=dHb)
+                torch.matmul(Gc.t(), Hh, out=dWc)
+
+            cfl = 8.0 * Nl * vc * D_h
+            g_ms, c_ms = _t(mine, reps=3), _t(cublas, reps=3)
+            lclk = smp.stop()
             fl = 8.0 * Nl * VOCAB * D_h
             out["next_f3_lmhead"] = {"ms": round(lm_ms, 3), "rows": Nl, "hidden": D_h, "vocab": VOCAB, "vocab_chunk": vc,
                                      "achieved_tflops": round(fl / lm_ms / 1e9, 1), "peak_tflops": peaks["bf16"],
                                      "frac": round(fl / lm_ms / 1e9 / peaks["bf16"], 4),
                                      "algorithmic": "8 N V D FLOPs (logits twice, dH, dW)", "l2": "flushed before every repetition",
+                                     "gemm": "the library's tcgen05 CTA-pair GEMM (tt_gemm), CE fused into its epilogues",
+                                     "chunk_gemms_tflops": {"tt_gemm": round(cfl / g_ms / 1e9, 1), "cublas": round(cfl / c_ms / 1e9, 1),
+                                                            "note": "one chunk's X_c (twice), dH, dW_c: library GEMM vs torch.matmul"},
+                                     "clocks": lclk, "cool_down_s": 3.0,
                                      "workspace_bytes": int(wsl.numel()),
                                      "materialised_logits_bytes_avoided": int(2 * 2 * Nl * VOCAB)}
+            del Gc, Xc, dHa, dWc, dHb
             del Hh, Wl, dHl, dWl, wsl
     if rank == 0 and not args.no_extras:
         run_leg(out, "next", leg_next)
