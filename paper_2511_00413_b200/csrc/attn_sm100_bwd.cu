@@ -101,9 +101,17 @@ static_assert(kSmemBytes <= 232448, "backward kernel exceeds 227 KB of shared me
 #define TT_BWD_KTMEM 1
 #endif
 constexpr bool kKT = TT_BWD_KTMEM != 0;
+// TT_BWD_VTMEM (requires KTMEM): V resident in TMEM too (dP^T = V dO^T as a TS MMA: the 32 KB per tile
+// of V reads from shared memory disappear) and dQ^T accumulates in the dP^T columns once the element-wise
+// warps have read dP^T; dP^T(i+1) is issued after the drain has read dQ^T(i).
+#ifndef TT_BWD_VTMEM
+#define TT_BWD_VTMEM 1
+#endif
+constexpr bool kVT = kKT && TT_BWD_VTMEM != 0;
 // TMEM columns: dV 0-127 | dK 128-255 | S^T 256-319 (KTMEM) or S^T x2 256-383 | K 320-383 (KTMEM) |
-// dP^T 384-447 | dQ^T 448-511
-constexpr uint32_t kColDV = 0, kColDK = 128, kColS = 256, kColK = 320, kColP = 384, kColQ = 448;
+// dP^T 384-447 (VTMEM: dP^T, then dQ^T) | dQ^T 448-511 (VTMEM: V)
+constexpr uint32_t kColDV = 0, kColDK = 128, kColS = 256, kColK = 320, kColP = 384;
+constexpr uint32_t kColQ = kVT ? kColP : 448, kColV = 448;
 
 // development instrumentation (TT_DEBUG_BWD & 8): per-role cycle counters summed over CTAs
 __device__ unsigned long long g_bwd_dbg[16];
@@ -129,13 +137,22 @@ struct BwdParams {
   __nv_bfloat16* dv;
   double* part_kv;  // nullable: [grid][2] fp64 partial sums of squares of this CTA's dV (0) / dK (1) rows
   const __nv_bfloat16* kmat;  // K [N, hkv, 128] (KTMEM: rows copied into TMEM by the drain warpgroup)
+  const __nv_bfloat16* vmat;  // V [N, hkv, 128] (VTMEM: likewise)
 };
 
-// work item `it` of a CTA -> (q head, first query row of the 64-row tile)
-__device__ __forceinline__ void bwd_item(const BwdParams& p, int it, int nq, int qt0, int hk, int& h, int& q0) {
+// work item `it` of a CTA -> (q head, first query row of the 64-row tile).  The shipped walk (GQA heads
+// outer, query tiles ascending) advances a (tile, head) counter pair: no integer division per tile.
+struct Walk {
+  int qi = 0, hi = 0;
+};
+__device__ __forceinline__ void bwd_item(const BwdParams& p, int it, Walk& wk, int nq, int qt0, int hk, int& h, int& q0) {
   const int w = dev_dbg(p.walk);
-  const int qi = (w & 2) ? it / p.g : it % nq;
-  const int hi = (w & 2) ? it % p.g : it / nq;
+  int qi = wk.qi, hi = wk.hi;
+  if (w) {
+    qi = (w & 2) ? it / p.g : it % nq;
+    hi = (w & 2) ? it % p.g : it / nq;
+  }
+  if (++wk.qi == nq) { wk.qi = 0; ++wk.hi; }
   h = hk * p.g + hi;
   q0 = ((w & 1) ? (qt0 + nq - 1 - qi) : (qt0 + qi)) * kBQ;
 }
@@ -214,18 +231,19 @@ __global__ void __maxnreg__(kNWG == 4 ? 80 : 128)  // 22 warps: 6 per SMSP x 80 
       tma_prefetch(&tmK);
       tma_prefetch(&tmV);
       tma_prefetch(&tmdO);
-      mbar_expect_tx(kv_full, 2 * kKVTile);
+      mbar_expect_tx(kv_full, (kVT ? 1 : 2) * kKVTile);
       for (int c = 0; c < 2; ++c) {
         tma_load_3d(smem + kOffK + c * kKVChunk, &tmK, kv_full, c * 64, hk, (int)k0);
-        tma_load_3d(smem + kOffV + c * kKVChunk, &tmV, kv_full, c * 64, hk, (int)k0);
+        if (!kVT) tma_load_3d(smem + kOffV + c * kKVChunk, &tmV, kv_full, c * 64, hk, (int)k0);
       }
     }
     if (lane == 0) {
+      Walk wk;
       for (int it = 0; it < n_it; ++it) {
         const int s = it % kQStages;
         if (it >= kQStages) mbar_wait_role(&q_empty[s], ((it / kQStages) - 1) & 1, dev_dbg(p.wait) & 1);
         int h, q0;
-        bwd_item(p, it, nq, qt0, hk, h, q0);
+        bwd_item(p, it, wk, nq, qt0, hk, h, q0);
         uint8_t* qd = smem + kOffQS + s * 2 * kQTile;
         uint8_t* st = smem + kOffStats + s * kStatBytes;
         if ((dev_dbg(p.dbg) & 2) && it >= kQStages) {
@@ -273,8 +291,25 @@ __global__ void __maxnreg__(kNWG == 4 ? 80 : 128)  // 22 warps: 6 per SMSP x 80 
         for (int kk = 0; kk < 8; ++kk) {
           const uint32_t offk = (kk >> 2) * kKVChunk + (kk & 3) * 32;
           const uint32_t offq = (kk >> 2) * kQChunk + (kk & 3) * 32;
-          mma_ss_w(tm + kColP, sdesc(vb_s + offk, 16, 1024), sdesc(ob + offq, 16, 1024), idSP, kk > 0);
+          if constexpr (kVT)
+            mma_ts_w(tm + kColP, tm + kColV + 8 * kk, sdesc(ob + offq, 16, 1024), idSP, kk > 0);
+          else
+            mma_ss_w(tm + kColP, sdesc(vb_s + offk, 16, 1024), sdesc(ob + offq, 16, 1024), idSP, kk > 0);
         }
+      };
+      // dQ^T = K^T dS^T   (A: K MN-major, LBO = 16 KB d-chunk; B: dS^T MN-major, one 64-wide group)
+      auto issue_dQ = [&](uint32_t dsb) {
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          mma_ss_w(tm + kColQ, sdesc(kb_s + kk * 2048, kKVChunk, 1024), sdesc(dsb + kk * 2048, kDSTile, 1024),
+                   idQ, kk > 0);
+      };
+      // dK += dS^T Q   (A: dS^T K-major 128 x 64 in smem; B: Q MN-major)
+      auto issue_dK = [&](uint32_t dsb, uint32_t qb, int it) {
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          mma_ss_w(tm + kColDK, sdesc(dsb + kk * 32, 16, 1024), sdesc(qb + kk * 2048, kQChunk, 1024), idVK,
+                   (it > 0 || kk > 0) ? 1u : 0u);
       };
       long long w_sm = 0, w_dq = 0, w_q = 0, t_start = TT_CLK();
       mbar_wait(kv_full, 0);
@@ -317,6 +352,23 @@ __global__ void __maxnreg__(kNWG == 4 ? 80 : 128)  // 22 warps: 6 per SMSP x 80 
           issue_SP(it + 1);
           mma_commit_w(&s_full[0]);
         }
+        if constexpr (kVT) {
+          // dS^T(it) ready (the warps have also read dP^T(it)): dQ^T(it) into the dP^T columns first (the
+          // drain reads it while dK(it) runs), then dP^T(it+1) once the drain has released the columns
+          { long long t0 = TT_CLK(); mbar_wait(&ds_ready[b], (it >> 1) & 1); w_sm += TT_CLK() - t0; }
+          tc_fence_after();
+          issue_dQ(dsb);
+          mma_commit_w(&dq_full[0]);
+          issue_dK(dsb, qb, it);
+          mma_commit_w(&q_empty[s]);
+          if (it + 1 < n_it) {
+            { long long t0 = TT_CLK(); mbar_wait(&dq_free[0], it & 1); w_dq += TT_CLK() - t0; }
+            tc_fence_after();
+            issue_dP(it + 1);
+            mma_commit_w(dp_full);
+          }
+          continue;
+        }
         // next tile's dP^T (single buffer) as soon as the warps have read dP^T(it)
         if (it + 1 < n_it) {
           { long long t0 = TT_CLK(); mbar_wait(dp_free, it & 1); w_sm += TT_CLK() - t0; }
@@ -326,20 +378,12 @@ __global__ void __maxnreg__(kNWG == 4 ? 80 : 128)  // 22 warps: 6 per SMSP x 80 
         }
         { long long t0 = TT_CLK(); mbar_wait(&ds_ready[b], (it >> 1) & 1); w_sm += TT_CLK() - t0; }
         tc_fence_after();
-        // dK += dS^T Q   (A: dS^T K-major 128 x 64 in smem; B: Q MN-major)
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-          mma_ss_w(tm + kColDK, sdesc(dsb + kk * 32, 16, 1024), sdesc(qb + kk * 2048, kQChunk, 1024), idVK,
-                 (it > 0 || kk > 0) ? 1u : 0u);
-        // dQ^T = K^T dS^T   (A: K MN-major, LBO = 16 KB d-chunk; B: dS^T MN-major, one 64-wide group)
+        issue_dK(dsb, qb, it);
         if (it > 0) {
           { long long t0 = TT_CLK(); mbar_wait(&dq_free[0], (it - 1) & 1); w_dq += TT_CLK() - t0; }
           tc_fence_after();
         }
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          mma_ss_w(tm + kColQ, sdesc(kb_s + kk * 2048, kKVChunk, 1024), sdesc(dsb + kk * 2048, kDSTile, 1024),
-                 idQ, kk > 0);
+        issue_dQ(dsb);
         mma_commit_w(&dq_full[0]);
         mma_commit_w(&q_empty[s]);
         // S^T(it+2) into S^T[b] (in issue order after dV(it) read P^T(it) from it)
@@ -383,13 +427,28 @@ __global__ void __maxnreg__(kNWG == 4 ? 80 : 128)  // 22 warps: 6 per SMSP x 80 
       }
       tmem_st32(tl + kColK, *reinterpret_cast<const uint32_t(*)[32]>(&kv[0]));
       tmem_st32(tl + kColK + 32, *reinterpret_cast<const uint32_t(*)[32]>(&kv[32]));
+      if constexpr (kVT) {
+        // V row (key k0 + r) -> TMEM lane r, columns kColV.. (A operand of the TS MMA dP^T = V dO^T)
+        tmem_wait_st();
+        if (jr < p.N) {
+          const uint4* src = reinterpret_cast<const uint4*>(p.vmat + (jr * p.hkv + hk) * kD);
+#pragma unroll
+          for (int u = 0; u < 16; ++u) {
+            const uint4 x = src[u];
+            kv[4 * u] = x.x; kv[4 * u + 1] = x.y; kv[4 * u + 2] = x.z; kv[4 * u + 3] = x.w;
+          }
+        }
+        tmem_st32(tl + kColV, *reinterpret_cast<const uint32_t(*)[32]>(&kv[0]));
+        tmem_st32(tl + kColV + 32, *reinterpret_cast<const uint32_t(*)[32]>(&kv[32]));
+      }
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(k_tmem);
     }
+    Walk wk;
     for (int it = 0; it < n_it; ++it) {
       int h, q0;
-      bwd_item(p, it, nq, qt0, hk, h, q0);
+      bwd_item(p, it, wk, nq, qt0, hk, h, q0);
       { long long t0 = TT_CLK(); mbar_wait_role(&dq_full[0], it & 1, dev_dbg(p.wait) & 2); c_wd += TT_CLK() - t0; }
       long long t_dr = TT_CLK();
       tc_fence_after();
@@ -455,10 +514,11 @@ __global__ void __maxnreg__(kNWG == 4 ? 80 : 128)  // 22 warps: 6 per SMSP x 80 
     const float sl2 = p.scale_log2;
     constexpr uint32_t kFull = kCW == 32 ? 0xffffffffu : ((1u << kCW) - 1u);
     long long c_ws = 0, c_el = 0, c_ld = 0, c_math = 0, c_st = 0;
+    Walk wk;
     for (int it = 0; it < n_it; ++it) {
       const int s = it % kQStages, b = it & 1;
       int h_unused, q0;
-      bwd_item(p, it, nq, qt0, hk, h_unused, q0);
+      bwd_item(p, it, wk, nq, qt0, hk, h_unused, q0);
       const int sb = kKT ? 0 : b;
       { long long t0 = TT_CLK(); mbar_wait_role(&s_full[sb], kKT ? (it & 1) : ((it >> 1) & 1), dev_dbg(p.wait) & 2); c_ws += TT_CLK() - t0; }
       tc_fence_after();
@@ -763,6 +823,7 @@ tt_status sm100_attn_bwd(const tt_packed& pk, const void* q, const void* k, cons
   prm.dv = static_cast<__nv_bfloat16*>(dv);
   prm.part_kv = sqnorm ? part_kv : nullptr;
   prm.kmat = static_cast<const __nv_bfloat16*>(k);
+  prm.vmat = static_cast<const __nv_bfloat16*>(v);
   cudaError_t e = cudaFuncSetAttribute(tree_attn_bwd_sm100, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
   if (e != cudaSuccess) { set_error("sm100_attn_bwd: smem attribute: %s", cudaGetErrorString(e)); return TT_ERR_CUDA; }
   const unsigned grid = (unsigned)pk.n_blk * hkv;

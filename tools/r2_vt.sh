@@ -1,0 +1,10 @@
+# V-in-TMEM backward A/B: parity subset on the shipped build (VTMEM=1), then timeall for VTMEM 1 vs 0
+set -u
+O=gpurun_out/${1:-r2vt}; mkdir -p $O
+python -m paper_2511_00413_b200.build --force > $O/build.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_attn.py tests/test_gpu_random_sweep.py tests/test_gpu_weights.py -m gpu -x -q > $O/pytest.log 2>&1; echo "exit $?" >> $O/pytest.log
+for r in 1 2; do echo "== VTMEM=1 run $r" >> $O/time.txt; timeout 300 python tools/timeall.py agentic8k deep32k batch64k >> $O/time.txt 2>&1; done
+TT_EXTRA_NVCC_FLAGS="-DTT_BWD_VTMEM=0" python -m paper_2511_00413_b200.build --dev --force > $O/build0.log 2>&1
+for r in 1 2; do echo "== VTMEM=0 run $r" >> $O/time.txt; timeout 300 python tools/timeall.py agentic8k deep32k batch64k >> $O/time.txt 2>&1; done
+python -m paper_2511_00413_b200.build --force > /dev/null 2>&1
+echo done >> $O/time.txt
