@@ -152,6 +152,13 @@ typedef struct {
   int32_t n_blk;
   int32_t n_succ;
   int32_t max_succ;            /* longest continuation list (tt_restore_loss supports <= 1024) */
+  /* host-computed schedule statistics of the backward's key-stationary walk (64-row query tiles per
+     128-key block: nq_kb = ceil(kblk_maxE[kb] / 64) - 2 kb): their sum and maximum.  The attention
+     kernels order their CTAs kv-head-major when the heaviest CTA is a small share of one SM's work
+     (better L2 locality under the power cap), heads-fastest otherwise (no late heavy tail). */
+  int64_t sched_sum_nq;
+  int32_t sched_max_nq;
+  int32_t reserved2;
 } tt_packed;
 
 /* Validate the forest and size the pack (HOST only, synchronous, no CUDA calls). */

@@ -1,4 +1,5 @@
-// attn_sm100.cu — device capability check for the sm_100a tensor-core attention path (bf16, d = 128).
+// attn_sm100.cu — device capability check for the sm_100a tensor-core attention path (bf16, d = 128)
+// and the CTA-order choice the forward and backward share.
 #include "tt_internal.cuh"
 
 namespace tt {
@@ -13,6 +14,18 @@ bool sm100_available() {
     cached = (major == 10 && minor == 0) ? 1 : 0;
   }
   return cached == 1;
+}
+
+bool head_major_order(const tt_packed& pk, int hkv) {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  if (pk.sched_sum_nq <= 0 || hkv <= 0) return false;
+  return (double)sms * pk.sched_max_nq < 0.3 * (double)hkv * (double)pk.sched_sum_nq;
 }
 
 }  // namespace tt

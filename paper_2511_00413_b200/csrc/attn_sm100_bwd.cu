@@ -120,11 +120,11 @@ struct BwdParams {
   int64_t N;
   int hq, hkv, g, nb;
   int restore;
-  int head_major;  // CTA order: 1 = all k-blocks of kv head 0, then head 1, ... (dQ rows of one
-                   // head group stay L2-resident); 0 = heads fastest
+  int chunk;  // CTA order: key blocks in chunks of `chunk`; within a chunk the kv heads outermost (1 = heads
+              // fastest, >= nb = head-major: the Q / dO / dQ rows of one head group stay L2-resident)
   int wait;  // dev A/B (TT_WAIT_HINT): suspend-hint waits, bit 0 producer, 1 consumers, 2 epilogue
   int walk;  // query-tile walk (TT_BWD_WALK, dev A/B): bit 0 descending from maxE, bit 1 heads inner
-  int dbg;  // development ablations (TT_DEBUG_BWD): 1 skip dQ reduce, 2 reuse Q/dO stage (no reload), 4 skip elementwise math
+  int dbg;  // development ablations (TT_DEBUG_BWD): 1 skip dQ reduce, 2 reuse Q/dO stage (no reload), 4 skip elementwise math, 32 stage dQ but skip the L2 reduce
   float scale, scale_log2;
   const int32_t* E;
   const int32_t* kmaxE;
@@ -183,8 +183,14 @@ __global__ void __maxnreg__(kNWG == 4 ? 80 : 128)  // 22 warps: 6 per SMSP x 80 
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long t_kernel0 = TT_CLK();
-  const int kb = p.head_major ? (int)(blockIdx.x % p.nb) : (int)(blockIdx.x / p.hkv);
-  const int hk = p.head_major ? (int)(blockIdx.x / p.nb) : (int)(blockIdx.x % p.hkv);
+  int kb, hk;
+  {
+    const int per = p.chunk * p.hkv, x = (int)blockIdx.x;
+    const int ch = x / per, w = x - ch * per;
+    const int len = min(p.chunk, p.nb - ch * p.chunk);
+    hk = w / len;
+    kb = ch * p.chunk + (w - hk * len);
+  }
   const int64_t k0 = (int64_t)kb * 128;
   const int qt0 = (int)(k0 / kBQ);                                    // first 64-row query tile
   const int qt1 = (int)((p.kmaxE[kb] + kBQ - 1) / kBQ);                // exclusive
@@ -487,7 +493,7 @@ __global__ void __maxnreg__(kNWG == 4 ? 80 : 128)  // 22 warps: 6 per SMSP x 80 
         fence_proxy_async_smem();
         named_bar_sync(1, 128);
         if (r == 0) {
-          tma_reduce_add_3d(&tmdQ, stg, 0, h, q0 + 32 * hh);
+          if (!(dev_dbg(p.dbg) & 32)) tma_reduce_add_3d(&tmdQ, stg, 0, h, q0 + 32 * hh);  // dbg 32: staging only
           bulk_commit();
         }
       }
@@ -808,7 +814,9 @@ tt_status sm100_attn_bwd(const tt_packed& pk, const void* q, const void* k, cons
     prm.walk = wk ? atoi(wk) : 0;
     const char* wh = dev_getenv("TT_WAIT_HINT");
     prm.wait = wh ? atoi(wh) : 0;
-    prm.head_major = o ? ((atoi(o) >> 1) & 1) : 0;  // measured: head-major loses the global heavy-first order (8K -10%, wide -12%)
+    prm.chunk = bwd_cta_chunk(pk, hkv);
+    if (o && ((atoi(o) >> 1) & 1)) prm.chunk = pk.n_blk;  // development A/B: head-major
+    if (const char* c = dev_getenv("TT_BWD_CHUNK")) prm.chunk = atoi(c) > 0 ? atoi(c) : 1;
   }
   prm.scale = scale;
   prm.scale_log2 = scale * kLog2e;

@@ -60,7 +60,8 @@ struct FwdParams {
   int64_t N;
   int hq, hkv, nb, npairs;
   float scale_log2;
-  int head_major;  // CTA order: 1 = kv-head groups outermost (K/V of one group L2-resident)
+  int chunk;  // CTA order: query-block pairs (heaviest first) in chunks of `chunk`; within a chunk the kv
+              // heads outermost (1 = heads fastest, >= npairs = head-major: K/V of one group L2-resident)
   int dbg;
   int wait;  // dev A/B (TT_WAIT_HINT): suspend-hint waits, bit 0 producer, 1 softmax, 2 epilogue
   const int32_t* E;
@@ -95,10 +96,15 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   const long long t_kernel0 = TT_CLK();
   // heavy (late) query blocks first; the q heads of one kv head adjacent
   const int gq = p.hq / p.hkv;
-  const int pair = p.head_major ? p.npairs - 1 - (int)((blockIdx.x % (p.npairs * gq)) / gq)
-                                : p.npairs - 1 - (int)(blockIdx.x / p.hq);
-  const int h = p.head_major ? (int)(blockIdx.x / (p.npairs * gq)) * gq + (int)(blockIdx.x % gq)
-                             : (int)(blockIdx.x % p.hq);
+  int pair, h;
+  {
+    const int per = p.chunk * p.hq, x = (int)blockIdx.x;
+    const int ch = x / per, w = x - ch * per;
+    const int len = min(p.chunk, p.npairs - ch * p.chunk);
+    const int hkk = w / (len * gq), w2 = w - hkk * (len * gq);
+    pair = p.npairs - 1 - (ch * p.chunk + w2 / gq);
+    h = hkk * gq + w2 % gq;
+  }
   const int hk = h / (p.hq / p.hkv);
   const int qa = 2 * pair;
   const bool has1 = qa + 1 < p.nb && !(dev_dbg(p.dbg) & 16);  // dbg 16: development ablation, drop query tile 1
@@ -506,7 +512,9 @@ tt_status sm100_attn_fwd(const tt_packed& pk, const void* q, const void* k, cons
     const char* e = dev_getenv("TT_DEBUG_FWD");
     prm.dbg = e ? atoi(e) : 0;
     const char* o = dev_getenv("TT_CTA_ORDER");  // development A/B: bit 0 = fwd head-major
-    prm.head_major = o ? (atoi(o) & 1) : 0;
+    prm.chunk = fwd_cta_chunk(pk, prm.npairs, hkv);
+    if (o && (atoi(o) & 1)) prm.chunk = prm.npairs;  // development A/B: head-major
+    if (const char* c = dev_getenv("TT_FWD_CHUNK")) prm.chunk = atoi(c) > 0 ? atoi(c) : 1;
     const char* wh = dev_getenv("TT_WAIT_HINT");
     prm.wait = wh ? atoi(wh) : 0;
   }

@@ -361,6 +361,23 @@ tt_status tt_pack(const int32_t* parent, const int32_t* len, const int32_t* term
   P.n_succ = n_succ;
   P.max_succ = 0;
   for (int32_t u = 0; u < n; ++u) P.max_succ = std::max(P.max_succ, H.succ_ptr[u + 1] - H.succ_ptr[u]);
+  {
+    // per 128-key block the largest subtree end of the nodes it holds (= kblk_maxE, which the device
+    // also writes), then the backward's per-block query-tile counts (CTA-order statistics)
+    std::vector<int32_t> bmax(L.nb, 0);
+    for (int32_t u : H.order) {
+      const int32_t b0 = H.start[u] / kBlock, b1 = (H.start[u] + H.len[u] - 1) / kBlock;
+      for (int32_t b = b0; b <= b1; ++b) bmax[b] = std::max(bmax[b], H.sub_end[u]);
+    }
+    P.sched_sum_nq = 0;
+    P.sched_max_nq = 0;
+    for (int32_t b = 0; b < L.nb; ++b) {
+      const int32_t nq = (bmax[b] + 63) / 64 - 2 * b;
+      P.sched_sum_nq += nq;
+      P.sched_max_nq = std::max(P.sched_max_nq, nq);
+    }
+    P.reserved2 = 0;
+  }
   s = launch_pack_fill(P, order, order_start, n_order, kb_lo, const_cast<int32_t*>(P.pos), const_cast<int32_t*>(P.w),
                        const_cast<int32_t*>(P.E), const_cast<int32_t*>(P.node), const_cast<int32_t*>(P.kblk_minE),
                        const_cast<int32_t*>(P.kblk_maxE), const_cast<int32_t*>(P.fwd_cnt),

@@ -127,4 +127,14 @@ tt_status launch_restore_grad(const tt_packed& pk, void* g, tt_dtype dt, int64_t
 
 constexpr int kSqnormBlocks = 296;
 
+// CTA orders of the attention kernels (chunk = consecutive query-block pairs / key blocks whose CTAs are
+// ordered kv-head-major; 1 = heads fastest).  Measured under the power cap (profiles/r2d_cta_chunk.txt):
+// head-major (one chunk) is 1-2% faster on the deep / 64K trees (the Q / dO / dQ or K / V rows of one
+// head group stay L2-resident: the backward runs 80 MHz higher at the same power) and 5-8% slower on the
+// 8K and wide trees (their heaviest CTAs would start late).  Head-major when the heaviest backward CTA
+// is under 30% of one SM's share of the work: sms * max_nq / (hkv * sum_nq) < 0.3.
+bool head_major_order(const tt_packed& pk, int hkv);
+inline int fwd_cta_chunk(const tt_packed& pk, int npairs, int hkv) { return head_major_order(pk, hkv) ? npairs : 1; }
+inline int bwd_cta_chunk(const tt_packed& pk, int hkv) { return head_major_order(pk, hkv) ? pk.n_blk : 1; }
+
 }  // namespace tt
