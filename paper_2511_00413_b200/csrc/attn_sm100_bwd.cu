@@ -123,6 +123,7 @@ struct BwdParams {
   int chunk;  // CTA order: key blocks in chunks of `chunk`; within a chunk the kv heads outermost (1 = heads
               // fastest, >= nb = head-major: the Q / dO / dQ rows of one head group stay L2-resident)
   int wait;  // dev A/B (TT_WAIT_HINT): suspend-hint waits, bit 0 producer, 1 consumers, 2 epilogue
+  int l2hint;  // dev A/B (TT_BWD_L2HINT): bit 0/1 dQ reduce evict_last / evict_first, bit 2/3 Q / dO loads evict_last / evict_first
   int walk;  // query-tile walk (TT_BWD_WALK, dev A/B): bit 0 descending from maxE, bit 1 heads inner
   int dbg;  // development ablations (TT_DEBUG_BWD): 1 skip dQ reduce, 2 reuse Q/dO stage (no reload), 4 skip elementwise math, 32 stage dQ but skip the L2 reduce
   float scale, scale_log2;
@@ -257,9 +258,17 @@ __global__ void __maxnreg__(kNWG == 4 ? 80 : 128)  // 22 warps: 6 per SMSP x 80 
           continue;
         }
         mbar_expect_tx(&q_full[s], 2 * kQTile + 3 * 256);
-        for (int c = 0; c < 2; ++c) {
-          tma_load_3d(qd + c * kQChunk, &tmQ, &q_full[s], c * 64, h, q0);
-          tma_load_3d(qd + kQTile + c * kQChunk, &tmdO, &q_full[s], c * 64, h, q0);
+        if (dev_dbg(p.l2hint) & 12) {
+          const uint64_t pol = (dev_dbg(p.l2hint) & 4) ? policy_evict_last() : policy_evict_first();
+          for (int c = 0; c < 2; ++c) {
+            tma_load_3d_hint(qd + c * kQChunk, &tmQ, &q_full[s], c * 64, h, q0, pol);
+            tma_load_3d_hint(qd + kQTile + c * kQChunk, &tmdO, &q_full[s], c * 64, h, q0, pol);
+          }
+        } else {
+          for (int c = 0; c < 2; ++c) {
+            tma_load_3d(qd + c * kQChunk, &tmQ, &q_full[s], c * 64, h, q0);
+            tma_load_3d(qd + kQTile + c * kQChunk, &tmdO, &q_full[s], c * 64, h, q0);
+          }
         }
         bulk_load_1d(st, p.L2p + (int64_t)h * p.Np + q0, 256, &q_full[s]);
         bulk_load_1d(st + 256, p.Dp + (int64_t)h * p.Np + q0, 256, &q_full[s]);
@@ -493,7 +502,14 @@ __global__ void __maxnreg__(kNWG == 4 ? 80 : 128)  // 22 warps: 6 per SMSP x 80 
         fence_proxy_async_smem();
         named_bar_sync(1, 128);
         if (r == 0) {
-          if (!(dev_dbg(p.dbg) & 32)) tma_reduce_add_3d(&tmdQ, stg, 0, h, q0 + 32 * hh);  // dbg 32: staging only
+          const int hint = dev_dbg(p.l2hint);
+          if (dev_dbg(p.dbg) & 32) {
+            // dbg 32: staging only
+          } else if (hint & 3) {
+            tma_reduce_add_3d_hint(&tmdQ, stg, 0, h, q0 + 32 * hh, (hint & 1) ? policy_evict_last() : policy_evict_first());
+          } else {
+            tma_reduce_add_3d(&tmdQ, stg, 0, h, q0 + 32 * hh);
+          }
           bulk_commit();
         }
       }
@@ -812,6 +828,8 @@ tt_status sm100_attn_bwd(const tt_packed& pk, const void* q, const void* k, cons
     const char* o = dev_getenv("TT_CTA_ORDER");  // development A/B: bit 1 = bwd head-major
     const char* wk = dev_getenv("TT_BWD_WALK");
     prm.walk = wk ? atoi(wk) : 0;
+    const char* lh = dev_getenv("TT_BWD_L2HINT");
+    prm.l2hint = lh ? atoi(lh) : 0;
     const char* wh = dev_getenv("TT_WAIT_HINT");
     prm.wait = wh ? atoi(wh) : 0;
     prm.chunk = bwd_cta_chunk(pk, hkv);
