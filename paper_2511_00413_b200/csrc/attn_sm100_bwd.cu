@@ -11,35 +11,30 @@
 //
 // Design — key-stationary: one CTA owns a 128-key block kb of one kv head and
 // walks the contiguous query range [128 kb, maxE_kb) (exact: the queries that see key j are
-// [j, E_j)) in 64-row query tiles, for every q head of the GQA group.  K and V stay in shared
-// memory; dK and dV accumulate in TMEM across all iterations.
-//   warp 0     producer: TMA of K, V once; per iteration TMA of Q_i, dO_i (64 x 128) into a
-//              3-stage ring, plus LSE (log2), D and w of the 64 rows staged by the 32 lanes
-//   warp 1     TMEM allocator + MMA issuer (one thread).  Per iteration:
-//                S^T = K Q^T, dP^T = V dO^T            (M=128 keys, N=64 queries, K=d)
+// [j, E_j)) in 64-row query tiles, for every q head of the GQA group.  K and V are resident in TMEM
+// (K also in shared memory as dQ^T's A operand); dK and dV accumulate in TMEM across all iterations.
+//   warp 0     producer: TMA of K once; per iteration TMA of Q_i, dO_i (64 x 128) into a 3-stage
+//              ring, plus LSE (log2), D and w of the 64 rows (bulk copies)
+//   warp 1     TMEM allocator + MMA issuer (one elected thread).  Per iteration:
+//                S^T = K Q^T, dP^T = V dO^T   (TS: A = K / V from TMEM; M=128 keys, N=64 queries, K=d)
 //                dV += P^T dO      (A = P^T from TMEM)  (M=128, N=128, K=64)
 //                dK += dS^T Q      (A = dS^T from smem) (M=128, N=128, K=64)
-//                dQ^T = K^T dS^T   (A = K^T MN-major)   (M=128 (d), N=64, K=128)
-//              Issue order per tile i: [P^T(i) ready] dV(i); [dP^T(i) read] dP(i+1);
-//              [dS^T(i) ready] dK(i), dQ(i); S(i+2).  S^T is double buffered, dP^T and dQ^T single.
-//              The element-wise warps run two phases per tile (P from S^T, then dS from dP^T), so the
-//              tensor pipe always has tile i's products or tile i+1's dP queued while they work.
-//              Measured bound (profiles/, tools/mma_rate.cu): shared-memory bandwidth.  Per 64-row
-//              tile the SS MMAs read 192 KB of operands (N = 64 SS MMAs run at 60% of the tensor
-//              peak because their A+B reads need 192 B/clk > 128 B/clk), TMA writes 32 KB, dS^T 16 KB,
-//              the dQ drain 64 KB (stage + TMA read): ~304 KB / 128 B/clk ~ 2400 cycles per tile.
+//                dQ^T = K^T dS^T   (A = K^T MN-major)   (M=128 (d), N=64, K=128) into the dP^T columns
+//              Issue order per tile i: [P^T(i) ready] dV(i), S(i+1); [dS^T(i) ready] dQ^T(i), dK(i);
+//              [dQ^T(i) drained] dP(i+1).  S^T, dP^T / dQ^T single buffered (TMEM is full).
+//              Bounds: N = 64 MMAs run at 45 (TS) / 53 (SS) cycles against a
+//              32-cycle floor, and sustained the kernel runs at the board power cap, where the dQ L2
+//              reduce and the element-wise math each cost ~14% of its energy.
 //   warps 2-9  two warpgroups sharing the 4 TMEM lane quadrants; warpgroup wg owns query columns
 //              [32 wg, 32 wg + 32) of each tile.  Element-wise (one thread per key row): P^T, dS^T
 //              with the tree-scale, P^T -> TMEM (bf16), dS^T -> smem (bf16, SWIZZLE_128B).
 //              Epilogue: warpgroup 0 writes dV, warpgroup 1 writes dK.
-//   warps 10-13 dQ drain warpgroup (one thread per head-dim lane of dQ^T): per tile it reads the
-//              64 query columns of dQ^T from TMEM, releases the buffer to the MMA issuer, and adds
-//              them into the fp32 dQ accumulator through two 16 KB smem stages (32 query rows x 128
-//              fp32 each, [row][dim]) with TMA bulk tensor reductions (cp.reduce.async.bulk.tensor
-//              .add.f32).  Measured (TT_PROFILE_COUNTERS): with the drain on the element-wise warps
-//              their per-tile critical path (element-wise ~1250 + drain ~1040 cycles) exceeded the
-//              tensor pipe's ~1790 cycles per tile; on its own warpgroup the drain runs concurrently.
-// TMEM columns: dV 0-127 | dK 128-255 | S^T[2] 256-383 | dP^T 384-447 | dQ^T 448-511.
+//   warps 10-13 dQ drain warpgroup (one thread per head-dim lane of dQ^T): copies K and V rows into
+//              TMEM at the start; per tile it reads the 64 query columns of dQ^T from TMEM, releases
+//              the columns to the MMA issuer, and adds them into the fp32 dQ accumulator through two
+//              16 KB smem stages (32 query rows x 128 fp32 each, [row][dim]) with TMA bulk tensor
+//              reductions (cp.reduce.async.bulk.tensor .add.f32).
+// TMEM columns: dV 0-127 | dK 128-255 | S^T 256-319 | K 320-383 | dP^T / dQ^T 384-447 | V 448-511.
 #include <cudaTypedefs.h>
 
 #include <cstdlib>
