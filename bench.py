@@ -566,11 +566,20 @@ def main():
         return main_reference(args, rank, world, cfg)
 
     import torch
+    # one process per GPU over NCCL; TT_BENCH_BACKEND=gloo runs the same multi-rank code path with several
+    # ranks sharing the GPUs there are (a functional check of sharding + aggregation on a 1-GPU box:
+    # tests/test_gpu_multirank_bench.py; its timings are not a measurement)
+    backend = os.environ.get("TT_BENCH_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
+    agg_dev = "cuda" if backend == "nccl" else "cpu"
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     import paper_2511_00413_b200 as tt
     tt.lib()
     refuse_dev_build(tt)
@@ -629,7 +638,7 @@ def main():
     # a6 across ranks + the job time: the step's records (identical every step) gathered once
     records = [(j.tid, j.rec) for j in jobs]
     totals, n_seen, t_max, flops_all = aggregate(records, my_ms, flops_mine, n_total_trees, dist, world,
-                                                 device="cuda")
+                                                 device=agg_dev)
 
     # ---- e2e: host buffers through the same public API, H2D + D2H inside the timed region ----
     e2e = None
@@ -648,7 +657,7 @@ def main():
             torch.cuda.synchronize()
             e_ms += a.elapsed_time(b)
         e_ms /= n_e2e
-        _, _, e_max, _ = aggregate([], e_ms, 0.0, n_total_trees, dist, world, device="cuda")
+        _, _, e_max, _ = aggregate([], e_ms, 0.0, n_total_trees, dist, world, device=agg_dev)
         e2e = {"value": round(flops_all / args.steps / (e_max * 1e-3) / 1e12, 3), "unit": "TFLOP/s",
                "ms_per_step": round(e_max, 4), "h2d_bytes_per_step": int(sum(j.h2d_bytes() for j in jobs)),
                "d2h_bytes_per_step": int(sum(j.d2h_bytes() for j in jobs)), "steps": n_e2e,

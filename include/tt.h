@@ -158,7 +158,8 @@ typedef struct {
      (better L2 locality under the power cap), heads-fastest otherwise (no late heavy tail). */
   int64_t sched_sum_nq;
   int32_t sched_max_nq;
-  int32_t reserved2;
+  int32_t wr_negative;         /* 1 when tt_pack_weights produced some W < 0 (else the backward folds
+                                  the tree-scale into the log-sum-exp: P w = exp2(. + log2 w))      */
 } tt_packed;
 
 /* Validate the forest and size the pack (HOST only, synchronous, no CUDA calls). */

@@ -49,7 +49,7 @@ class TTPlanInfo(C.Structure):
 class TTPacked(C.Structure):
     _fields_ = [(f, C.c_void_p) for f in _PTR_FIELDS] + [
         ("n_tokens", C.c_int64), ("n_nodes", C.c_int32), ("n_blk", C.c_int32), ("n_succ", C.c_int32),
-        ("max_succ", C.c_int32), ("sched_sum_nq", C.c_int64), ("sched_max_nq", C.c_int32), ("reserved2", C.c_int32)]
+        ("max_succ", C.c_int32), ("sched_sum_nq", C.c_int64), ("sched_max_nq", C.c_int32), ("wr_negative", C.c_int32)]
 
 
 _lock = threading.Lock()

@@ -153,6 +153,10 @@ __device__ __forceinline__ void bwd_item(const BwdParams& p, int it, Walk& wk, i
   q0 = ((w & 1) ? (qt0 + nq - 1 - qi) : (qt0 + qi)) * kBQ;
 }
 
+// FOLD: the tree-scale is folded into the preprocessed LSE (L2p = -LSE log2e + log2 w, valid for w >= 0:
+// integer trajectory counts, non-negative real weights, or restore off), so P w = exp2(s scale log2e + L2p)
+// costs no multiply and no per-tile load of w; real-valued weights with some w < 0 take the multiply.
+template <bool FOLD>
 __global__ void __maxnreg__(kNWG == 4 ? 80 : 128)  // 22 warps: 6 per SMSP x 80 regs x 32 fit its 16K registers
     tree_attn_bwd_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                         const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
@@ -573,8 +577,8 @@ __global__ void __maxnreg__(kNWG == 4 ? 80 : 128)  // 22 warps: 6 per SMSP x 80 
 #pragma unroll
           for (int c4 = 0; c4 < kCW / 4; ++c4) {
             const int cg = (kCW / 4) * wg + c4;  // float4 group within the 64 columns
-            const float4 NL = st_lse[cg];  // -LSE * log2e
-            const float4 W = st_w[cg];
+            const float4 NL = st_lse[cg];  // -LSE * log2e (FOLD: + log2 w)
+            const float4 W = FOLD ? make_float4(1.f, 1.f, 1.f, 1.f) : st_w[cg];
             const int c = 4 * c4;
             // P = 2^(s * scale * log2e - LSE2): columns c, c+1 on the MUFU, c+2, c+3 on the FMA pipe
             const float2 a01 = ffma2(make_float2(__uint_as_float(sv[c]), __uint_as_float(sv[c + 1])), SL, make_float2(NL.x, NL.y));
@@ -592,8 +596,13 @@ __global__ void __maxnreg__(kNWG == 4 ? 80 : 128)  // 22 warps: 6 per SMSP x 80 
               p23.x = ((cmask >> (c + 2)) & 1u) ? p23.x : 0.f;
               p23.y = ((cmask >> (c + 3)) & 1u) ? p23.y : 0.f;
             }
-            pw[2 * c4] = fmul2(p01, make_float2(W.x, W.y));
-            pw[2 * c4 + 1] = fmul2(p23, make_float2(W.z, W.w));
+            if constexpr (FOLD) {
+              pw[2 * c4] = p01;
+              pw[2 * c4 + 1] = p23;
+            } else {
+              pw[2 * c4] = fmul2(p01, make_float2(W.x, W.y));
+              pw[2 * c4 + 1] = fmul2(p23, make_float2(W.z, W.w));
+            }
             pwk[2 * c4] = pack_bf16(pw[2 * c4].x, pw[2 * c4].y);
             pwk[2 * c4 + 1] = pack_bf16(pw[2 * c4 + 1].x, pw[2 * c4 + 1].y);
           }
@@ -799,7 +808,9 @@ tt_status sm100_attn_bwd(const tt_packed& pk, const void* q, const void* k, cons
   double* part_q = reinterpret_cast<double*>(w8 + 2 * al256b((size_t)hq * Np * 4) + al256b((size_t)Np * 4) +
                                              al256b((size_t)N * hq * d * 4));
   double* part_kv = part_q + kDqConvBlocks;
-  tt_status s = launch_bwd_pre_tc(o, dout, lse, pk.w, pk.wr, restore, N, Np, hq, Dp, L2p, wf, dq_acc, st);
+  bool fold = !restore || pk.wr == nullptr || !pk.wr_negative;  // integer trajectory counts are >= 0
+  if (dev_getenv("TT_BWD_NOFOLD")) fold = false;  // development A/B: the multiply form
+  tt_status s = launch_bwd_pre_tc(o, dout, lse, pk.w, pk.wr, restore, fold ? 1 : 0, N, Np, hq, Dp, L2p, wf, dq_acc, st);
   if (s) return s;
   CUtensorMap mq, mk, mv, mdo, mdq;
   const auto BF = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
@@ -845,10 +856,11 @@ tt_status sm100_attn_bwd(const tt_packed& pk, const void* q, const void* k, cons
   prm.part_kv = sqnorm ? part_kv : nullptr;
   prm.kmat = static_cast<const __nv_bfloat16*>(k);
   prm.vmat = static_cast<const __nv_bfloat16*>(v);
-  cudaError_t e = cudaFuncSetAttribute(tree_attn_bwd_sm100, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+  auto kern = fold ? tree_attn_bwd_sm100<true> : tree_attn_bwd_sm100<false>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
   if (e != cudaSuccess) { set_error("sm100_attn_bwd: smem attribute: %s", cudaGetErrorString(e)); return TT_ERR_CUDA; }
   const unsigned grid = (unsigned)pk.n_blk * hkv;
-  tree_attn_bwd_sm100<<<grid, kBwdThreads, kSmemBytes, st>>>(mq, mk, mv, mdo, mdq, prm);
+  kern<<<grid, kBwdThreads, kSmemBytes, st>>>(mq, mk, mv, mdo, mdq, prm);
   count_launch();
   if ((s = check_launch("tree_attn_bwd_sm100"))) return s;
   const int64_t n4 = N * hq * d / 4;

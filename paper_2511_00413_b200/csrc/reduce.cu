@@ -61,7 +61,7 @@ __global__ void __launch_bounds__(256) bwd_pre_tc_kernel(const __nv_bfloat16* __
                                                          const __nv_bfloat16* __restrict__ dout,
                                                          const float* __restrict__ lse, const int32_t* __restrict__ w,
                                                          const float* __restrict__ wr,
-                                                         int restore, int64_t N, int64_t Np, int hq,
+                                                         int restore, int fold, int64_t N, int64_t Np, int hq,
                                                          float* __restrict__ Dp, float* __restrict__ L2p,
                                                          float* __restrict__ wf, float* __restrict__ dq_acc) {
   const int lane = threadIdx.x & 31, half = lane >> 4, l16 = lane & 15;
@@ -101,8 +101,10 @@ __global__ void __launch_bounds__(256) bwd_pre_tc_kernel(const __nv_bfloat16* __
       const int64_t i = row / hq;
       const int h = (int)(row % hq);
       Dp[(int64_t)h * Np + i] = -s;                                              // stored negated
-      L2p[(int64_t)h * Np + i] = i < N ? -lse[(int64_t)h * N + i] * kLog2e : 0.f;  // stored negated
-      if (h == 0) wf[i] = i < N ? (restore ? (wr ? wr[i] : (float)w[i]) : 1.f) : 0.f;
+      const float wv = i < N ? (restore ? (wr ? wr[i] : (float)w[i]) : 1.f) : 0.f;
+      // stored negated; fold: + log2 w (w >= 0; w = 0 gives -inf, i.e. P w = 0)
+      L2p[(int64_t)h * Np + i] = i < N ? -lse[(int64_t)h * N + i] * kLog2e + (fold ? log2f(wv) : 0.f) : 0.f;
+      if (h == 0) wf[i] = wv;
     }
   }
 }
@@ -202,11 +204,11 @@ tt_status launch_bwd_pre(const void* o, const void* dout, tt_dtype dt, int64_t N
 }
 
 tt_status launch_bwd_pre_tc(const void* o, const void* dout, const float* lse, const int32_t* w, const float* wr, int restore,
-                            int64_t N, int64_t Np, int hq, float* Dp, float* L2p, float* wf, float* dq_acc,
+                            int fold, int64_t N, int64_t Np, int hq, float* Dp, float* L2p, float* wf, float* dq_acc,
                             cudaStream_t st) {
   const int64_t rows = Np * hq;
   bwd_pre_tc_kernel<<<(unsigned)((rows + 8 * kPreRowsPerWarp - 1) / (8 * kPreRowsPerWarp)), 256, 0, st>>>((const __nv_bfloat16*)o, (const __nv_bfloat16*)dout,
-                                                               lse, w, wr, restore, N, Np, hq, Dp, L2p, wf, dq_acc);
+                                                               lse, w, wr, restore, fold, N, Np, hq, Dp, L2p, wf, dq_acc);
   count_launch();
   return check_launch("bwd_pre_tc_kernel");
 }

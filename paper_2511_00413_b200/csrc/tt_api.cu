@@ -376,7 +376,7 @@ tt_status tt_pack(const int32_t* parent, const int32_t* len, const int32_t* term
       P.sched_sum_nq += nq;
       P.sched_max_nq = std::max(P.sched_max_nq, nq);
     }
-    P.reserved2 = 0;
+    P.wr_negative = 0;
   }
   s = launch_pack_fill(P, order, order_start, n_order, kb_lo, const_cast<int32_t*>(P.pos), const_cast<int32_t*>(P.w),
                        const_cast<int32_t*>(P.E), const_cast<int32_t*>(P.node), const_cast<int32_t*>(P.kblk_minE),
@@ -424,12 +424,15 @@ tt_status tt_pack_weights(const int32_t* parent, const int32_t* len, const int32
   }
   const int64_t Np = (int64_t)pk->n_blk * kBlock;
   std::vector<float> img((size_t)Np, 0.f);
+  int32_t negative = 0;
   for (int32_t u = 0; u < n; ++u) {
     const float wu = (float)W[u];
+    if (H.len[u] > 0 && wu < 0.f) negative = 1;
     for (int32_t i = H.start[u]; i < H.start[u] + H.len[u]; ++i) img[i] = wu;
   }
   if (tt_status s2 = stage_h2d(wr, img.data(), img.size() * 4, as_cuda(stream), "tt_pack_weights")) return s2;
   pk->wr = wr;
+  pk->wr_negative = negative;
   return TT_OK;
 }
 

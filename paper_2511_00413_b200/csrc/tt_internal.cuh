@@ -69,7 +69,7 @@ tt_status simt_attn_fwd(const tt_packed& pk, const void* q, const void* k, const
 tt_status simt_attn_bwd(const tt_packed& pk, const void* q, const void* k, const void* v, const float* lse,
                         const float* Dvec, const void* dout, int restore, tt_dtype dt, int hq, int hkv, int d,
                         float scale, void* dq, void* dk, void* dv, cudaStream_t st);
-tt_status launch_bwd_pre_tc(const void* o, const void* dout, const float* lse, const int32_t* w, const float* wr, int restore,
+tt_status launch_bwd_pre_tc(const void* o, const void* dout, const float* lse, const int32_t* w, const float* wr, int restore, int fold,
                             int64_t N, int64_t Np, int hq, float* Dp, float* L2p, float* wf, float* dq_acc,
                             cudaStream_t st);
 tt_status launch_bwd_pre(const void* o, const void* dout, tt_dtype dt, int64_t N, int hq, int d, float* Dvec,
