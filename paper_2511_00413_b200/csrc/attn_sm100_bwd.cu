@@ -118,6 +118,7 @@ struct BwdParams {
   int chunk;  // CTA order: key blocks in chunks of `chunk`; within a chunk the kv heads outermost (1 = heads
               // fastest, >= nb = head-major: the Q / dO / dQ rows of one head group stay L2-resident)
   int wait;  // dev A/B (TT_WAIT_HINT): suspend-hint waits, bit 0 producer, 1 consumers, 2 epilogue
+  int order;   // dev A/B (TT_BWD_ORDER): bit 0 issues dP(i+1) before dK(i)
   int l2hint;  // dev A/B (TT_BWD_L2HINT): bit 0/1 dQ reduce evict_last / evict_first, bit 2/3 Q / dO loads evict_last / evict_first
   int walk;  // query-tile walk (TT_BWD_WALK, dev A/B): bit 0 descending from maxE, bit 1 heads inner
   int dbg;  // development ablations (TT_DEBUG_BWD): 1 skip dQ reduce, 2 reuse Q/dO stage (no reload), 4 skip elementwise math, 32 stage dQ but skip the L2 reduce
@@ -373,13 +374,20 @@ __global__ void __maxnreg__(kNWG == 4 ? 80 : 128)  // 22 warps: 6 per SMSP x 80 
           tc_fence_after();
           issue_dQ(dsb);
           mma_commit_w(&dq_full[0]);
-          issue_dK(dsb, qb, it);
-          mma_commit_w(&q_empty[s]);
+          const bool dk_first = !(dev_dbg(p.order) & 1);  // dev A/B (TT_BWD_ORDER=1): dP(i+1) before dK(i)
+          if (dk_first) {
+            issue_dK(dsb, qb, it);
+            mma_commit_w(&q_empty[s]);
+          }
           if (it + 1 < n_it) {
             { long long t0 = TT_CLK(); mbar_wait(&dq_free[0], it & 1); w_dq += TT_CLK() - t0; }
             tc_fence_after();
             issue_dP(it + 1);
             mma_commit_w(dp_full);
+          }
+          if (!dk_first) {
+            issue_dK(dsb, qb, it);
+            mma_commit_w(&q_empty[s]);
           }
           continue;
         }
@@ -834,6 +842,8 @@ tt_status sm100_attn_bwd(const tt_packed& pk, const void* q, const void* k, cons
     const char* o = dev_getenv("TT_CTA_ORDER");  // development A/B: bit 1 = bwd head-major
     const char* wk = dev_getenv("TT_BWD_WALK");
     prm.walk = wk ? atoi(wk) : 0;
+    const char* od = dev_getenv("TT_BWD_ORDER");
+    prm.order = od ? atoi(od) : 0;
     const char* lh = dev_getenv("TT_BWD_L2HINT");
     prm.l2hint = lh ? atoi(lh) : 0;
     const char* wh = dev_getenv("TT_WAIT_HINT");
