@@ -1145,9 +1145,10 @@ LcLaunch try_launch_cluster(const LcArgs& a0, int sms, cudaStream_t st) {
   if (const char* mc = dev_getenv("TT_LOSS_MAXCL")) want = std::min<int64_t>(want, std::max(1, atoi(mc)));  // dev: SM-count sweep
   if (dev_getenv("TT_LOSS_DEBUG")) fprintf(stderr, "loss_cluster<%d,%d>: %d active clusters, Cq %d, smem %zu\n", CS, NBUF, ncl, a.Cq, smem);
   cfg.gridDim = dim3((unsigned)(want * CS));
-  // tail rows for the SMs the clusters leave idle (split by per-SM row rate, pipe / cluster ~ 0.7: profiles/r1k_loss_split.txt)
+  // tail rows for the SMs the clusters leave idle (split by per-SM row rate, pipe / cluster ~ 0.75:
+  // profiles/r1k_loss_split.txt, re-swept in profiles/r2d_loss_split.txt)
   const int idle = sms - (int)want * CS;
-  double ratio = 0.7;
+  double ratio = 0.75;
   if (const char* e = dev_getenv("TT_LOSS_SPLIT")) ratio = atof(e);  // development A/B: 0 disables the split
   int64_t n_pipe = 0;
   if (idle > 0 && ratio > 0 && a.N >= 8 * sms && (a.V % 16 == 0) && (a.ld % 16 == 0) &&
