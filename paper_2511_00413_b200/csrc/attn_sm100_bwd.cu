@@ -558,7 +558,7 @@ __global__ void __maxnreg__(kNWG == 4 ? 80 : 128)  // 22 warps: 6 per SMSP x 80 
         mbar_wait(dp_full, it & 1);
         tc_fence_after();
         tc_fence_before();
-        mbar_arrive(dp_free);
+        if constexpr (!kVT) mbar_arrive(dp_free);
         mbar_arrive(&ds_ready[b]);
       } else {
         const float4* st_lse = reinterpret_cast<const float4*>(smem + kOffStats + s * kStatBytes);
@@ -637,7 +637,7 @@ __global__ void __maxnreg__(kNWG == 4 ? 80 : 128)  // 22 warps: 6 per SMSP x 80 
             tmem_ld16(tl + kColP + kCW * wg, *reinterpret_cast<uint32_t(*)[16]>(&pv[0]));
           tmem_wait_ld();
           tc_fence_before();
-          mbar_arrive(dp_free);
+          if constexpr (!kVT) mbar_arrive(dp_free);  // VTMEM: ds_ready (below) releases dP^T's columns
 #pragma unroll
           for (int c4 = 0; c4 < kCW / 4; ++c4) {
             const float4 ND = st_D[(kCW / 4) * wg + c4];  // -D
