@@ -110,3 +110,20 @@ def test_pack_refuses_graph_capture_and_explicit_stream():
     outs = [tt.tt_pack(t.parent, t.length) for _ in range(9)]
     torch.cuda.synchronize()
     assert all(torch.equal(o.arrays()["E"], ref.arrays()["E"]) for o in outs)
+
+
+@pytest.mark.parametrize("name", ["agentic8k", "deep32k", "wide"])
+def test_schedule_statistics(tt, name):
+    """tt_pack's host-side CTA-order statistics (include/tt.h: the backward's per-key-block query-tile
+    counts nq_kb = ceil(maxE_kb / 64) - 2 kb, their sum and maximum) equal the definition applied to the
+    oracle's subtree ends E."""
+    t = trees.config_tree(name)
+    pk = tt.tt_pack(t.parent, t.length, t.term)
+    E = oracle.pack(t.parent, t.length, t.term)["E"].astype(np.int64)
+    nb = (len(E) + 127) // 128
+    nq = np.array([(int(E[128 * b:128 * b + 128].max()) + 63) // 64 - 2 * b for b in range(nb)])
+    assert int(pk.c.sched_sum_nq) == int(nq.sum())
+    assert int(pk.c.sched_max_nq) == int(nq.max())
+    assert int(pk.c.wr_negative) == 0
+    tt.tt_pack_weights(pk, np.full(pk.info["n_traj"], -0.5, np.float32))
+    assert int(pk.c.wr_negative) == 1
