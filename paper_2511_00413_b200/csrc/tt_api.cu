@@ -186,7 +186,7 @@ static PackLayout pack_layout(int64_t N, int32_t n, int32_t n_succ, int32_t n_or
   L.off_flist = o; o = al256(o + (size_t)tri_off(L.nb) * 4);
   // node block: start, len, sub_end, depth, leaves [n] each, succ_ptr [n+1], succ_tok, order, order_start
   L.off_nodeblk = o;
-  L.nodeblk_bytes = (size_t)(5 * (size_t)n + (n + 1) + n_succ + 2 * (size_t)n_order + L.nb) * 4;
+  L.nodeblk_bytes = (size_t)(5 * (size_t)n + (n + 1) + n_succ + 2 * (size_t)n_order + 2 * (size_t)L.nb) * 4;
   o = al256(o + L.nodeblk_bytes);
   L.total = o;
   return L;
@@ -328,11 +328,15 @@ tt_status tt_pack(const int32_t* parent, const int32_t* len, const int32_t* term
   img.insert(img.end(), H.order_start.begin(), H.order_start.end());
   // per q-block: the first k-block of the tree holding the block's first token (no key of an
   // earlier tree is ever visible, so the tile classification of a forest starts there)
+  // and per block the packed-order index of the node holding its first token (pack_fill_kernel's start)
+  std::vector<int32_t> blk_first_h(L.nb);
   for (int32_t qb = 0; qb < L.nb; ++qb) {
     const int32_t i0 = qb * kBlock;
     const int32_t k = (int32_t)(std::upper_bound(H.order_start.begin(), H.order_start.end(), i0) - H.order_start.begin()) - 1;
     img.push_back(H.root_start[H.order[std::max(k, 0)]] / kBlock);
+    blk_first_h[qb] = std::max(k, 0);
   }
+  img.insert(img.end(), blk_first_h.begin(), blk_first_h.end());
   int32_t* nb = reinterpret_cast<int32_t*>(base + L.off_nodeblk);
   cudaStream_t st = as_cuda(stream);
   if ((s = stage_h2d(nb, img.data(), img.size() * 4, st, "tt_pack"))) return s;
@@ -351,6 +355,7 @@ tt_status tt_pack(const int32_t* parent, const int32_t* len, const int32_t* term
   const int32_t* order = nb + 6 * n + 1 + n_succ;
   const int32_t* order_start = order + n_order;
   const int32_t* kb_lo = order_start + n_order;
+  const int32_t* blk_first = kb_lo + L.nb;
   P.kblk_minE = reinterpret_cast<int32_t*>(base + L.off_kmin);
   P.kblk_maxE = reinterpret_cast<int32_t*>(base + L.off_kmax);
   P.fwd_cnt = reinterpret_cast<int32_t*>(base + L.off_fcnt);
@@ -378,7 +383,7 @@ tt_status tt_pack(const int32_t* parent, const int32_t* len, const int32_t* term
     }
     P.wr_negative = 0;
   }
-  s = launch_pack_fill(P, order, order_start, n_order, kb_lo, const_cast<int32_t*>(P.pos), const_cast<int32_t*>(P.w),
+  s = launch_pack_fill(P, order, order_start, n_order, kb_lo, blk_first, const_cast<int32_t*>(P.pos), const_cast<int32_t*>(P.w),
                        const_cast<int32_t*>(P.E), const_cast<int32_t*>(P.node), const_cast<int32_t*>(P.kblk_minE),
                        const_cast<int32_t*>(P.kblk_maxE), const_cast<int32_t*>(P.fwd_cnt),
                        const_cast<int32_t*>(P.fwd_list), st);

@@ -60,7 +60,7 @@ __host__ __device__ inline int64_t tri_off(int64_t qb) { return qb * (qb + 1) / 
 
 // ---- kernel launchers implemented in the .cu files ----
 tt_status launch_pack_fill(const tt_packed& pk, const int32_t* order, const int32_t* order_start, int32_t n_order,
-                           const int32_t* kb_lo,
+                           const int32_t* kb_lo, const int32_t* blk_first,
                            int32_t* pos, int32_t* w, int32_t* E, int32_t* node, int32_t* kminE, int32_t* kmaxE,
                            int32_t* fwd_cnt, int32_t* fwd_list, cudaStream_t st);
 
