@@ -1,0 +1,9 @@
+# final check C (after the pack changes): full GPU suite, smoke, memcheck of the pack tests, default bench
+set -u
+O=gpurun_out/${1:-r2fc}; mkdir -p $O
+python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1
+timeout 2400 python -m pytest tests -m gpu -q --durations=10 > $O/pytest_gpu.log 2>&1; echo "pytest exit $?" >> $O/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke exit $?" >> $O/smoke.log
+timeout 900 compute-sanitizer --tool memcheck --print-limit 20 --error-exitcode 9 python -m pytest tests/test_gpu_pack.py -x -q > $O/pack_memcheck.txt 2>&1; echo "exit $?" >> $O/pack_memcheck.txt
+timeout 1500 python bench.py --steps 20 --warmup 5 > $O/bench_batch64k.json 2> $O/bench_batch64k.err
+echo done > $O/done.txt
