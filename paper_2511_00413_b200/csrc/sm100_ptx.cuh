@@ -147,6 +147,32 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// ------------------------------------------------------------------------------ cluster launch control
+// Persistent scheduling with the hardware's own CTA order: a running CTA cancels a CTA of its grid
+// that has not been launched yet and takes over that CTA's work item.  The 16-byte response lands in
+// shared memory and completes 16 transaction bytes on `bar` (expect_tx(bar, 16) first).  After one
+// failed request (nothing left to cancel) no further request may be issued.
+__device__ __forceinline__ void clc_try_cancel(void* resp16, uint64_t* bar) {
+  asm volatile("clusterlaunchcontrol.try_cancel.async.shared::cta.mbarrier::complete_tx::bytes.b128 [%0], [%1];" ::"r"(
+                   smem_u32(resp16)),
+               "r"(smem_u32(bar))
+               : "memory");
+}
+// blockIdx.x of the cancelled CTA, or -1 when the request found nothing left to cancel.
+__device__ __forceinline__ int clc_query_x(const void* resp16) {
+  uint32_t x = 0, ok = 0;
+  asm volatile(
+      "{\n.reg .pred p;\n.reg .b128 r;\n"
+      "ld.shared.b128 r, [%2];\n"
+      "clusterlaunchcontrol.query_cancel.is_canceled.pred.b128 p, r;\n"
+      "selp.u32 %1, 1, 0, p;\n"
+      "@p clusterlaunchcontrol.query_cancel.get_first_ctaid::x.b32.b128 %0, r;\n}\n"
+      : "+r"(x), "=r"(ok)
+      : "r"(smem_u32(resp16))
+      : "memory");
+  return ok ? (int)x : -1;
+}
+
 // ------------------------------------------------------------------------------ tcgen05
 __device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {
   asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)), "r"(ncols)
