@@ -9,13 +9,19 @@
 // The tree-scale enters as a per-query-column factor on P and dS in registers:
 // dO and D stay unscaled and no restored copy of dO is ever materialised.
 //
-// Design — key-stationary: one CTA owns a 128-key block kb of one kv head and
-// walks the contiguous query range [128 kb, maxE_kb) (exact: the queries that see key j are
-// [j, E_j)) in 64-row query tiles, for every q head of the GQA group.  K and V are resident in TMEM
-// (K also in shared memory as dQ^T's A operand); dK and dV accumulate in TMEM across all iterations.
-//   warp 0     producer: TMA of K once; per iteration TMA of Q_i, dO_i (64 x 128) into a 3-stage
-//              ring, plus LSE (log2), D and w of the 64 rows (bulk copies)
-//   warp 1     TMEM allocator + MMA issuer (one elected thread).  Per iteration:
+// Design — key-stationary: a work item is a 128-key block kb of one kv head; it walks
+// the contiguous query range [128 kb, maxE_kb) (exact: the queries that see key j are [j, E_j)) in
+// 64-row query tiles, for every q head of the GQA group.  K and V are resident in TMEM (copied in from
+// shared memory with tcgen05.cp; K also stays in shared memory as dQ^T's A operand); dK and dV
+// accumulate in TMEM across all of the item's tiles.
+// Persistent CTAs: the grid has one CTA per item and the hardware launches them in order, but a running
+// CTA takes over the next not-yet-launched CTA's item through cluster launch control, one item ahead,
+// so the next item's K/V loads, TMEM copies and first S^T / dP^T MMAs overlap this item's last tiles and
+// its dK/dV epilogue (no CTA exit / launch / TMEM allocation between items).
+//   warp 0     producer: the item scheduler (CLC) and TMA: K, V of each item; per tile Q_i, dO_i
+//              (64 x 128) into a 3-stage ring, plus LSE (log2), D and w of the 64 rows (bulk copies)
+//   warp 1     TMEM allocator + MMA issuer (one elected thread).  Per item: K, V -> TMEM (tcgen05.cp).
+//              Per tile:
 //                S^T = K Q^T, dP^T = V dO^T   (TS: A = K / V from TMEM; M=128 keys, N=64 queries, K=d)
 //                dV += P^T dO      (A = P^T from TMEM)  (M=128, N=128, K=64)
 //                dK += dS^T Q      (A = dS^T from smem) (M=128, N=128, K=64)
@@ -28,12 +34,11 @@
 //   warps 2-9  two warpgroups sharing the 4 TMEM lane quadrants; warpgroup wg owns query columns
 //              [32 wg, 32 wg + 32) of each tile.  Element-wise (one thread per key row): P^T, dS^T
 //              with the tree-scale, P^T -> TMEM (bf16), dS^T -> smem (bf16, SWIZZLE_128B).
-//              Epilogue: warpgroup 0 writes dV, warpgroup 1 writes dK.
-//   warps 10-13 dQ drain warpgroup (one thread per head-dim lane of dQ^T): copies K and V rows into
-//              TMEM at the start; per tile it reads the 64 query columns of dQ^T from TMEM, releases
-//              the columns to the MMA issuer, and adds them into the fp32 dQ accumulator through two
-//              16 KB smem stages (32 query rows x 128 fp32 each, [row][dim]) with TMA bulk tensor
-//              reductions (cp.reduce.async.bulk.tensor .add.f32).
+//              Epilogue of each item: warpgroup 0 writes dV, warpgroup 1 writes dK.
+//   warps 10-13 dQ drain warpgroup (one thread per head-dim lane of dQ^T): per tile it reads the 64
+//              query columns of dQ^T from TMEM, releases the columns to the MMA issuer, and adds them
+//              into the fp32 dQ accumulator through two 16 KB smem stages (32 query rows x 128 fp32
+//              each, [row][dim]) with TMA bulk tensor reductions (cp.reduce.async.bulk.tensor .add.f32).
 // TMEM columns: dV 0-127 | dK 128-255 | S^T 256-319 | K 320-383 | dP^T / dQ^T 384-447 | V 448-511.
 #include <cudaTypedefs.h>
 
@@ -67,12 +72,13 @@ constexpr int kCW = 64 / kNWG;
 static_assert(kNWG == 2 || kNWG == 4, "2 or 4 element-wise warpgroups");
 constexpr int kDrainWarp0 = 2 + 4 * kNWG;                  // first warp of the dQ drain warpgroup
 constexpr int kBwdThreads = 32 * (kDrainWarp0 + 4);        // producer, MMA, element-wise, drain
+constexpr int kConsumerThreads = kBwdThreads - 32;         // read every item's info (all but the producer)
 constexpr uint32_t kKVTile = 128 * kD * 2;     // 32 KB (two 16 KB chunks of 128 rows x 128 B)
 constexpr uint32_t kKVChunk = 128 * 64 * 2;    // 16 KB
 constexpr uint32_t kQTile = kBQ * kD * 2;      // 16 KB (two 8 KB chunks of 64 rows x 128 B)
 constexpr uint32_t kQChunk = kBQ * 64 * 2;     // 8 KB
-constexpr uint32_t kOffK = 0;
-constexpr uint32_t kOffV = kKVTile;
+// K / V slots 0 and 1: item n's K in slot n & 1 (also dQ^T's A operand), its V in the other (source of
+// its TMEM copy only)
 constexpr uint32_t kOffQS = 2 * kKVTile;                     // stage s: Q at +s*32K, dO at +s*32K+16K
 constexpr uint32_t kDSTile = 128 * kBQ * 2;
 constexpr uint32_t kOffDS = kOffQS + kQStages * 2 * kQTile;      // dS^T[2], 16 KB each (1024-aligned)
@@ -81,32 +87,24 @@ constexpr uint32_t kDQStage = 32 * kD * 4;
 constexpr uint32_t kStatBytes = 768;                              // per stage: -LSE2 | -D | w (256 B each)
 constexpr uint32_t kOffStats = kOffDQ + 2 * kDQStage;
 constexpr uint32_t kOffBar = kOffStats + kQStages * kStatBytes;
-constexpr uint32_t kNumBars = 1 + 2 * kQStages + 12 + 1 + 1;
-constexpr uint32_t kOffMisc = kOffBar + kNumBars * 8;
+// k_full, v_full, q_full[3], q_empty[3], s_full, p_ready, ds_ready[2], dq_full, dq_free, dp_full,
+// acc_done, acc_free, v_free, k_free, item_full[2], item_empty[2], clc
+constexpr uint32_t kNumBars = 2 + 2 * kQStages + 1 + 1 + 2 + 1 + 1 + 1 + 1 + 1 + 2 + 4 + 1;
+// the next item is claimed (CLC) when its producer reaches this many tiles before the current item's
+// end, and published (info + K load) at kPrepareAhead tiles before it
+constexpr int kClaimAhead = 6, kPrepareAhead = 3;
+constexpr uint32_t kOffMisc = (kOffBar + kNumBars * 8 + 15) & ~15u;  // [0] TMEM base
+constexpr uint32_t kOffInfo = kOffMisc + 16;                     // item buffers [2]: {item, kb, hk, nq} (item -1: done)
+constexpr uint32_t kOffClc = kOffInfo + 2 * 16;                  // cluster-launch-control response
 // The dynamic shared-memory window is 1024-byte aligned on sm_100 (checked at run time; the kernel
 // traps otherwise), so no alignment slack is reserved.
-constexpr uint32_t kOffRed = kOffMisc + 16;                       // a6 reduction scratch: double [kNWG][4]
+constexpr uint32_t kOffRed = kOffClc + 16;                        // a6 reduction scratch: double [kNWG][4]
 // (no static __shared__ in this kernel: it would shift the 1024-byte aligned dynamic window)
 constexpr uint32_t kSmemBytes = kOffRed + 32 * kNWG;
 static_assert(kSmemBytes <= 232448, "backward kernel exceeds 227 KB of shared memory");
 
-// TT_BWD_KTMEM: K resident in TMEM (A operand of S^T = K Q^T as a TS MMA: the 32 KB per tile of K
-// re-reads from shared memory disappear) at the price of a single S^T buffer.
-#ifndef TT_BWD_KTMEM
-#define TT_BWD_KTMEM 1
-#endif
-constexpr bool kKT = TT_BWD_KTMEM != 0;
-// TT_BWD_VTMEM (requires KTMEM): V resident in TMEM too (dP^T = V dO^T as a TS MMA: the 32 KB per tile
-// of V reads from shared memory disappear) and dQ^T accumulates in the dP^T columns once the element-wise
-// warps have read dP^T; dP^T(i+1) is issued after the drain has read dQ^T(i).
-#ifndef TT_BWD_VTMEM
-#define TT_BWD_VTMEM 1
-#endif
-constexpr bool kVT = kKT && TT_BWD_VTMEM != 0;
-// TMEM columns: dV 0-127 | dK 128-255 | S^T 256-319 (KTMEM) or S^T x2 256-383 | K 320-383 (KTMEM) |
-// dP^T 384-447 (VTMEM: dP^T, then dQ^T) | dQ^T 448-511 (VTMEM: V)
-constexpr uint32_t kColDV = 0, kColDK = 128, kColS = 256, kColK = 320, kColP = 384;
-constexpr uint32_t kColQ = kVT ? kColP : 448, kColV = 448;
+// TMEM columns: dV 0-127 | dK 128-255 | S^T 256-319 | K 320-383 | dP^T, then dQ^T 384-447 | V 448-511
+constexpr uint32_t kColDV = 0, kColDK = 128, kColS = 256, kColK = 320, kColP = 384, kColQ = 384, kColV = 448;
 
 // development instrumentation (TT_DEBUG_BWD & 8): per-role cycle counters summed over CTAs
 __device__ unsigned long long g_bwd_dbg[16];
@@ -117,11 +115,10 @@ struct BwdParams {
   int restore;
   int chunk;  // CTA order: key blocks in chunks of `chunk`; within a chunk the kv heads outermost (1 = heads
               // fastest, >= nb = head-major: the Q / dO / dQ rows of one head group stay L2-resident)
-  int wait;  // dev A/B (TT_WAIT_HINT): suspend-hint waits, bit 0 producer, 1 consumers, 2 epilogue
-  int order;   // dev A/B (TT_BWD_ORDER): bit 0 issues dP(i+1) before dK(i)
-  int l2hint;  // dev A/B (TT_BWD_L2HINT): bit 0/1 dQ reduce evict_last / evict_first, bit 2/3 Q / dO loads evict_last / evict_first
-  int walk;  // query-tile walk (TT_BWD_WALK, dev A/B): bit 0 descending from maxE, bit 1 heads inner
-  int dbg;  // development ablations (TT_DEBUG_BWD): 1 skip dQ reduce, 2 reuse Q/dO stage (no reload), 4 skip elementwise math, 32 stage dQ but skip the L2 reduce
+  int steal;  // persistent CTAs: take over not-yet-launched CTAs' items (dev A/B TT_BWD_NOSTEAL: 0)
+  int wait;   // dev A/B (TT_WAIT_HINT): suspend-hint waits, bit 0 producer, 1 consumers, 2 epilogue
+  int dbg;    // development ablations (TT_DEBUG_BWD): 1 skip dQ reduce, 4 skip elementwise math, 8 counters,
+              // 32 stage dQ but skip the L2 reduce
   float scale, scale_log2;
   const int32_t* E;
   const int32_t* kmaxE;
@@ -132,27 +129,30 @@ struct BwdParams {
   float* dq_acc;
   __nv_bfloat16* dk;
   __nv_bfloat16* dv;
-  double* part_kv;  // nullable: [grid][2] fp64 partial sums of squares of this CTA's dV (0) / dK (1) rows
-  const __nv_bfloat16* kmat;  // K [N, hkv, 128] (KTMEM: rows copied into TMEM by the drain warpgroup)
-  const __nv_bfloat16* vmat;  // V [N, hkv, 128] (VTMEM: likewise)
+  double* part_kv;  // nullable: [grid][2] fp64 partial sums of squares of an item's dV (0) / dK (1) rows
 };
 
-// work item `it` of a CTA -> (q head, first query row of the 64-row tile).  The shipped walk (GQA heads
-// outer, query tiles ascending) advances a (tile, head) counter pair: no integer division per tile.
+// work item x (a blockIdx.x of the grid) -> (key block, kv head) and its number of 64-row query tiles
+__device__ __forceinline__ int4 bwd_item_of(const BwdParams& p, int x) {
+  const int per = p.chunk * p.hkv;
+  const int ch = x / per, w = x - ch * per;
+  const int len = min(p.chunk, p.nb - ch * p.chunk);
+  const int hk = w / len;
+  const int kb = ch * p.chunk + (w - hk * len);
+  const int nq = (int)((p.kmaxE[kb] + kBQ - 1) / kBQ) - 2 * kb;  // query tiles [2 kb, ceil(maxE / 64))
+  return make_int4(x, kb, hk, nq);
+}
+
+// tile `it` of an item -> (q head, first query row): GQA heads outer, query tiles ascending, advanced
+// with a (tile, head) counter pair (no integer division per tile)
 struct Walk {
   int qi = 0, hi = 0;
-};
-__device__ __forceinline__ void bwd_item(const BwdParams& p, int it, Walk& wk, int nq, int qt0, int hk, int& h, int& q0) {
-  const int w = dev_dbg(p.walk);
-  int qi = wk.qi, hi = wk.hi;
-  if (w) {
-    qi = (w & 2) ? it / p.g : it % nq;
-    hi = (w & 2) ? it % p.g : it / nq;
+  __device__ __forceinline__ void next(const BwdParams& p, int nq, int kb, int hk, int& h, int& q0) {
+    h = hk * p.g + hi;
+    q0 = (2 * kb + qi) * kBQ;
+    if (++qi == nq) { qi = 0; ++hi; }
   }
-  if (++wk.qi == nq) { wk.qi = 0; ++wk.hi; }
-  h = hk * p.g + hi;
-  q0 = ((w & 1) ? (qt0 + nq - 1 - qi) : (qt0 + qi)) * kBQ;
-}
+};
 
 // FOLD: the tree-scale is folded into the preprocessed LSE (L2p = -LSE log2e + log2 w, valid for w >= 0:
 // integer trajectory counts, non-negative real weights, or restore off), so P w = exp2(s scale log2e + L2p)
@@ -168,51 +168,46 @@ __global__ void __maxnreg__(kNWG == 4 ? 80 : 128)  // 22 warps: 6 per SMSP x 80 
   uint8_t* smem = smem_raw;
   if (smem_u32(smem_raw) & 1023u) __trap();
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBar);
-  uint64_t* kv_full = bars;
-  uint64_t* q_full = bars + 1;
+  uint64_t* k_full = bars;                // K of the item in shared memory
+  uint64_t* v_full = bars + 1;            // V of the item in shared memory
+  uint64_t* q_full = bars + 2;
   uint64_t* q_empty = q_full + kQStages;
-  uint64_t* s_full = q_empty + kQStages;  // [2] S^T(i) in TMEM
-  uint64_t* p_ready = s_full + 2;         // [2] P^T(i) packed back into S^T[b] (256 arrivals)
-  uint64_t* ds_ready = p_ready + 2;       // [2] dS^T(i) in smem (256 arrivals)
-  uint64_t* dq_full = ds_ready + 2;       // [2]
-  uint64_t* dq_free = dq_full + 2;        // [2]
-  uint64_t* dp_full = dq_free + 2;        // dP^T(i) in TMEM
-  uint64_t* dp_free = dp_full + 1;        // dP^T(i) read by the element-wise warps (256 arrivals)
-  uint64_t* acc_done = dp_free + 1;
-  uint64_t* k_tmem = acc_done + 1;        // K written into TMEM (128 arrivals, KTMEM)
+  uint64_t* s_full = q_empty + kQStages;  // S^T(i) in TMEM
+  uint64_t* p_ready = s_full + 1;         // P^T(i) packed back into S^T (128 kNWG arrivals)
+  uint64_t* ds_ready = p_ready + 1;       // [2] dS^T(i) in smem (128 kNWG arrivals)
+  uint64_t* dq_full = ds_ready + 2;       // dQ^T(i) in TMEM
+  uint64_t* dq_free = dq_full + 1;        // dQ^T(i) read by the drain (128 arrivals)
+  uint64_t* dp_full = dq_free + 1;        // dP^T(i) in TMEM
+  uint64_t* acc_done = dp_full + 1;       // the item's dK / dV final
+  uint64_t* acc_free = acc_done + 1;      // the item's dK / dV read out of TMEM (128 drain arrivals)
+  uint64_t* v_free = acc_free + 1;        // the item's V TMEM copy done (V's smem slot free)
+  uint64_t* k_free = v_free + 1;          // the item's last dQ^T done (K's smem slot free)
+  uint64_t* item_full = k_free + 1;       // [2] item info written
+  uint64_t* item_empty = item_full + 2;   // [2] item info read (every consumer thread)
+  uint64_t* clc_bar = item_empty + 2;
   uint32_t* misc = reinterpret_cast<uint32_t*>(smem + kOffMisc);
+  int4* info = reinterpret_cast<int4*>(smem + kOffInfo);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long t_kernel0 = TT_CLK();
-  int kb, hk;
-  {
-    const int per = p.chunk * p.hkv, x = (int)blockIdx.x;
-    const int ch = x / per, w = x - ch * per;
-    const int len = min(p.chunk, p.nb - ch * p.chunk);
-    hk = w / len;
-    kb = ch * p.chunk + (w - hk * len);
-  }
-  const int64_t k0 = (int64_t)kb * 128;
-  const int qt0 = (int)(k0 / kBQ);                                    // first 64-row query tile
-  const int qt1 = (int)((p.kmaxE[kb] + kBQ - 1) / kBQ);                // exclusive
-  const int nq = qt1 - qt0;
-  const int n_it = nq * p.g;                                          // (head, query tile) pairs
 
   if (warp == 1) {
     if (lane == 0) {
-      mbar_init(kv_full, 1);
+      mbar_init(k_full, 1);
+      mbar_init(v_full, 1);
+      mbar_init(acc_free, 128);
       for (int s = 0; s < kQStages; ++s) { mbar_init(&q_full[s], 1); mbar_init(&q_empty[s], 1); }
-      for (int b = 0; b < 2; ++b) {
-        mbar_init(&s_full[b], 1);
-        mbar_init(&p_ready[b], 128 * kNWG);
-        mbar_init(&ds_ready[b], 128 * kNWG);
-        mbar_init(&dq_full[b], 1);
-        mbar_init(&dq_free[b], 128);
-      }
+      mbar_init(s_full, 1);
+      mbar_init(p_ready, 128 * kNWG);
+      for (int b = 0; b < 2; ++b) mbar_init(&ds_ready[b], 128 * kNWG);
+      mbar_init(dq_full, 1);
+      mbar_init(dq_free, 128);
       mbar_init(dp_full, 1);
-      mbar_init(dp_free, 128 * kNWG);
       mbar_init(acc_done, 1);
-      mbar_init(k_tmem, 128);
+      mbar_init(v_free, 1);
+      mbar_init(k_free, 1);
+      for (int b = 0; b < 2; ++b) { mbar_init(&item_full[b], 1); mbar_init(&item_empty[b], kConsumerThreads); }
+      mbar_init(clc_bar, 1);
       mbar_fence_init();
     }
   }
@@ -232,295 +227,351 @@ __global__ void __maxnreg__(kNWG == 4 ? 80 : 128)  // 22 warps: 6 per SMSP x 80 
   }
 
   if (warp == 0) {
-    // ===================== producer (lane 0) =====================
+    // ===================== producer warp: item scheduler (CLC) + TMA =====================
+    // An item's K goes to shared-memory slot (n & 1), its V to the other slot: K(n+1) can land in V(n)'s
+    // slot as soon as V(n) was copied into TMEM (early in item n), V(n+1) in K(n)'s slot once item n's
+    // last dQ^T (K's last reader) completed.
+    bool steal = p.steal != 0;
+    uint32_t clc_ph = 0;
     if (lane == 0) {
       tma_prefetch(&tmQ);
       tma_prefetch(&tmK);
       tma_prefetch(&tmV);
       tma_prefetch(&tmdO);
-      mbar_expect_tx(kv_full, (kVT ? 1 : 2) * kKVTile);
-      for (int c = 0; c < 2; ++c) {
-        tma_load_3d(smem + kOffK + c * kKVChunk, &tmK, kv_full, c * 64, hk, (int)k0);
-        if (!kVT) tma_load_3d(smem + kOffV + c * kKVChunk, &tmV, kv_full, c * 64, hk, (int)k0);
-      }
     }
+    auto load_k = [&](int slot, int kb, int hk) {
+      mbar_expect_tx(k_full, kKVTile);
+      for (int c = 0; c < 2; ++c) tma_load_3d(smem + slot * kKVTile + c * kKVChunk, &tmK, k_full, c * 64, hk, kb * 128);
+    };
+    auto load_v = [&](int slot, int kb, int hk) {
+      mbar_expect_tx(v_full, kKVTile);
+      for (int c = 0; c < 2; ++c) tma_load_3d(smem + slot * kKVTile + c * kKVChunk, &tmV, v_full, c * 64, hk, kb * 128);
+    };
+    int4 cur = bwd_item_of(p, (int)blockIdx.x);
     if (lane == 0) {
-      Walk wk;
-      for (int it = 0; it < n_it; ++it) {
-        const int s = it % kQStages;
-        if (it >= kQStages) mbar_wait_role(&q_empty[s], ((it / kQStages) - 1) & 1, dev_dbg(p.wait) & 1);
-        int h, q0;
-        bwd_item(p, it, wk, nq, qt0, hk, h, q0);
-        uint8_t* qd = smem + kOffQS + s * 2 * kQTile;
-        uint8_t* st = smem + kOffStats + s * kStatBytes;
-        if ((dev_dbg(p.dbg) & 2) && it >= kQStages) {
-          mbar_arrive(&q_full[s]);
-          continue;
+      load_k(0, cur.y, cur.z);
+      load_v(1, cur.y, cur.z);
+      info[0] = cur;
+      mbar_arrive(&item_full[0]);
+    }
+    uint32_t G = 0;  // query tiles issued so far (all items): stage G % kQStages
+    for (int n = 0;; ++n) {
+      const int kb = cur.y, hk = cur.z, nq = cur.w, n_it = nq * p.g;
+      // V(n) (n >= 1) goes into K(n-1)'s slot once item n-1's last dQ^T completed; that dQ^T is issued
+      // after item n's first S^T, so the wait comes after this item's first Q / dO load
+      int4 nxt = make_int4(-1, 0, 0, 0);
+      bool claimed = false, prepared = false;
+      // The next item is claimed late (a few tiles before this one ends: claiming at the start of an
+      // item would pair heavy items on one CTA and unbalance the tail) and published with its K load
+      // once this item's last Q / dO tiles are in flight.
+      auto claim = [&]() {
+        claimed = true;
+        if (steal && lane == 0) {
+          mbar_expect_tx(clc_bar, 16);
+          clc_try_cancel(smem + kOffClc, clc_bar);
         }
-        mbar_expect_tx(&q_full[s], 2 * kQTile + 3 * 256);
-        if (dev_dbg(p.l2hint) & 12) {
-          const uint64_t pol = (dev_dbg(p.l2hint) & 4) ? policy_evict_last() : policy_evict_first();
-          for (int c = 0; c < 2; ++c) {
-            tma_load_3d_hint(qd + c * kQChunk, &tmQ, &q_full[s], c * 64, h, q0, pol);
-            tma_load_3d_hint(qd + kQTile + c * kQChunk, &tmdO, &q_full[s], c * 64, h, q0, pol);
-          }
-        } else {
+      };
+      auto prepare_next = [&]() {
+        prepared = true;
+        if (!claimed) claim();
+        if (steal) {
+          mbar_wait(clc_bar, clc_ph);
+          clc_ph ^= 1;
+          const int xn = clc_query_x(smem + kOffClc);
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (xn < 0) steal = false;  // no further request after a failed one
+          else nxt = bwd_item_of(p, xn);
+        }
+        if (n >= 1) mbar_wait(&item_empty[(n + 1) & 1], ((n - 1) >> 1) & 1);  // item n-1's info read
+        if (lane == 0) {
+          info[(n + 1) & 1] = nxt;
+          mbar_arrive(&item_full[(n + 1) & 1]);
+        }
+        if (nxt.x >= 0) {
+          mbar_wait(v_free, n & 1);  // V(n) copied into TMEM: its slot takes K(n+1)
+          if (lane == 0) load_k((n + 1) & 1, nxt.y, nxt.z);
+        }
+      };
+      Walk wk;
+      for (int it = 0; it < n_it; ++it, ++G) {
+        const int s = (int)(G % kQStages);
+        if (G >= (uint32_t)kQStages) mbar_wait_role(&q_empty[s], ((G / kQStages) - 1) & 1, dev_dbg(p.wait) & 1);
+        int h, q0;
+        wk.next(p, nq, kb, hk, h, q0);
+        if (lane == 0) {
+          uint8_t* qd = smem + kOffQS + s * 2 * kQTile;
+          uint8_t* st = smem + kOffStats + s * kStatBytes;
+          mbar_expect_tx(&q_full[s], 2 * kQTile + 3 * 256);
           for (int c = 0; c < 2; ++c) {
             tma_load_3d(qd + c * kQChunk, &tmQ, &q_full[s], c * 64, h, q0);
             tma_load_3d(qd + kQTile + c * kQChunk, &tmdO, &q_full[s], c * 64, h, q0);
           }
+          bulk_load_1d(st, p.L2p + (int64_t)h * p.Np + q0, 256, &q_full[s]);
+          bulk_load_1d(st + 256, p.Dp + (int64_t)h * p.Np + q0, 256, &q_full[s]);
+          bulk_load_1d(st + 512, p.wf + q0, 256, &q_full[s]);
         }
-        bulk_load_1d(st, p.L2p + (int64_t)h * p.Np + q0, 256, &q_full[s]);
-        bulk_load_1d(st + 256, p.Dp + (int64_t)h * p.Np + q0, 256, &q_full[s]);
-        bulk_load_1d(st + 512, p.wf + q0, 256, &q_full[s]);
+        if (it == 0 && n >= 1) {
+          mbar_wait(k_free, (n - 1) & 1);
+          if (lane == 0) load_v((n - 1) & 1, kb, hk);
+        }
+        if (!claimed && it >= n_it - kClaimAhead) claim();
+        if (!prepared && it >= n_it - kPrepareAhead) prepare_next();
       }
+      if (!prepared) prepare_next();
+      if (nxt.x < 0) break;
+      cur = nxt;
     }
   } else if (warp == 1) {
-    {
-      // ===================== MMA issuer (whole warp, one elected lane issues) =====================
-      constexpr uint32_t idSP = idesc_bf16(128, kBQ, 0, 0);   // K/V (K-major) x Q/dO^T (K-major)
-      constexpr uint32_t idVK = idesc_bf16(128, 128, 0, 1);   // P^T/dS^T (K-major) x dO/Q (MN-major)
-      constexpr uint32_t idQ = idesc_bf16(128, kBQ, 1, 1);    // K^T (MN-major) x dS^T (MN-major)
-      const uint32_t kb_s = warp_uniform(smem_u32(smem + kOffK)), vb_s = kb_s + kOffV;
-      const uint32_t tm = warp_uniform(tmem);
-      const uint32_t qs0 = kb_s + kOffQS, ds0 = kb_s + kOffDS;
-      auto issue_SP = [&](int it) {
-        const int s = it % kQStages, b = it & 1;
-        const uint32_t qb = qs0 + s * 2 * kQTile;
-        const uint32_t ob = qb + kQTile;
+    // ===================== MMA issuer (whole warp, one elected lane issues) =====================
+    // One stream of query tiles across items: the last tile of item n issues item n+1's K copy and
+    // first S^T in place of "S(i+1)", and its V copy and first dP^T in place of "dP(i+1)", so the tensor
+    // pipe runs on while item n's dK / dV are read out by the drain warpgroup; item n+1's first dV
+    // (which overwrites them) waits for acc_free.
+    constexpr uint32_t idSP = idesc_bf16(128, kBQ, 0, 0);   // K/V (TMEM) x Q/dO^T (K-major)
+    constexpr uint32_t idVK = idesc_bf16(128, 128, 0, 1);   // P^T/dS^T (K-major) x dO/Q (MN-major)
+    constexpr uint32_t idQ = idesc_bf16(128, kBQ, 1, 1);    // K^T (MN-major) x dS^T (MN-major)
+    const uint32_t sm0 = warp_uniform(smem_u32(smem));
+    const uint32_t tm = warp_uniform(tmem);
+    const uint32_t qs0 = sm0 + kOffQS, ds0 = sm0 + kOffDS;
+    auto issue_S = [&](uint32_t Gi) {
+      const uint32_t qb = qs0 + (Gi % kQStages) * 2 * kQTile;
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          const uint32_t offk = (kk >> 2) * kKVChunk + (kk & 3) * 32;
-          const uint32_t offq = (kk >> 2) * kQChunk + (kk & 3) * 32;
-          if constexpr (kKT)
-            mma_ts_w(tm + kColS, tm + kColK + 8 * kk, sdesc(qb + offq, 16, 1024), idSP, kk > 0);
-          else
-            mma_ss_w(tm + kColS + 64 * b, sdesc(kb_s + offk, 16, 1024), sdesc(qb + offq, 16, 1024), idSP, kk > 0);
-        }
-        return ob;
-      };
-      auto issue_dP = [&](int it) {
-        const int s = it % kQStages;
-        const uint32_t ob = qs0 + s * 2 * kQTile + kQTile;
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          const uint32_t offk = (kk >> 2) * kKVChunk + (kk & 3) * 32;
-          const uint32_t offq = (kk >> 2) * kQChunk + (kk & 3) * 32;
-          if constexpr (kVT)
-            mma_ts_w(tm + kColP, tm + kColV + 8 * kk, sdesc(ob + offq, 16, 1024), idSP, kk > 0);
-          else
-            mma_ss_w(tm + kColP, sdesc(vb_s + offk, 16, 1024), sdesc(ob + offq, 16, 1024), idSP, kk > 0);
-        }
-      };
-      // dQ^T = K^T dS^T   (A: K MN-major, LBO = 16 KB d-chunk; B: dS^T MN-major, one 64-wide group)
-      auto issue_dQ = [&](uint32_t dsb) {
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          mma_ss_w(tm + kColQ, sdesc(kb_s + kk * 2048, kKVChunk, 1024), sdesc(dsb + kk * 2048, kDSTile, 1024),
-                   idQ, kk > 0);
-      };
-      // dK += dS^T Q   (A: dS^T K-major 128 x 64 in smem; B: Q MN-major)
-      auto issue_dK = [&](uint32_t dsb, uint32_t qb, int it) {
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-          mma_ss_w(tm + kColDK, sdesc(dsb + kk * 32, 16, 1024), sdesc(qb + kk * 2048, kQChunk, 1024), idVK,
-                   (it > 0 || kk > 0) ? 1u : 0u);
-      };
-      long long w_sm = 0, w_dq = 0, w_q = 0, t_start = TT_CLK();
-      mbar_wait(kv_full, 0);
-      // prologue: S(0) -> s_full[0], dP(0) -> dp_full, S(1) -> s_full[1]
-      mbar_wait(&q_full[0], 0);
-      if constexpr (kKT) mbar_wait(k_tmem, 0);
-      tc_fence_after();
-      issue_SP(0);
-      mma_commit_w(&s_full[0]);
-      issue_dP(0);
-      mma_commit_w(dp_full);
-      if (!kKT && n_it > 1) {
-        mbar_wait(&q_full[1], 0);
-        tc_fence_after();
-        issue_SP(1);
-        mma_commit_w(&s_full[1]);
+      for (int kk = 0; kk < 8; ++kk) {
+        const uint32_t offq = (kk >> 2) * kQChunk + (kk & 3) * 32;
+        mma_ts_w(tm + kColS, tm + kColK + 8 * kk, sdesc(qb + offq, 16, 1024), idSP, kk > 0);
       }
-      // Per tile i the element-wise warps run two phases: P (needs S^T(i) only) then dS (needs
-      // dP^T(i)).  Each product is issued as soon as its operand is ready, so the tensor pipe works
-      // on tile i's dV / dK / dQ and tile i+1's dP / tile i+2's S while the warps run phase P of the
-      // next tile, and the warps never wait for a product issued after their previous tile finished.
+    };
+    auto issue_dP = [&](uint32_t Gi) {
+      const uint32_t ob = qs0 + (Gi % kQStages) * 2 * kQTile + kQTile;
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        const uint32_t offq = (kk >> 2) * kQChunk + (kk & 3) * 32;
+        mma_ts_w(tm + kColP, tm + kColV + 8 * kk, sdesc(ob + offq, 16, 1024), idSP, kk > 0);
+      }
+    };
+    // K or V (128 keys x 128 dims, SWIZZLE_128B K-major in shared memory) -> TMEM (TS-MMA A layout)
+    auto copy_in = [&](uint32_t col, uint32_t src) {
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk)
+        tmem_cp_w(tm + col + 8 * kk, sdesc(src + (kk >> 2) * kKVChunk + (kk & 3) * 32, 16, 1024));
+    };
+    // dQ^T = K^T dS^T   (A: K MN-major, LBO = 16 KB d-chunk; B: dS^T MN-major, one 64-wide group)
+    auto issue_dQ = [&](uint32_t ksb, uint32_t dsb) {
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk)
+        mma_ss_w(tm + kColQ, sdesc(ksb + kk * 2048, kKVChunk, 1024), sdesc(dsb + kk * 2048, kDSTile, 1024),
+                 idQ, kk > 0);
+    };
+    // dK += dS^T Q   (A: dS^T K-major 128 x 64 in smem; B: Q MN-major)
+    auto issue_dK = [&](uint32_t dsb, uint32_t qb, int it) {
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk)
+        mma_ss_w(tm + kColDK, sdesc(dsb + kk * 32, 16, 1024), sdesc(qb + kk * 2048, kQChunk, 1024), idVK,
+                 (it > 0 || kk > 0) ? 1u : 0u);
+    };
+    long long w_sm = 0, w_dq = 0, w_q = 0, w_item = 0, t_start = TT_CLK();
+    uint32_t G = 0;  // query tiles consumed so far (all items)
+    int n_items = 0;
+    mbar_wait(&item_full[0], 0);
+    int4 cur = info[0];
+    mbar_arrive(&item_empty[0]);
+    // item 0: K, V -> TMEM, S(0), dP(0)
+    mbar_wait(k_full, 0);
+    tc_fence_after();
+    copy_in(kColK, sm0 + 0 * kKVTile);
+    mbar_wait(&q_full[0], 0);
+    tc_fence_after();
+    issue_S(0);
+    mma_commit_w(s_full);
+    mbar_wait(v_full, 0);
+    tc_fence_after();
+    copy_in(kColV, sm0 + 1 * kKVTile);
+    mma_commit_w(v_free);
+    issue_dP(0);
+    mma_commit_w(dp_full);
+    for (int n = 0;; ++n) {
+      const int n_it = cur.w * p.g;
+      const uint32_t ksb = sm0 + (n & 1) * kKVTile;  // this item's K slot
+      int4 nxt = make_int4(-1, 0, 0, 0);
+      ++n_items;
       for (int it = 0; it < n_it; ++it) {
-        const int s = it % kQStages, b = it & 1;
+        const uint32_t Gi = G + (uint32_t)it;
+        const uint32_t s = Gi % kQStages;
         const uint32_t qb = qs0 + s * 2 * kQTile;
         const uint32_t ob = qb + kQTile;
-        const uint32_t dsb = ds0 + b * kDSTile;
-        const int pb = kKT ? 0 : b;
-        { long long t0 = TT_CLK(); mbar_wait(&p_ready[pb], kKT ? (it & 1) : ((it >> 1) & 1)); w_sm += TT_CLK() - t0; }
+        const uint32_t dsb = ds0 + (Gi & 1) * kDSTile;
+        const bool last = it + 1 == n_it;
+        { long long t0 = TT_CLK(); mbar_wait(p_ready, Gi & 1); w_sm += TT_CLK() - t0; }
+        if (it == 0 && n > 0) {  // the drain warpgroup has read item n-1's dK / dV out of TMEM
+          const long long t0 = TT_CLK();
+          mbar_wait(acc_free, (n - 1) & 1);
+          w_item += TT_CLK() - t0;
+        }
         tc_fence_after();
-        // dV += P^T dO   (A: P^T bf16 in TMEM over S^T[b]; B: dO MN-major, LBO = 8 KB d-chunk)
+        // dV += P^T dO   (A: P^T bf16 in TMEM over S^T; B: dO MN-major, LBO = 8 KB d-chunk)
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)  // P^T of query columns 16 kk.. : warpgroup 16 kk / kCW packed it at its own S^T columns
-          mma_ts_w(tm + kColDV, tm + kColS + 64 * pb + kCW * ((16 * kk) / kCW) + 8 * (((16 * kk) % kCW) / 16),
-                   sdesc(ob + kk * 2048, kQChunk, 1024),
-                   idVK, (it > 0 || kk > 0) ? 1u : 0u);
-        // KTMEM: the single S^T buffer takes S^T(it+1) right after dV(it) has read P^T(it) from it
-        if (kKT && it + 1 < n_it) {
-          { long long t0 = TT_CLK(); mbar_wait(&q_full[(it + 1) % kQStages], ((it + 1) / kQStages) & 1); w_q += TT_CLK() - t0; }
-          tc_fence_after();
-          issue_SP(it + 1);
-          mma_commit_w(&s_full[0]);
-        }
-        if constexpr (kVT) {
-          // dS^T(it) ready (the warps have also read dP^T(it)): dQ^T(it) into the dP^T columns first (the
-          // drain reads it while dK(it) runs), then dP^T(it+1) once the drain has released the columns
-          { long long t0 = TT_CLK(); mbar_wait(&ds_ready[b], (it >> 1) & 1); w_sm += TT_CLK() - t0; }
-          tc_fence_after();
-          issue_dQ(dsb);
-          mma_commit_w(&dq_full[0]);
-          const bool dk_first = !(dev_dbg(p.order) & 1);  // dev A/B (TT_BWD_ORDER=1): dP(i+1) before dK(i)
-          if (dk_first) {
-            issue_dK(dsb, qb, it);
-            mma_commit_w(&q_empty[s]);
-          }
-          if (it + 1 < n_it) {
-            { long long t0 = TT_CLK(); mbar_wait(&dq_free[0], it & 1); w_dq += TT_CLK() - t0; }
+          mma_ts_w(tm + kColDV, tm + kColS + kCW * ((16 * kk) / kCW) + 8 * (((16 * kk) % kCW) / 16),
+                   sdesc(ob + kk * 2048, kQChunk, 1024), idVK, (it > 0 || kk > 0) ? 1u : 0u);
+        // the single S^T buffer takes the next tile's S^T right after dV(i) has read P^T(i) from it
+        if (last) {
+          mbar_wait(&item_full[(n + 1) & 1], ((n + 1) >> 1) & 1);
+          nxt = info[(n + 1) & 1];
+          mbar_arrive(&item_empty[(n + 1) & 1]);
+          if (nxt.x >= 0) {  // item n+1's K -> TMEM (item n's S^T MMAs, its readers, are complete)
+            const long long t0 = TT_CLK();
+            mbar_wait(k_full, (n + 1) & 1);
+            w_item += TT_CLK() - t0;
             tc_fence_after();
-            issue_dP(it + 1);
-            mma_commit_w(dp_full);
+            copy_in(kColK, sm0 + ((n + 1) & 1) * kKVTile);
           }
-          if (!dk_first) {
-            issue_dK(dsb, qb, it);
-            mma_commit_w(&q_empty[s]);
-          }
-          continue;
         }
-        // next tile's dP^T (single buffer) as soon as the warps have read dP^T(it)
-        if (it + 1 < n_it) {
-          { long long t0 = TT_CLK(); mbar_wait(dp_free, it & 1); w_sm += TT_CLK() - t0; }
+        if (!last || nxt.x >= 0) {
+          { long long t0 = TT_CLK(); mbar_wait(&q_full[(Gi + 1) % kQStages], ((Gi + 1) / kQStages) & 1); w_q += TT_CLK() - t0; }
           tc_fence_after();
-          issue_dP(it + 1);
+          issue_S(Gi + 1);
+          mma_commit_w(s_full);
+        }
+        // dS^T(i) ready (the warps have also read dP^T(i)): dQ^T(i) into the dP^T columns first (the
+        // drain reads it while dK(i) runs), then the next dP^T once the drain has released the columns
+        { long long t0 = TT_CLK(); mbar_wait(&ds_ready[Gi & 1], (Gi >> 1) & 1); w_sm += TT_CLK() - t0; }
+        tc_fence_after();
+        issue_dQ(ksb, dsb);
+        mma_commit_w(dq_full);
+        if (last) mma_commit_w(k_free);  // the item's last reader of K in shared memory
+        issue_dK(dsb, qb, it);
+        mma_commit_w(&q_empty[s]);
+        if (last) mma_commit_w(acc_done);  // item n's dK / dV final
+        if (last && nxt.x >= 0) {  // item n+1's V -> TMEM (item n's dP^T MMAs, its readers, are complete)
+          const long long t0 = TT_CLK();
+          mbar_wait(v_full, (n + 1) & 1);
+          w_item += TT_CLK() - t0;
+          tc_fence_after();
+          copy_in(kColV, sm0 + (n & 1) * kKVTile);
+          mma_commit_w(v_free);
+        }
+        if (!last || nxt.x >= 0) {
+          { long long t0 = TT_CLK(); mbar_wait(dq_free, Gi & 1); w_dq += TT_CLK() - t0; }
+          tc_fence_after();
+          issue_dP(Gi + 1);
           mma_commit_w(dp_full);
         }
-        { long long t0 = TT_CLK(); mbar_wait(&ds_ready[b], (it >> 1) & 1); w_sm += TT_CLK() - t0; }
-        tc_fence_after();
-        issue_dK(dsb, qb, it);
-        if (it > 0) {
-          { long long t0 = TT_CLK(); mbar_wait(&dq_free[0], (it - 1) & 1); w_dq += TT_CLK() - t0; }
-          tc_fence_after();
-        }
-        issue_dQ(dsb);
-        mma_commit_w(&dq_full[0]);
-        mma_commit_w(&q_empty[s]);
-        // S^T(it+2) into S^T[b] (in issue order after dV(it) read P^T(it) from it)
-        if (!kKT && it + 2 < n_it) {
-          { long long t0 = TT_CLK(); mbar_wait(&q_full[(it + 2) % kQStages], ((it + 2) / kQStages) & 1); w_q += TT_CLK() - t0; }
-          tc_fence_after();
-          issue_SP(it + 2);
-          mma_commit_w(&s_full[b]);
-        }
       }
-      mma_commit_w(acc_done);
-      if ((dev_dbg(p.dbg) & 8) && lane == 0) {
-        atomicAdd(&g_bwd_dbg[0], (unsigned long long)(TT_CLK() - t_start));
-        atomicAdd(&g_bwd_dbg[1], (unsigned long long)w_sm);
-        atomicAdd(&g_bwd_dbg[2], (unsigned long long)w_dq);
-        atomicAdd(&g_bwd_dbg[3], (unsigned long long)w_q);
-        atomicAdd(&g_bwd_dbg[4], (unsigned long long)n_it);
-      }
+      G += (uint32_t)n_it;
+      if (nxt.x < 0) break;
+      cur = nxt;
+    }
+    if ((dev_dbg(p.dbg) & 8) && lane == 0) {
+      atomicAdd(&g_bwd_dbg[0], (unsigned long long)(TT_CLK() - t_start));
+      atomicAdd(&g_bwd_dbg[1], (unsigned long long)w_sm);
+      atomicAdd(&g_bwd_dbg[2], (unsigned long long)w_dq);
+      atomicAdd(&g_bwd_dbg[3], (unsigned long long)w_q);
+      atomicAdd(&g_bwd_dbg[4], (unsigned long long)G);
+      atomicAdd(&g_bwd_dbg[14], (unsigned long long)w_item);
+      atomicAdd(&g_bwd_dbg[15], (unsigned long long)n_items);
     }
   } else if (warp >= kDrainWarp0) {
-    // ===================== dQ drain warpgroup =====================
+    // ===================== dQ drain warpgroup (+ each item's dK / dV epilogue) =====================
     const int q4 = warp & 3;
-    const int r = q4 * 32 + lane;                      // head-dim lane of dQ^T
+    const int r = q4 * 32 + lane;                      // head-dim lane of dQ^T; key row of dK / dV
     const uint32_t tl = tmem + ((uint32_t)(q4 * 32) << 16);
+    const int Nn = (int)p.N;
     long long c_wd = 0, c_dr = 0;
-    if constexpr (kKT) {
-      // K row (key k0 + r) -> TMEM lane r, columns kColK.. as packed bf16 pairs along d: the A-operand
-      // layout of a TS MMA (same packing as P^T)
-      const int64_t jr = k0 + r;
-      uint32_t kv[64];
-      if (jr < p.N) {
-        const uint4* src = reinterpret_cast<const uint4*>(p.kmat + (jr * p.hkv + hk) * kD);
+    uint32_t G = 0;
+    for (int n = 0;; ++n) {
+      mbar_wait(&item_full[n & 1], (n >> 1) & 1);
+      const int4 cur = info[n & 1];
+      mbar_arrive(&item_empty[n & 1]);
+      if (cur.x < 0) break;
+      const int nq = cur.w, n_it = nq * p.g;
+      Walk wk;
+      for (int it = 0; it < n_it; ++it, ++G) {
+        int h, q0;
+        wk.next(p, nq, cur.y, cur.z, h, q0);
+        { long long t0 = TT_CLK(); mbar_wait_role(dq_full, G & 1, dev_dbg(p.wait) & 2); c_wd += TT_CLK() - t0; }
+        long long t_dr = TT_CLK();
+        tc_fence_after();
+        uint32_t v0[32], v1[32];
+        tmem_ld32(tl + kColQ, v0);
+        tmem_ld32(tl + kColQ + 32, v1);
+        tmem_wait_ld();
+        tc_fence_before();
+        mbar_arrive(dq_free);
+        if (dev_dbg(p.dbg) & 1) continue;
 #pragma unroll
-        for (int u = 0; u < 16; ++u) {
-          const uint4 x = src[u];
-          kv[4 * u] = x.x; kv[4 * u + 1] = x.y; kv[4 * u + 2] = x.z; kv[4 * u + 3] = x.w;
-        }
-      } else {
+        for (int hh = 0; hh < 2; ++hh) {
+          // stage hh holds query rows [q0 + 32 hh, +32) x 128 dims ([row][dim], scaled fp32); its previous
+          // reduction (one half-tile earlier in issue order) must have finished reading it
+          float* stg = reinterpret_cast<float*>(smem + kOffDQ + hh * kDQStage);
+          if (r == 0) bulk_wait_read<1>();
+          named_bar_sync(1, 128);
+          const uint32_t* vv = hh ? v1 : v0;
 #pragma unroll
-        for (int u = 0; u < 64; ++u) kv[u] = 0u;
-      }
-      tmem_st32(tl + kColK, *reinterpret_cast<const uint32_t(*)[32]>(&kv[0]));
-      tmem_st32(tl + kColK + 32, *reinterpret_cast<const uint32_t(*)[32]>(&kv[32]));
-      if constexpr (kVT) {
-        // V row (key k0 + r) -> TMEM lane r, columns kColV.. (A operand of the TS MMA dP^T = V dO^T)
-        tmem_wait_st();
-        if (jr < p.N) {
-          const uint4* src = reinterpret_cast<const uint4*>(p.vmat + (jr * p.hkv + hk) * kD);
-#pragma unroll
-          for (int u = 0; u < 16; ++u) {
-            const uint4 x = src[u];
-            kv[4 * u] = x.x; kv[4 * u + 1] = x.y; kv[4 * u + 2] = x.z; kv[4 * u + 3] = x.w;
+          for (int c = 0; c < 32; ++c) stg[c * kD + r] = __uint_as_float(vv[c]) * p.scale;
+          fence_proxy_async_smem();
+          named_bar_sync(1, 128);
+          if (r == 0) {
+            if (!(dev_dbg(p.dbg) & 32)) tma_reduce_add_3d(&tmdQ, stg, 0, h, q0 + 32 * hh);  // dbg 32: staging only
+            bulk_commit();
           }
         }
-        tmem_st32(tl + kColV, *reinterpret_cast<const uint32_t(*)[32]>(&kv[0]));
-        tmem_st32(tl + kColV + 32, *reinterpret_cast<const uint32_t(*)[32]>(&kv[32]));
-      }
-      tmem_wait_st();
-      tc_fence_before();
-      mbar_arrive(k_tmem);
-    }
-    Walk wk;
-    for (int it = 0; it < n_it; ++it) {
-      int h, q0;
-      bwd_item(p, it, wk, nq, qt0, hk, h, q0);
-      { long long t0 = TT_CLK(); mbar_wait_role(&dq_full[0], it & 1, dev_dbg(p.wait) & 2); c_wd += TT_CLK() - t0; }
-      long long t_dr = TT_CLK();
-      tc_fence_after();
-      uint32_t v0[32], v1[32];
-      tmem_ld32(tl + kColQ, v0);
-      tmem_ld32(tl + kColQ + 32, v1);
-      tmem_wait_ld();
-      tc_fence_before();
-      mbar_arrive(&dq_free[0]);
-      if (dev_dbg(p.dbg) & 1) continue;
-      if (dev_dbg(p.dbg) & 16) {
-        // variant: coalesced fp32 REDs straight from registers (a warp instruction covers 32
-        // consecutive head dims of one query row = 128 contiguous bytes); no shared-memory staging
-        float* base = p.dq_acc + ((int64_t)q0 * p.hq + h) * kD + r;
-        const int64_t rs = (int64_t)p.hq * kD;
-        const int nv = (int)imin64(64, p.N - q0);
-#pragma unroll
-        for (int c = 0; c < 32; ++c)
-          if (c < nv) red_add_f32(base + c * rs, __uint_as_float(v0[c]) * p.scale);
-#pragma unroll
-        for (int c = 0; c < 32; ++c)
-          if (32 + c < nv) red_add_f32(base + (32 + c) * rs, __uint_as_float(v1[c]) * p.scale);
         c_dr += TT_CLK() - t_dr;
-        continue;
       }
+      // ---- item epilogue: key row r's dV and dK (scaled) -> bf16 (a6: fp64 sums of squares of the
+      //      stored values, fp32 per 8).  acc_free is arrived on once every TMEM read is done, before
+      //      the stores drain, so item n+1's first dV / dK MMAs wait only for the reads. ----
+      mbar_wait_role(acc_done, n & 1, dev_dbg(p.wait) & 4);
+      tc_fence_after();
+      const int j = cur.y * 128 + r;
+      double sq[2] = {0.0, 0.0};
 #pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
-        // stage hh holds query rows [q0 + 32 hh, +32) x 128 dims ([row][dim], scaled fp32); its previous
-        // reduction (one half-tile earlier in issue order) must have finished reading it
-        float* stg = reinterpret_cast<float*>(smem + kOffDQ + hh * kDQStage);
-        if (r == 0) bulk_wait_read<1>();
-        named_bar_sync(1, 128);
-        const uint32_t* vv = hh ? v1 : v0;
-#pragma unroll
-        for (int c = 0; c < 32; ++c) stg[c * kD + r] = __uint_as_float(vv[c]) * p.scale;
-        fence_proxy_async_smem();
-        named_bar_sync(1, 128);
-        if (r == 0) {
-          const int hint = dev_dbg(p.l2hint);
-          if (dev_dbg(p.dbg) & 32) {
-            // dbg 32: staging only
-          } else if (hint & 3) {
-            tma_reduce_add_3d_hint(&tmdQ, stg, 0, h, q0 + 32 * hh, (hint & 1) ? policy_evict_last() : policy_evict_first());
-          } else {
-            tma_reduce_add_3d(&tmdQ, stg, 0, h, q0 + 32 * hh);
+      for (int tsr = 0; tsr < 2; ++tsr) {  // 0 = dV (columns 0-127), 1 = dK (128-255)
+        const float mul = tsr == 0 ? 1.f : p.scale;
+        __nv_bfloat16* dst = (tsr == 0 ? p.dv : p.dk) + ((int64_t)j * p.hkv + cur.z) * kD;
+#pragma unroll 1
+        for (int cc = 0; cc < 4; ++cc) {
+          uint32_t ov[32];
+          tmem_ld32(tl + kColDV + 128 * tsr + 32 * cc, ov);
+          tmem_wait_ld();
+          if (tsr == 1 && cc == 3) {
+            tc_fence_before();
+            mbar_arrive(acc_free);
           }
-          bulk_commit();
+          if (j < Nn) {
+            uint32_t pk[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u)
+              pk[u] = pack_bf16(__uint_as_float(ov[2 * u]) * mul, __uint_as_float(ov[2 * u + 1]) * mul);
+            uint4* d4 = reinterpret_cast<uint4*>(dst + 32 * cc);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) d4[u] = make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+            if (p.part_kv) {
+#pragma unroll
+              for (int u8 = 0; u8 < 4; ++u8) {
+                float s8 = 0.f;
+#pragma unroll
+                for (int u = 4 * u8; u < 4 * u8 + 4; ++u) {
+                  const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&pk[u]));
+                  s8 = fmaf(f.x, f.x, fmaf(f.y, f.y, s8));
+                }
+                sq[tsr] += (double)s8;
+              }
+            }
+          }
         }
       }
-      c_dr += TT_CLK() - t_dr;
+      if (p.part_kv) {
+        // fixed-order reduction over the item's 128 key rows -> one fp64 partial per (item, tensor)
+        double (*red)[4] = reinterpret_cast<double (*)[4]>(smem + kOffRed);
+        for (int t2 = 0; t2 < 2; ++t2)
+          for (int o = 16; o > 0; o >>= 1) sq[t2] += __shfl_xor_sync(0xffffffffu, sq[t2], o);
+        if (lane == 0) { red[0][q4] = sq[0]; red[1][q4] = sq[1]; }
+        named_bar_sync(2, 128);
+        if (r == 0)
+          for (int t2 = 0; t2 < 2; ++t2)
+            p.part_kv[2 * (int64_t)cur.x + t2] = ((red[t2][0] + red[t2][1]) + red[t2][2]) + red[t2][3];
+      }
     }
     if (r == 0) bulk_wait<0>();
     if ((dev_dbg(p.dbg) & 8) && r == 0) {
@@ -530,137 +581,140 @@ __global__ void __maxnreg__(kNWG == 4 ? 80 : 128)  // 22 warps: 6 per SMSP x 80 
   } else {
     // ===================== element-wise warps 2 .. kDrainWarp0-1 =====================
     // kNWG warpgroups share every TMEM lane quadrant (lane quadrant = warp % 4): warpgroup wg owns
-    // query columns [kCW wg, kCW wg + kCW) of each 64-row tile.  One thread = one key row.  Measured
-    // (role counters, profiles/r1f_bwd_counters_ktmem.txt): with 2 warpgroups (32 columns per thread)
-    // these warps were busy ~85% of a tile and latency-bound; 4 warpgroups halve each thread's chain.
+    // query columns [kCW wg, kCW wg + kCW) of each 64-row tile.  One thread = one key row.
     const int wg = (warp - 2) >> 2;
     const int q4 = warp & 3;
     const int r = q4 * 32 + lane;
-    const int j = (int)k0 + r;
     const int Nn = (int)p.N;
     const uint32_t tl = tmem + ((uint32_t)(q4 * 32) << 16);
-    const int Ej = (j < Nn) ? p.E[j] : -1;
     const float sl2 = p.scale_log2;
     constexpr uint32_t kFull = kCW == 32 ? 0xffffffffu : ((1u << kCW) - 1u);
     long long c_ws = 0, c_el = 0, c_ld = 0, c_math = 0, c_st = 0;
-    Walk wk;
-    for (int it = 0; it < n_it; ++it) {
-      const int s = it % kQStages, b = it & 1;
-      int h_unused, q0;
-      bwd_item(p, it, wk, nq, qt0, hk, h_unused, q0);
-      const int sb = kKT ? 0 : b;
-      { long long t0 = TT_CLK(); mbar_wait_role(&s_full[sb], kKT ? (it & 1) : ((it >> 1) & 1), dev_dbg(p.wait) & 2); c_ws += TT_CLK() - t0; }
-      tc_fence_after();
-      long long t_el = TT_CLK();
-      if (dev_dbg(p.dbg) & 4) {
-        tc_fence_before();
-        mbar_arrive(&p_ready[sb]);
-        mbar_wait(dp_full, it & 1);
+    uint32_t G = 0;
+    for (int n = 0;; ++n) {
+      mbar_wait(&item_full[n & 1], (n >> 1) & 1);
+      const int4 cur = info[n & 1];
+      mbar_arrive(&item_empty[n & 1]);
+      if (cur.x < 0) break;
+      const int kb = cur.y, hk = cur.z, nq = cur.w, n_it = nq * p.g;
+      const int j = kb * 128 + r;
+      const int Ej = (j < Nn) ? p.E[j] : -1;
+      Walk wk;
+      for (int it = 0; it < n_it; ++it, ++G) {
+        const int s = (int)(G % kQStages), b = (int)(G & 1);
+        int h_unused, q0;
+        wk.next(p, nq, kb, hk, h_unused, q0);
+        { long long t0 = TT_CLK(); mbar_wait_role(s_full, G & 1, dev_dbg(p.wait) & 2); c_ws += TT_CLK() - t0; }
         tc_fence_after();
-        tc_fence_before();
-        if constexpr (!kVT) mbar_arrive(dp_free);
-        mbar_arrive(&ds_ready[b]);
-      } else {
-        const float4* st_lse = reinterpret_cast<const float4*>(smem + kOffStats + s * kStatBytes);
-        const float4* st_D = reinterpret_cast<const float4*>(smem + kOffStats + s * kStatBytes + 256);
-        const float4* st_w = reinterpret_cast<const float4*>(smem + kOffStats + s * kStatBytes + 512);
-        const int c0 = q0 + kCW * wg;
-        // allowed query columns of this key form one interval: [max(j, c0), min(E_j, N)) - c0
-        const int lo = max(j - c0, 0), hi = min(min(Ej, Nn) - c0, kCW);
-        const uint32_t cmask = (hi <= lo) ? 0u : ((hi >= kCW ? kFull : ((1u << hi) - 1u)) & ~((1u << lo) - 1u));
-        const bool all_in = __all_sync(0xffffffffu, cmask == kFull);
-        const float2 SL = make_float2(sl2, sl2);
-        // ---- phase P (S^T only): pw = w P, P^T -> TMEM as bf16 ----
-        float2 pw[kCW / 2];
-        {
-          uint32_t sv[kCW], pwk[kCW / 2];
-          long long tA = TT_CLK();
-          if constexpr (kCW == 32)
-            tmem_ld32(tl + kColS + 64 * sb + kCW * wg, *reinterpret_cast<uint32_t(*)[32]>(&sv[0]));
-          else
-            tmem_ld16(tl + kColS + 64 * sb + kCW * wg, *reinterpret_cast<uint32_t(*)[16]>(&sv[0]));
-          tmem_wait_ld();
-          c_ld += TT_CLK() - tA;
-          tA = TT_CLK();
+        long long t_el = TT_CLK();
+        if (dev_dbg(p.dbg) & 4) {
+          tc_fence_before();
+          mbar_arrive(p_ready);
+          mbar_wait(dp_full, G & 1);
+          tc_fence_after();
+          tc_fence_before();
+          mbar_arrive(&ds_ready[b]);
+        } else {
+          const float4* st_lse = reinterpret_cast<const float4*>(smem + kOffStats + s * kStatBytes);
+          const float4* st_D = reinterpret_cast<const float4*>(smem + kOffStats + s * kStatBytes + 256);
+          const float4* st_w = reinterpret_cast<const float4*>(smem + kOffStats + s * kStatBytes + 512);
+          const int c0 = q0 + kCW * wg;
+          // allowed query columns of this key form one interval: [max(j, c0), min(E_j, N)) - c0
+          const int lo = max(j - c0, 0), hi = min(min(Ej, Nn) - c0, kCW);
+          const uint32_t cmask = (hi <= lo) ? 0u : ((hi >= kCW ? kFull : ((1u << hi) - 1u)) & ~((1u << lo) - 1u));
+          const bool all_in = __all_sync(0xffffffffu, cmask == kFull);
+          const float2 SL = make_float2(sl2, sl2);
+          // ---- phase P (S^T only): pw = w P, P^T -> TMEM as bf16 ----
+          float2 pw[kCW / 2];
+          {
+            uint32_t sv[kCW], pwk[kCW / 2];
+            long long tA = TT_CLK();
+            if constexpr (kCW == 32)
+              tmem_ld32(tl + kColS + kCW * wg, *reinterpret_cast<uint32_t(*)[32]>(&sv[0]));
+            else
+              tmem_ld16(tl + kColS + kCW * wg, *reinterpret_cast<uint32_t(*)[16]>(&sv[0]));
+            tmem_wait_ld();
+            c_ld += TT_CLK() - tA;
+            tA = TT_CLK();
 #pragma unroll
-          for (int c4 = 0; c4 < kCW / 4; ++c4) {
-            const int cg = (kCW / 4) * wg + c4;  // float4 group within the 64 columns
-            const float4 NL = st_lse[cg];  // -LSE * log2e (FOLD: + log2 w)
-            const float4 W = FOLD ? make_float4(1.f, 1.f, 1.f, 1.f) : st_w[cg];
-            const int c = 4 * c4;
-            // P = 2^(s * scale * log2e - LSE2): columns c, c+1 on the MUFU, c+2, c+3 on the FMA pipe
-            const float2 a01 = ffma2(make_float2(__uint_as_float(sv[c]), __uint_as_float(sv[c + 1])), SL, make_float2(NL.x, NL.y));
-            const float2 a23 = ffma2(make_float2(__uint_as_float(sv[c + 2]), __uint_as_float(sv[c + 3])), SL, make_float2(NL.z, NL.w));
-            float2 p01 = make_float2(ex2(a01.x), ex2(a01.y));
+            for (int c4 = 0; c4 < kCW / 4; ++c4) {
+              const int cg = (kCW / 4) * wg + c4;  // float4 group within the 64 columns
+              const float4 NL = st_lse[cg];  // -LSE * log2e (FOLD: + log2 w)
+              const float4 W = FOLD ? make_float4(1.f, 1.f, 1.f, 1.f) : st_w[cg];
+              const int c = 4 * c4;
+              // P = 2^(s * scale * log2e - LSE2): columns c, c+1 on the MUFU, c+2, c+3 on the FMA pipe
+              const float2 a01 = ffma2(make_float2(__uint_as_float(sv[c]), __uint_as_float(sv[c + 1])), SL, make_float2(NL.x, NL.y));
+              const float2 a23 = ffma2(make_float2(__uint_as_float(sv[c + 2]), __uint_as_float(sv[c + 3])), SL, make_float2(NL.z, NL.w));
+              float2 p01 = make_float2(ex2(a01.x), ex2(a01.y));
 #ifndef TT_BWD_POLY
 #define TT_BWD_POLY 1
 #endif
-            // 2 x TT_BWD_POLY of every 8 exponentials run on the FMA pipe
-            float2 p23 = (TT_BWD_POLY == 2 || (TT_BWD_POLY == 1 && (c4 & 1))) ? exp2_poly2(a23)
-                                                                             : make_float2(ex2(a23.x), ex2(a23.y));
-            if (!all_in) {
-              p01.x = ((cmask >> c) & 1u) ? p01.x : 0.f;
-              p01.y = ((cmask >> (c + 1)) & 1u) ? p01.y : 0.f;
-              p23.x = ((cmask >> (c + 2)) & 1u) ? p23.x : 0.f;
-              p23.y = ((cmask >> (c + 3)) & 1u) ? p23.y : 0.f;
+              // 2 x TT_BWD_POLY of every 8 exponentials run on the FMA pipe
+              float2 p23 = (TT_BWD_POLY == 2 || (TT_BWD_POLY == 1 && (c4 & 1))) ? exp2_poly2(a23)
+                                                                               : make_float2(ex2(a23.x), ex2(a23.y));
+              if (!all_in) {
+                p01.x = ((cmask >> c) & 1u) ? p01.x : 0.f;
+                p01.y = ((cmask >> (c + 1)) & 1u) ? p01.y : 0.f;
+                p23.x = ((cmask >> (c + 2)) & 1u) ? p23.x : 0.f;
+                p23.y = ((cmask >> (c + 3)) & 1u) ? p23.y : 0.f;
+              }
+              if constexpr (FOLD) {
+                pw[2 * c4] = p01;
+                pw[2 * c4 + 1] = p23;
+              } else {
+                pw[2 * c4] = fmul2(p01, make_float2(W.x, W.y));
+                pw[2 * c4 + 1] = fmul2(p23, make_float2(W.z, W.w));
+              }
+              pwk[2 * c4] = pack_bf16(pw[2 * c4].x, pw[2 * c4].y);
+              pwk[2 * c4 + 1] = pack_bf16(pw[2 * c4 + 1].x, pw[2 * c4 + 1].y);
             }
-            if constexpr (FOLD) {
-              pw[2 * c4] = p01;
-              pw[2 * c4 + 1] = p23;
-            } else {
-              pw[2 * c4] = fmul2(p01, make_float2(W.x, W.y));
-              pw[2 * c4 + 1] = fmul2(p23, make_float2(W.z, W.w));
+            // P^T (bf16) over this warpgroup's own S^T columns [kCW wg, kCW wg + kCW / 2) — never over
+            // columns another warpgroup may still be reading
+            if constexpr (kCW == 32)
+              tmem_st16(tl + kColS + kCW * wg, pwk);
+            else
+              tmem_st8(tl + kColS + kCW * wg, pwk);
+            tmem_wait_st();
+            tc_fence_before();
+            mbar_arrive(p_ready);
+            c_math += TT_CLK() - tA;
+          }
+          // ---- phase dS (dP^T): dS^T = pw (dP - D) -> smem ----
+          {
+            uint32_t pv[kCW], dsk[kCW / 2];
+            long long tA = TT_CLK();
+            { long long t0 = TT_CLK(); mbar_wait_role(dp_full, G & 1, dev_dbg(p.wait) & 2); c_ws += TT_CLK() - t0; }
+            tc_fence_after();
+            if constexpr (kCW == 32)
+              tmem_ld32(tl + kColP + kCW * wg, *reinterpret_cast<uint32_t(*)[32]>(&pv[0]));
+            else
+              tmem_ld16(tl + kColP + kCW * wg, *reinterpret_cast<uint32_t(*)[16]>(&pv[0]));
+            tmem_wait_ld();
+            tc_fence_before();  // ds_ready (below) also releases dP^T's columns to dQ^T
+#pragma unroll
+            for (int c4 = 0; c4 < kCW / 4; ++c4) {
+              const float4 ND = st_D[(kCW / 4) * wg + c4];  // -D
+              const int c = 4 * c4;
+              const float2 ds01 = fmul2(pw[2 * c4], fadd2(make_float2(__uint_as_float(pv[c]), __uint_as_float(pv[c + 1])), make_float2(ND.x, ND.y)));
+              const float2 ds23 = fmul2(pw[2 * c4 + 1], fadd2(make_float2(__uint_as_float(pv[c + 2]), __uint_as_float(pv[c + 3])), make_float2(ND.z, ND.w)));
+              dsk[2 * c4] = pack_bf16(ds01.x, ds01.y);
+              dsk[2 * c4 + 1] = pack_bf16(ds23.x, ds23.y);
             }
-            pwk[2 * c4] = pack_bf16(pw[2 * c4].x, pw[2 * c4].y);
-            pwk[2 * c4 + 1] = pack_bf16(pw[2 * c4 + 1].x, pw[2 * c4 + 1].y);
-          }
-          // P^T (bf16) over this warpgroup's own S^T columns [kCW wg, kCW wg + kCW / 2) — never over
-          // columns another warpgroup may still be reading
-          if constexpr (kCW == 32)
-            tmem_st16(tl + kColS + 64 * sb + kCW * wg, pwk);
-          else
-            tmem_st8(tl + kColS + 64 * sb + kCW * wg, pwk);
-          tmem_wait_st();
-          tc_fence_before();
-          mbar_arrive(&p_ready[sb]);
-          c_math += TT_CLK() - tA;
-        }
-        // ---- phase dS (dP^T): dS^T = pw (dP - D) -> smem ----
-        {
-          uint32_t pv[kCW], dsk[kCW / 2];
-          long long tA = TT_CLK();
-          { long long t0 = TT_CLK(); mbar_wait_role(dp_full, it & 1, dev_dbg(p.wait) & 2); c_ws += TT_CLK() - t0; }
-          tc_fence_after();
-          if constexpr (kCW == 32)
-            tmem_ld32(tl + kColP + kCW * wg, *reinterpret_cast<uint32_t(*)[32]>(&pv[0]));
-          else
-            tmem_ld16(tl + kColP + kCW * wg, *reinterpret_cast<uint32_t(*)[16]>(&pv[0]));
-          tmem_wait_ld();
-          tc_fence_before();
-          if constexpr (!kVT) mbar_arrive(dp_free);  // VTMEM: ds_ready (below) releases dP^T's columns
+            // dS^T row r into the SWIZZLE_128B smem tile: 16-byte chunk c at (c ^ (r & 7))
+            uint8_t* drow = smem + kOffDS + b * kDSTile + r * 128;
 #pragma unroll
-          for (int c4 = 0; c4 < kCW / 4; ++c4) {
-            const float4 ND = st_D[(kCW / 4) * wg + c4];  // -D
-            const int c = 4 * c4;
-            const float2 ds01 = fmul2(pw[2 * c4], fadd2(make_float2(__uint_as_float(pv[c]), __uint_as_float(pv[c + 1])), make_float2(ND.x, ND.y)));
-            const float2 ds23 = fmul2(pw[2 * c4 + 1], fadd2(make_float2(__uint_as_float(pv[c + 2]), __uint_as_float(pv[c + 3])), make_float2(ND.z, ND.w)));
-            dsk[2 * c4] = pack_bf16(ds01.x, ds01.y);
-            dsk[2 * c4 + 1] = pack_bf16(ds23.x, ds23.y);
+            for (int c = 0; c < kCW / 8; ++c) {
+              const int ch = (kCW / 8) * wg + c;
+              *reinterpret_cast<uint4*>(drow + ((ch ^ (r & 7)) << 4)) =
+                  make_uint4(dsk[4 * c], dsk[4 * c + 1], dsk[4 * c + 2], dsk[4 * c + 3]);
+            }
+            fence_proxy_async_smem();
+            mbar_arrive(&ds_ready[b]);
+            c_st += TT_CLK() - tA;
           }
-          // dS^T row r into the SWIZZLE_128B smem tile: 16-byte chunk c at (c ^ (r & 7))
-          uint8_t* drow = smem + kOffDS + b * kDSTile + r * 128;
-#pragma unroll
-          for (int c = 0; c < kCW / 8; ++c) {
-            const int ch = (kCW / 8) * wg + c;
-            *reinterpret_cast<uint4*>(drow + ((ch ^ (r & 7)) << 4)) =
-                make_uint4(dsk[4 * c], dsk[4 * c + 1], dsk[4 * c + 2], dsk[4 * c + 3]);
-          }
-          fence_proxy_async_smem();
-          mbar_arrive(&ds_ready[b]);
-          c_st += TT_CLK() - tA;
         }
+        c_el += TT_CLK() - t_el;
       }
-      c_el += TT_CLK() - t_el;
     }
     if ((dev_dbg(p.dbg) & 8) && r == 0 && wg == 0) {
       atomicAdd(&g_bwd_dbg[5], (unsigned long long)c_ws);
@@ -668,58 +722,6 @@ __global__ void __maxnreg__(kNWG == 4 ? 80 : 128)  // 22 warps: 6 per SMSP x 80 
       atomicAdd(&g_bwd_dbg[9], (unsigned long long)c_ld);
       atomicAdd(&g_bwd_dbg[10], (unsigned long long)c_math);
       atomicAdd(&g_bwd_dbg[11], (unsigned long long)c_st);
-    }
-    // ---- epilogue: the first kNWG/2 warpgroups write dV, the others dK (scaled), each its share of
-    //      this key row's 128 head dims ----
-    mbar_wait_role(acc_done, 0, dev_dbg(p.wait) & 4);
-    tc_fence_after();
-    {
-      constexpr int kPer = kNWG / 2;              // warpgroups per tensor
-      constexpr int kCols = 128 / kPer;           // head dims per warpgroup
-      const int tsr = wg / kPer, part = wg % kPer;  // tensor 0 = dV, 1 = dK
-      const uint32_t col = (tsr == 0 ? kColDV : kColDK) + kCols * part;
-      const float mul = tsr == 0 ? 1.f : p.scale;
-      __nv_bfloat16* dst = (tsr == 0 ? p.dv : p.dk) + ((int64_t)j * p.hkv + hk) * kD + kCols * part;
-      double sq = 0.0;  // a6: sum of squares of the stored (bf16-rounded) values, fp32 per 8 / fp64 across
-#pragma unroll 1
-      for (int cc = 0; cc < kCols / 32; ++cc) {
-        uint32_t ov[32];
-        tmem_ld32(tl + col + 32 * cc, ov);
-        tmem_wait_ld();
-        if (j < Nn) {
-          uint32_t pk[16];
-#pragma unroll
-          for (int u = 0; u < 16; ++u)
-            pk[u] = pack_bf16(__uint_as_float(ov[2 * u]) * mul, __uint_as_float(ov[2 * u + 1]) * mul);
-          uint4* d4 = reinterpret_cast<uint4*>(dst + 32 * cc);
-#pragma unroll
-          for (int u = 0; u < 4; ++u) d4[u] = make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
-          if (p.part_kv) {
-#pragma unroll
-            for (int u8 = 0; u8 < 4; ++u8) {
-              float s8 = 0.f;
-#pragma unroll
-              for (int u = 4 * u8; u < 4 * u8 + 4; ++u) {
-                const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&pk[u]));
-                s8 = fmaf(f.x, f.x, fmaf(f.y, f.y, s8));
-              }
-              sq += (double)s8;
-            }
-          }
-        }
-      }
-      if (p.part_kv) {
-        // fixed-order reduction over the warpgroup's 128 rows -> one fp64 partial per (CTA, tensor)
-        double (*red)[4] = reinterpret_cast<double (*)[4]>(smem + kOffRed);
-        for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
-        if (lane == 0) red[wg][q4] = sq;
-        named_bar_sync(2 + tsr, 128 * kPer);
-        if (r == 0 && part == 0) {
-          double t = 0.0;
-          for (int g2 = tsr * kPer; g2 < (tsr + 1) * kPer; ++g2) t += ((red[g2][0] + red[g2][1]) + red[g2][2]) + red[g2][3];
-          p.part_kv[2 * (int64_t)blockIdx.x + tsr] = t;
-        }
-      }
     }
   }
   tc_fence_before();
@@ -840,14 +842,9 @@ tt_status sm100_attn_bwd(const tt_packed& pk, const void* q, const void* k, cons
     const char* e = dev_getenv("TT_DEBUG_BWD");
     prm.dbg = e ? atoi(e) : 0;
     const char* o = dev_getenv("TT_CTA_ORDER");  // development A/B: bit 1 = bwd head-major
-    const char* wk = dev_getenv("TT_BWD_WALK");
-    prm.walk = wk ? atoi(wk) : 0;
-    const char* od = dev_getenv("TT_BWD_ORDER");
-    prm.order = od ? atoi(od) : 0;
-    const char* lh = dev_getenv("TT_BWD_L2HINT");
-    prm.l2hint = lh ? atoi(lh) : 0;
     const char* wh = dev_getenv("TT_WAIT_HINT");
     prm.wait = wh ? atoi(wh) : 0;
+    prm.steal = dev_getenv("TT_BWD_NOSTEAL") ? 0 : 1;  // development A/B: one item per CTA
     prm.chunk = bwd_cta_chunk(pk, hkv);
     if (o && ((atoi(o) >> 1) & 1)) prm.chunk = pk.n_blk;  // development A/B: head-major
     if (const char* c = dev_getenv("TT_BWD_CHUNK")) prm.chunk = atoi(c) > 0 ? atoi(c) : 1;
@@ -864,8 +861,6 @@ tt_status sm100_attn_bwd(const tt_packed& pk, const void* q, const void* k, cons
   prm.dk = static_cast<__nv_bfloat16*>(dk);
   prm.dv = static_cast<__nv_bfloat16*>(dv);
   prm.part_kv = sqnorm ? part_kv : nullptr;
-  prm.kmat = static_cast<const __nv_bfloat16*>(k);
-  prm.vmat = static_cast<const __nv_bfloat16*>(v);
   auto kern = fold ? tree_attn_bwd_sm100<true> : tree_attn_bwd_sm100<false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
   if (e != cudaSuccess) { set_error("sm100_attn_bwd: smem attribute: %s", cudaGetErrorString(e)); return TT_ERR_CUDA; }

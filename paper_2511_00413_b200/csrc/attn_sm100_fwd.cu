@@ -57,6 +57,9 @@ constexpr uint32_t kOffClc = kOffInfo + 2 * 16;     // cluster-launch-control re
 constexpr uint32_t kOffX = kOffClc + 16;            // row-max exchange [2 parity][2 tiles][2 halves][128] + l [2][2][128]
 constexpr uint32_t kOffTiles = kOffX + (2 * 2 * 2 * 128 + 2 * 2 * 128) * 4;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
+// the next item is claimed (CLC) when the producer loads the current item's k-tile T - kClaimAhead and
+// its tile list built from k-tile T - kPrepareAhead on
+constexpr int kClaimAhead = 5, kPrepareAhead = 3;
 
 __device__ unsigned long long g_fwd_dbg[16];  // development instrumentation (TT_DEBUG_FWD & 8)
 
@@ -92,9 +95,9 @@ __device__ __forceinline__ void fwd_item(const FwdParams& p, int x, int& pair, i
 
 // Persistent over work items: the grid has one CTA per (query-block pair, head) and the hardware
 // launches them in order (heaviest first), but a running CTA takes over the next not-yet-launched CTA's
-// item through cluster launch control (clc_try_cancel) one item ahead, so item n+1's Q / first K/V
-// loads, tile list and first S MMAs overlap item n's last tiles and epilogue instead of a CTA exit,
-// launch, barrier init and TMEM allocation.  Each item's merged tile list is built by the producer warp
+// item through cluster launch control (clc_try_cancel) a few tiles before its current item ends, so
+// item n+1's Q / first K/V loads, tile list and first S MMAs overlap item n's last tiles and epilogue
+// instead of a CTA exit, launch, barrier init and TMEM allocation.  Each item's merged tile list is built by the producer warp
 // into one of two buffers (item_full / item_empty hand them to the MMA and softmax warps).
 __global__ void __launch_bounds__(kFwdThreads, 1)
     tree_attn_fwd_sm100(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
@@ -157,10 +160,6 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       tma_prefetch(&tmQ);
       tma_prefetch(&tmK);
       tma_prefetch(&tmV);
-      if (steal) {  // the next item, one ahead
-        mbar_expect_tx(clc_bar, 16);
-        clc_try_cancel(smem + kOffClc, clc_bar);
-      }
     }
     auto has1_of = [&](int qa) { return qa + 1 < p.nb && !(dev_dbg(p.dbg) & 16); };  // dbg 16: drop query tile 1
     // merged tile list of an item's two query blocks (kb | cls0 << 28 | cls1 << 30, ascending) into
@@ -234,12 +233,22 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     for (int n = 0;; ++n) {
       const int b = n & 1;
       const int32_t* tl = tiles_buf + b * tl_stride;
-      // The next item (claimed one ahead through the CLC) is prepared early — once this item's first
-      // two k-tiles are in flight — so its tile list is ready when this item's MMAs end.
+      // The next item (through the CLC) is prepared while this item's last k-tiles are loaded (the
+      // producer runs ~2 tiles ahead of the MMAs), so its tile list is ready when this item's MMAs end.
+      // (claimed late, a few tiles before this item's end: claiming at an item's start would pair heavy
+      // items on one CTA and unbalance the tail)
       int xn = -1, pair_n = 0, h_n = 0, T_n = 0;
-      bool has1_n = false, prepared = false;
+      bool has1_n = false, claimed = false, prepared = false;
+      auto claim = [&]() {
+        claimed = true;
+        if (steal && lane == 0) {
+          mbar_expect_tx(clc_bar, 16);
+          clc_try_cancel(smem + kOffClc, clc_bar);
+        }
+      };
       auto prepare_next = [&]() {
         prepared = true;
+        if (!claimed) claim();
         if (steal) {
           mbar_wait(clc_bar, clc_ph);
           clc_ph ^= 1;
@@ -247,10 +256,6 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           fence_proxy_async_smem();
           __syncwarp();
           if (xn < 0) steal = false;  // no further request after a failed one
-          else if (lane == 0) {
-            mbar_expect_tx(clc_bar, 16);
-            clc_try_cancel(smem + kOffClc, clc_bar);
-          }
         }
         if (n >= 1) mbar_wait(&item_empty[b ^ 1], ((n - 1) >> 1) & 1);  // item n-1 released buffer b^1
         if (xn < 0) {
@@ -266,7 +271,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         const int s = (int)(g % kStages);
         if (g >= (uint32_t)kStages) mbar_wait_role(&empty[s], ((g / kStages) - 1) & 1, dev_dbg(p.wait) & 1);
         if (lane == 0) load_kv(g, tl[t] & kKbMask, h);
-        if (t >= 1 && !prepared) prepare_next();
+        if (!claimed && t >= T - kClaimAhead) claim();
+        if (!prepared && t >= T - kPrepareAhead) prepare_next();
       }
       if (!prepared) prepare_next();
       if (xn < 0) break;

@@ -226,6 +226,16 @@ __device__ __forceinline__ void mma_commit_w(uint64_t* bar) {
       "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(smem_u32(bar))
       : "memory");
 }
+// tcgen05.cp 128x256b: 128 rows x 32 bytes of a (swizzled, K-major) shared-memory matrix described by
+// `desc` -> TMEM lanes 0-127, 8 columns; the layout a K = 16 step of a TS MMA reads its A operand in.
+// Issued by one elected lane of a converged warp, ordered with that lane's tcgen05.mma instructions.
+__device__ __forceinline__ void tmem_cp_w(uint32_t taddr, uint64_t desc) {
+  asm volatile(
+      "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.cp.cta_group::1.128x256b [%0], %1;\n}\n" ::"r"(taddr),
+      "l"(desc)
+      : "memory");
+}
 __device__ __forceinline__ uint32_t warp_uniform(uint32_t x) { return __shfl_sync(0xffffffffu, x, 0); }
 
 // arrive on `bar` once all previously issued tcgen05.mma of this thread have completed
