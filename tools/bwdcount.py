@@ -10,7 +10,7 @@ for cfg, seed in [("agentic8k", 0), ("deep32k", 1), ("wide", None)]:
     q, k, v = (x.cuda() for x in tensors.qkv_tensors(N, hq, hkv, d, "bf16", seed=0))
     G = tensors.grad_tensor(N, hq, d, "bf16", seed=1).cuda()
     o, lse = tt.tt_attn_fwd(pk, q, k, v)
-    buf = (ctypes.c_ulonglong * 16)()
+    buf = (ctypes.c_ulonglong * 20)()
     tt.tt_attn_bwd(pk, q, k, v, o, lse, G); torch.cuda.synchronize()
     L.tt_debug_bwd_counters(buf, 1)
     tt.tt_attn_bwd(pk, q, k, v, o, lse, G); torch.cuda.synchronize()
@@ -21,3 +21,4 @@ for cfg, seed in [("agentic8k", 0), ("deep32k", 1), ("wide", None)]:
     ni = max(b[15], 1)
     print("   CTAs", b[13], "items", b[15], "mean CTA lifetime %.0f cycles, mean MMA-loop %.0f cycles, loop fraction %.3f, item boundary (MMA: item start -> first S/dP issued) %.0f cycles per later item" %
           (b[12] / b[13], b[0] / b[13], b[0] / b[12], b[14] / max(ni - b[13], 1)), flush=True)
+    print("   item boundary waits per later item: acc_free %.0f  k_full %.0f  v_full %.0f" % tuple(x / max(ni - b[13], 1) for x in b[16:19]), flush=True)
