@@ -15,12 +15,9 @@
 // shared memory with tcgen05.cp; K also stays in shared memory as dQ^T's A operand); dK and dV
 // accumulate in TMEM across all of the item's tiles.
 // Persistent CTAs: the grid has one CTA per item and the hardware launches them in order, but a running
-// CTA takes over the next not-yet-launched CTA's item through cluster launch control a few tiles before
-// its current item ends.  The MMA issuer sees one stream of query tiles: the next item's K copy and
-// first S^T, V copy and first dP^T are issued in the last tile of the current one (K / V alternate
-// between two shared-memory slots), while the drain warpgroup reads the finished dV (during the last
-// tile) and dK out of TMEM (dv_free / dk_free gate the next item's first dV / dK) — no CTA exit, launch
-// or TMEM allocation between items.
+// CTA takes over the next not-yet-launched CTA's item through cluster launch control, one item ahead,
+// so the next item's K/V loads, TMEM copies and first S^T / dP^T MMAs overlap this item's last tiles and
+// its dK/dV epilogue (no CTA exit / launch / TMEM allocation between items).
 //   warp 0     producer: the item scheduler (CLC) and TMA: K, V of each item; per tile Q_i, dO_i
 //              (64 x 128) into a 3-stage ring, plus LSE (log2), D and w of the 64 rows (bulk copies)
 //   warp 1     TMEM allocator + MMA issuer (one elected thread).  Per item: K, V -> TMEM (tcgen05.cp).
@@ -37,8 +34,8 @@
 //   warps 2-9  two warpgroups sharing the 4 TMEM lane quadrants; warpgroup wg owns query columns
 //              [32 wg, 32 wg + 32) of each tile.  Element-wise (one thread per key row): P^T, dS^T
 //              with the tree-scale, P^T -> TMEM (bf16), dS^T -> smem (bf16, SWIZZLE_128B).
-//   warps 10-13 dQ drain warpgroup (one thread per head-dim lane of dQ^T; per item also the dV / dK
-//              epilogue, one thread per key row): per tile it reads the 64
+//              Epilogue of each item: warpgroup 0 writes dV, warpgroup 1 writes dK.
+//   warps 10-13 dQ drain warpgroup (one thread per head-dim lane of dQ^T): per tile it reads the 64
 //              query columns of dQ^T from TMEM, releases the columns to the MMA issuer, and adds them
 //              into the fp32 dQ accumulator through two 16 KB smem stages (32 query rows x 128 fp32
 //              each, [row][dim]) with TMA bulk tensor reductions (cp.reduce.async.bulk.tensor .add.f32).
@@ -91,8 +88,8 @@ constexpr uint32_t kStatBytes = 768;                              // per stage: 
 constexpr uint32_t kOffStats = kOffDQ + 2 * kDQStage;
 constexpr uint32_t kOffBar = kOffStats + kQStages * kStatBytes;
 // k_full, v_full, q_full[3], q_empty[3], s_full, p_ready, ds_ready[2], dq_full, dq_free, dp_full,
-// dv_done, dk_done, dv_free, dk_free, v_free, k_free, item_full[2], item_empty[2], clc
-constexpr uint32_t kNumBars = 2 + 2 * kQStages + 1 + 1 + 2 + 1 + 1 + 1 + 4 + 2 + 4 + 1;
+// acc_done, acc_free, v_free, k_free, item_full[2], item_empty[2], clc
+constexpr uint32_t kNumBars = 2 + 2 * kQStages + 1 + 1 + 2 + 1 + 1 + 1 + 1 + 1 + 2 + 4 + 1;
 // the next item is claimed (CLC) when its producer reaches this many tiles before the current item's
 // end, and published (info + K load) at kPrepareAhead tiles before it
 constexpr int kClaimAhead = 6, kPrepareAhead = 3;
@@ -110,7 +107,7 @@ static_assert(kSmemBytes <= 232448, "backward kernel exceeds 227 KB of shared me
 constexpr uint32_t kColDV = 0, kColDK = 128, kColS = 256, kColK = 320, kColP = 384, kColQ = 384, kColV = 448;
 
 // development instrumentation (TT_DEBUG_BWD & 8): per-role cycle counters summed over CTAs
-__device__ unsigned long long g_bwd_dbg[20];
+__device__ unsigned long long g_bwd_dbg[16];
 
 struct BwdParams {
   int64_t N;
@@ -181,11 +178,9 @@ __global__ void __maxnreg__(kNWG == 4 ? 80 : 128)  // 22 warps: 6 per SMSP x 80 
   uint64_t* dq_full = ds_ready + 2;       // dQ^T(i) in TMEM
   uint64_t* dq_free = dq_full + 1;        // dQ^T(i) read by the drain (128 arrivals)
   uint64_t* dp_full = dq_free + 1;        // dP^T(i) in TMEM
-  uint64_t* dv_done = dp_full + 1;        // the item's dV final (its last dV MMA completed)
-  uint64_t* dk_done = dv_done + 1;        // the item's dK final
-  uint64_t* dv_free = dk_done + 1;        // the item's dV read out of TMEM (128 drain arrivals)
-  uint64_t* dk_free = dv_free + 1;        // the item's dK read out of TMEM (128 drain arrivals)
-  uint64_t* v_free = dk_free + 1;         // the item's V TMEM copy done (V's smem slot free)
+  uint64_t* acc_done = dp_full + 1;       // the item's dK / dV final
+  uint64_t* acc_free = acc_done + 1;      // the item's dK / dV read out of TMEM (128 drain arrivals)
+  uint64_t* v_free = acc_free + 1;        // the item's V TMEM copy done (V's smem slot free)
   uint64_t* k_free = v_free + 1;          // the item's last dQ^T done (K's smem slot free)
   uint64_t* item_full = k_free + 1;       // [2] item info written
   uint64_t* item_empty = item_full + 2;   // [2] item info read (every consumer thread)
@@ -200,9 +195,7 @@ __global__ void __maxnreg__(kNWG == 4 ? 80 : 128)  // 22 warps: 6 per SMSP x 80 
     if (lane == 0) {
       mbar_init(k_full, 1);
       mbar_init(v_full, 1);
-      mbar_init(dv_free, 128);
-      mbar_init(dk_free, 128);
-      mbar_init(dk_done, 1);
+      mbar_init(acc_free, 128);
       for (int s = 0; s < kQStages; ++s) { mbar_init(&q_full[s], 1); mbar_init(&q_empty[s], 1); }
       mbar_init(s_full, 1);
       mbar_init(p_ready, 128 * kNWG);
@@ -210,7 +203,7 @@ __global__ void __maxnreg__(kNWG == 4 ? 80 : 128)  // 22 warps: 6 per SMSP x 80 
       mbar_init(dq_full, 1);
       mbar_init(dq_free, 128);
       mbar_init(dp_full, 1);
-      mbar_init(dv_done, 1);
+      mbar_init(acc_done, 1);
       mbar_init(v_free, 1);
       mbar_init(k_free, 1);
       for (int b = 0; b < 2; ++b) { mbar_init(&item_full[b], 1); mbar_init(&item_empty[b], kConsumerThreads); }
@@ -333,8 +326,8 @@ __global__ void __maxnreg__(kNWG == 4 ? 80 : 128)  // 22 warps: 6 per SMSP x 80 
     // ===================== MMA issuer (whole warp, one elected lane issues) =====================
     // One stream of query tiles across items: the last tile of item n issues item n+1's K copy and
     // first S^T in place of "S(i+1)", and its V copy and first dP^T in place of "dP(i+1)", so the tensor
-    // pipe runs on while item n's dK / dV are read out by the drain warpgroup; item n+1's first dV / dK
-    // (which overwrite them) wait for dv_free / dk_free.
+    // pipe runs on while item n's dK / dV are read out by the drain warpgroup; item n+1's first dV
+    // (which overwrites them) waits for acc_free.
     constexpr uint32_t idSP = idesc_bf16(128, kBQ, 0, 0);   // K/V (TMEM) x Q/dO^T (K-major)
     constexpr uint32_t idVK = idesc_bf16(128, 128, 0, 1);   // P^T/dS^T (K-major) x dO/Q (MN-major)
     constexpr uint32_t idQ = idesc_bf16(128, kBQ, 1, 1);    // K^T (MN-major) x dS^T (MN-major)
@@ -377,7 +370,7 @@ __global__ void __maxnreg__(kNWG == 4 ? 80 : 128)  // 22 warps: 6 per SMSP x 80 
         mma_ss_w(tm + kColDK, sdesc(dsb + kk * 32, 16, 1024), sdesc(qb + kk * 2048, kQChunk, 1024), idVK,
                  (it > 0 || kk > 0) ? 1u : 0u);
     };
-    long long w_sm = 0, w_dq = 0, w_q = 0, w_item = 0, w_af = 0, w_kf = 0, w_vf = 0, t_start = TT_CLK();
+    long long w_sm = 0, w_dq = 0, w_q = 0, w_item = 0, t_start = TT_CLK();
     uint32_t G = 0;  // query tiles consumed so far (all items)
     int n_items = 0;
     mbar_wait(&item_full[0], 0);
@@ -410,11 +403,10 @@ __global__ void __maxnreg__(kNWG == 4 ? 80 : 128)  // 22 warps: 6 per SMSP x 80 
         const uint32_t dsb = ds0 + (Gi & 1) * kDSTile;
         const bool last = it + 1 == n_it;
         { long long t0 = TT_CLK(); mbar_wait(p_ready, Gi & 1); w_sm += TT_CLK() - t0; }
-        if (it == 0 && n > 0) {  // the drain warpgroup has read item n-1's dV out of TMEM
+        if (it == 0 && n > 0) {  // the drain warpgroup has read item n-1's dK / dV out of TMEM
           const long long t0 = TT_CLK();
-          mbar_wait(dv_free, (n - 1) & 1);
+          mbar_wait(acc_free, (n - 1) & 1);
           w_item += TT_CLK() - t0;
-          w_af += TT_CLK() - t0;
         }
         tc_fence_after();
         // dV += P^T dO   (A: P^T bf16 in TMEM over S^T; B: dO MN-major, LBO = 8 KB d-chunk)
@@ -422,7 +414,6 @@ __global__ void __maxnreg__(kNWG == 4 ? 80 : 128)  // 22 warps: 6 per SMSP x 80 
         for (int kk = 0; kk < 4; ++kk)  // P^T of query columns 16 kk.. : warpgroup 16 kk / kCW packed it at its own S^T columns
           mma_ts_w(tm + kColDV, tm + kColS + kCW * ((16 * kk) / kCW) + 8 * (((16 * kk) % kCW) / 16),
                    sdesc(ob + kk * 2048, kQChunk, 1024), idVK, (it > 0 || kk > 0) ? 1u : 0u);
-        if (last) mma_commit_w(dv_done);  // item n's dV final
         // the single S^T buffer takes the next tile's S^T right after dV(i) has read P^T(i) from it
         if (last) {
           mbar_wait(&item_full[(n + 1) & 1], ((n + 1) >> 1) & 1);
@@ -432,7 +423,6 @@ __global__ void __maxnreg__(kNWG == 4 ? 80 : 128)  // 22 warps: 6 per SMSP x 80 
             const long long t0 = TT_CLK();
             mbar_wait(k_full, (n + 1) & 1);
             w_item += TT_CLK() - t0;
-            w_kf += TT_CLK() - t0;
             tc_fence_after();
             copy_in(kColK, sm0 + ((n + 1) & 1) * kKVTile);
           }
@@ -450,21 +440,13 @@ __global__ void __maxnreg__(kNWG == 4 ? 80 : 128)  // 22 warps: 6 per SMSP x 80 
         issue_dQ(ksb, dsb);
         mma_commit_w(dq_full);
         if (last) mma_commit_w(k_free);  // the item's last reader of K in shared memory
-        if (it == 0 && n > 0) {  // the drain warpgroup has read item n-1's dK out of TMEM
-          const long long t0 = TT_CLK();
-          mbar_wait(dk_free, (n - 1) & 1);
-          w_item += TT_CLK() - t0;
-          w_af += TT_CLK() - t0;
-          tc_fence_after();
-        }
         issue_dK(dsb, qb, it);
         mma_commit_w(&q_empty[s]);
-        if (last) mma_commit_w(dk_done);  // item n's dK final
+        if (last) mma_commit_w(acc_done);  // item n's dK / dV final
         if (last && nxt.x >= 0) {  // item n+1's V -> TMEM (item n's dP^T MMAs, its readers, are complete)
           const long long t0 = TT_CLK();
           mbar_wait(v_full, (n + 1) & 1);
           w_item += TT_CLK() - t0;
-          w_vf += TT_CLK() - t0;
           tc_fence_after();
           copy_in(kColV, sm0 + (n & 1) * kKVTile);
           mma_commit_w(v_free);
@@ -488,9 +470,6 @@ __global__ void __maxnreg__(kNWG == 4 ? 80 : 128)  // 22 warps: 6 per SMSP x 80 
       atomicAdd(&g_bwd_dbg[4], (unsigned long long)G);
       atomicAdd(&g_bwd_dbg[14], (unsigned long long)w_item);
       atomicAdd(&g_bwd_dbg[15], (unsigned long long)n_items);
-      atomicAdd(&g_bwd_dbg[16], (unsigned long long)w_af);
-      atomicAdd(&g_bwd_dbg[17], (unsigned long long)w_kf);
-      atomicAdd(&g_bwd_dbg[18], (unsigned long long)w_vf);
     }
   } else if (warp >= kDrainWarp0) {
     // ===================== dQ drain warpgroup (+ each item's dK / dV epilogue) =====================
@@ -506,38 +485,70 @@ __global__ void __maxnreg__(kNWG == 4 ? 80 : 128)  // 22 warps: 6 per SMSP x 80 
       mbar_arrive(&item_empty[n & 1]);
       if (cur.x < 0) break;
       const int nq = cur.w, n_it = nq * p.g;
-      // Item epilogue, split by tensor: key row r's dV (after the item's last dV MMA, while the drain
-      // would otherwise wait for the last dQ^T) and dK (scaled; after the last dK MMA) -> bf16, with the
-      // a6 fp64 sums of squares of the stored values (fp32 per 8).  dv_free / dk_free are arrived on once
-      // the TMEM reads are done, so item n+1's first dV / dK MMAs wait only for those reads.
+      Walk wk;
+      for (int it = 0; it < n_it; ++it, ++G) {
+        int h, q0;
+        wk.next(p, nq, cur.y, cur.z, h, q0);
+        { long long t0 = TT_CLK(); mbar_wait_role(dq_full, G & 1, dev_dbg(p.wait) & 2); c_wd += TT_CLK() - t0; }
+        long long t_dr = TT_CLK();
+        tc_fence_after();
+        uint32_t v0[32], v1[32];
+        tmem_ld32(tl + kColQ, v0);
+        tmem_ld32(tl + kColQ + 32, v1);
+        tmem_wait_ld();
+        tc_fence_before();
+        mbar_arrive(dq_free);
+        if (dev_dbg(p.dbg) & 1) continue;
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          // stage hh holds query rows [q0 + 32 hh, +32) x 128 dims ([row][dim], scaled fp32); its previous
+          // reduction (one half-tile earlier in issue order) must have finished reading it
+          float* stg = reinterpret_cast<float*>(smem + kOffDQ + hh * kDQStage);
+          if (r == 0) bulk_wait_read<1>();
+          named_bar_sync(1, 128);
+          const uint32_t* vv = hh ? v1 : v0;
+#pragma unroll
+          for (int c = 0; c < 32; ++c) stg[c * kD + r] = __uint_as_float(vv[c]) * p.scale;
+          fence_proxy_async_smem();
+          named_bar_sync(1, 128);
+          if (r == 0) {
+            if (!(dev_dbg(p.dbg) & 32)) tma_reduce_add_3d(&tmdQ, stg, 0, h, q0 + 32 * hh);  // dbg 32: staging only
+            bulk_commit();
+          }
+        }
+        c_dr += TT_CLK() - t_dr;
+      }
+      // ---- item epilogue: key row r's dV and dK (scaled) -> bf16 (a6: fp64 sums of squares of the
+      //      stored values, fp32 per 8).  acc_free is arrived on once every TMEM read is done, before
+      //      the stores drain, so item n+1's first dV / dK MMAs wait only for the reads. ----
+      mbar_wait_role(acc_done, n & 1, dev_dbg(p.wait) & 4);
+      tc_fence_after();
       const int j = cur.y * 128 + r;
       double sq[2] = {0.0, 0.0};
-      auto epilogue = [&](int tsr, uint64_t* done, uint64_t* freed) {
-        mbar_wait_role(done, n & 1, dev_dbg(p.wait) & 4);
-        tc_fence_after();
+#pragma unroll
+      for (int tsr = 0; tsr < 2; ++tsr) {  // 0 = dV (columns 0-127), 1 = dK (128-255)
         const float mul = tsr == 0 ? 1.f : p.scale;
         __nv_bfloat16* dst = (tsr == 0 ? p.dv : p.dk) + ((int64_t)j * p.hkv + cur.z) * kD;
 #pragma unroll 1
-        for (int c2 = 0; c2 < 2; ++c2) {  // two 32-column loads in flight per wait
-          uint32_t ov[64];
-          tmem_ld32(tl + (tsr == 0 ? kColDV : kColDK) + 64 * c2, *reinterpret_cast<uint32_t(*)[32]>(&ov[0]));
-          tmem_ld32(tl + (tsr == 0 ? kColDV : kColDK) + 64 * c2 + 32, *reinterpret_cast<uint32_t(*)[32]>(&ov[32]));
+        for (int cc = 0; cc < 4; ++cc) {
+          uint32_t ov[32];
+          tmem_ld32(tl + kColDV + 128 * tsr + 32 * cc, ov);
           tmem_wait_ld();
-          if (c2 == 1) {
+          if (tsr == 1 && cc == 3) {
             tc_fence_before();
-            mbar_arrive(freed);
+            mbar_arrive(acc_free);
           }
           if (j < Nn) {
-            uint32_t pk[32];
+            uint32_t pk[16];
 #pragma unroll
-            for (int u = 0; u < 32; ++u)
+            for (int u = 0; u < 16; ++u)
               pk[u] = pack_bf16(__uint_as_float(ov[2 * u]) * mul, __uint_as_float(ov[2 * u + 1]) * mul);
-            uint4* d4 = reinterpret_cast<uint4*>(dst + 64 * c2);
+            uint4* d4 = reinterpret_cast<uint4*>(dst + 32 * cc);
 #pragma unroll
-            for (int u = 0; u < 8; ++u) d4[u] = make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+            for (int u = 0; u < 4; ++u) d4[u] = make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
             if (p.part_kv) {
 #pragma unroll
-              for (int u8 = 0; u8 < 8; ++u8) {
+              for (int u8 = 0; u8 < 4; ++u8) {
                 float s8 = 0.f;
 #pragma unroll
                 for (int u = 4 * u8; u < 4 * u8 + 4; ++u) {
@@ -549,43 +560,6 @@ __global__ void __maxnreg__(kNWG == 4 ? 80 : 128)  // 22 warps: 6 per SMSP x 80 
             }
           }
         }
-      };
-      Walk wk;
-      for (int it = 0; it < n_it; ++it, ++G) {
-        int h, q0;
-        wk.next(p, nq, cur.y, cur.z, h, q0);
-        const bool last = it + 1 == n_it;
-        if (last) epilogue(0, dv_done, dv_free);
-        { long long t0 = TT_CLK(); mbar_wait_role(dq_full, G & 1, dev_dbg(p.wait) & 2); c_wd += TT_CLK() - t0; }
-        long long t_dr = TT_CLK();
-        tc_fence_after();
-        uint32_t v0[32], v1[32];
-        tmem_ld32(tl + kColQ, v0);
-        tmem_ld32(tl + kColQ + 32, v1);
-        tmem_wait_ld();
-        tc_fence_before();
-        mbar_arrive(dq_free);
-        if (!(dev_dbg(p.dbg) & 1)) {
-#pragma unroll
-          for (int hh = 0; hh < 2; ++hh) {
-            // stage hh holds query rows [q0 + 32 hh, +32) x 128 dims ([row][dim], scaled fp32); its previous
-            // reduction (one half-tile earlier in issue order) must have finished reading it
-            float* stg = reinterpret_cast<float*>(smem + kOffDQ + hh * kDQStage);
-            if (r == 0) bulk_wait_read<1>();
-            named_bar_sync(1, 128);
-            const uint32_t* vv = hh ? v1 : v0;
-#pragma unroll
-            for (int c = 0; c < 32; ++c) stg[c * kD + r] = __uint_as_float(vv[c]) * p.scale;
-            fence_proxy_async_smem();
-            named_bar_sync(1, 128);
-            if (r == 0) {
-              if (!(dev_dbg(p.dbg) & 32)) tma_reduce_add_3d(&tmdQ, stg, 0, h, q0 + 32 * hh);  // dbg 32: staging only
-              bulk_commit();
-            }
-          }
-        }
-        if (last) epilogue(1, dk_done, dk_free);
-        c_dr += TT_CLK() - t_dr;
       }
       if (p.part_kv) {
         // fixed-order reduction over the item's 128 key rows -> one fp64 partial per (item, tensor)
@@ -814,7 +788,7 @@ __global__ void __launch_bounds__(256) sqnorm_final_kernel(const double* __restr
 extern "C" int tt_debug_bwd_counters(unsigned long long* out, int reset) {
   cudaMemcpyFromSymbol(out, g_bwd_dbg, sizeof(g_bwd_dbg));
   if (reset) {
-    unsigned long long z[20] = {0};
+    unsigned long long z[16] = {0};
     cudaMemcpyToSymbol(g_bwd_dbg, z, sizeof(z));
   }
   return 0;
@@ -829,6 +803,14 @@ size_t sm100_bwd_ws_bytes(int64_t N, int hq, int hkv, int d) {
   return 2 * al256b((size_t)hq * Np * 4) + al256b((size_t)Np * 4) + al256b((size_t)N * hq * d * 4) +
          al256b((size_t)(kDqConvBlocks + 2 * nb * hkv) * sizeof(double));
 }
+
+// the non-persistent kernel for long work items (attn_sm100_bwd_flat.cu)
+constexpr double kFlatMinTilesPerItem = 96.0;
+tt_status launch_bwd_flat(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv, const CUtensorMap& mdo,
+                          const CUtensorMap& mdq, const tt_packed& pk, int hq, int hkv, int restore, bool fold,
+                          float scale, int chunk, const float* L2p, const float* Dp, const float* wf, int64_t Np,
+                          float* dq_acc, void* dk, void* dv, double* part_kv, const void* k, const void* v,
+                          cudaStream_t st);
 
 tt_status sm100_attn_bwd(const tt_packed& pk, const void* q, const void* k, const void* v, const void* o,
                          const float* lse, const void* dout, int restore, int hq, int hkv, int d, float scale,
@@ -887,13 +869,25 @@ tt_status sm100_attn_bwd(const tt_packed& pk, const void* q, const void* k, cons
   prm.dk = static_cast<__nv_bfloat16*>(dk);
   prm.dv = static_cast<__nv_bfloat16*>(dv);
   prm.part_kv = sqnorm ? part_kv : nullptr;
-  auto kern = fold ? tree_attn_bwd_sm100<true> : tree_attn_bwd_sm100<false>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
-  if (e != cudaSuccess) { set_error("sm100_attn_bwd: smem attribute: %s", cudaGetErrorString(e)); return TT_ERR_CUDA; }
-  const unsigned grid = (unsigned)pk.n_blk * hkv;
-  kern<<<grid, kBwdThreads, kSmemBytes, st>>>(mq, mk, mv, mdo, mdq, prm);
-  count_launch();
-  if ((s = check_launch("tree_attn_bwd_sm100"))) return s;
+  // Long work items (mean query tiles per item >= kFlatMinTilesPerItem, from the pack's host schedule
+  // statistics) go to the non-persistent kernel (attn_sm100_bwd_flat.cu): item boundaries are rare there
+  // and it measured 1-2% faster per tile; short items (small trees) take the persistent kernel.
+  const double tiles_per_item = (double)pk.sched_sum_nq * (hq / hkv) / std::max(1, pk.n_blk);
+  bool flat = tiles_per_item >= kFlatMinTilesPerItem;
+  if (const char* f = dev_getenv("TT_BWD_FLAT")) flat = atoi(f) != 0;  // development A/B: force either kernel
+  if (flat) {
+    s = launch_bwd_flat(mq, mk, mv, mdo, mdq, pk, hq, hkv, restore, fold, scale, prm.chunk, L2p, Dp, wf, Np, dq_acc, dk,
+                        dv, prm.part_kv, k, v, st);
+    if (s) return s;
+  } else {
+    auto kern = fold ? tree_attn_bwd_sm100<true> : tree_attn_bwd_sm100<false>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+    if (e != cudaSuccess) { set_error("sm100_attn_bwd: smem attribute: %s", cudaGetErrorString(e)); return TT_ERR_CUDA; }
+    const unsigned grid = (unsigned)pk.n_blk * hkv;
+    kern<<<grid, kBwdThreads, kSmemBytes, st>>>(mq, mk, mv, mdo, mdq, prm);
+    count_launch();
+    if ((s = check_launch("tree_attn_bwd_sm100"))) return s;
+  }
   const int64_t n4 = N * hq * d / 4;
   const int nconv = (int)std::min<int64_t>((n4 + 255) / 256, kDqConvBlocks);
   dq_convert_kernel<<<(unsigned)nconv, 256, 0, st>>>(reinterpret_cast<const float4*>(dq_acc),
@@ -901,7 +895,7 @@ tt_status sm100_attn_bwd(const tt_packed& pk, const void* q, const void* k, cons
   count_launch();
   if ((s = check_launch("dq_convert_kernel"))) return s;
   if (!sqnorm) return TT_OK;
-  sqnorm_final_kernel<<<1, 256, 0, st>>>(part_q, nconv, part_kv, (int)grid, sqnorm);
+  sqnorm_final_kernel<<<1, 256, 0, st>>>(part_q, nconv, part_kv, (int)(pk.n_blk * hkv), sqnorm);
   count_launch();
   return check_launch("sqnorm_final_kernel");
 }

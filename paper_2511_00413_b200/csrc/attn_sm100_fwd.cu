@@ -426,16 +426,29 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           if (cls == kClsPartial && !(dev_dbg(p.dbg) & 64)) {  // dbg 64: development ablation, partial tiles unmasked
             // int32 index math (N < 2^31): key c allowed iff c <= row - j0, c < N - j0, row < E_c
             const int4* Es = reinterpret_cast<const int4*>(smem + kOffE + ((g + t) % kStages) * 512) + 16 * hf;
-            const int cmax = min((int)(row - j0), (int)(p.N - j0) - 1);
             const int irow = (int)row;
+            if (kb != (int)(row >> 7) && !(dev_dbg(p.dbg) & 128)) {  // dbg 128: dev A/B, full test everywhere
+              // below the diagonal (kb < query block) every key precedes every row and no key is past N:
+              // only the subtree-end test (warp-uniform branch)
 #pragma unroll
-            for (int c4 = 0; c4 < 16; ++c4) {
-              const int4 ev = Es[c4];
-              const int ee[4] = {ev.x, ev.y, ev.z, ev.w};
+              for (int c4 = 0; c4 < 16; ++c4) {
+                const int4 ev = Es[c4];
+                const int ee[4] = {ev.x, ev.y, ev.z, ev.w};
 #pragma unroll
-              for (int u = 0; u < 4; ++u) {
-                const int c = 4 * c4 + u;
-                if (!((c <= cmax) && (irow < ee[u]))) s[c] = __float_as_uint(-INFINITY);
+                for (int u = 0; u < 4; ++u)
+                  if (irow >= ee[u]) s[4 * c4 + u] = __float_as_uint(-INFINITY);
+              }
+            } else {
+              const int cmax = min((int)(row - j0), (int)(p.N - j0) - 1);
+#pragma unroll
+              for (int c4 = 0; c4 < 16; ++c4) {
+                const int4 ev = Es[c4];
+                const int ee[4] = {ev.x, ev.y, ev.z, ev.w};
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                  const int c = 4 * c4 + u;
+                  if (!((c <= cmax) && (irow < ee[u]))) s[c] = __float_as_uint(-INFINITY);
+                }
               }
             }
           } else if (ragged) {

@@ -1,0 +1,98 @@
+"""GPU parity of the persistent attention kernels (cluster-launch-control work stealing, DESIGN.md §5.2,
+§5.3) on forests with several work items per CTA: many small trees, so every CTA takes over several
+(query-block pair, head) / (key block, kv head) items, many of them shorter than the kernels' claim /
+prepare look-ahead (items of 1-3 query tiles), GQA and MHA.  Whole-tensor comparison against the fp64
+oracle (Eqs. 1, 14-16, P:119-126 / P:408-436), plus bitwise reproducibility of dK / dV and of the fused
+a6 scalars (an item's result must not depend on which CTA ran it or in which order)."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from workloads import trees, tensors
+from _util import TOL_G_BF16, TOL_O_BF16, max_abs, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def tt():
+    import paper_2511_00413_b200 as P
+    P.lib()
+    return P
+
+
+def _forest(n_trees, seed, max_tokens=160):
+    """n_trees small agentic trees side by side (one root each); lengths drawn so that most trees span
+    one or two 128-token blocks."""
+    rng = np.random.default_rng(seed)
+    parent, length = [], []
+    for i in range(n_trees):
+        n = int(rng.integers(24, max_tokens))
+        t = trees.gen_agentic(n, D=3, root_len=max(1, n // 3), seed=seed * 1000 + i)
+        off = len(parent)
+        parent.extend([-1 if p < 0 else p + off for p in t.parent])
+        length.extend(int(x) for x in t.length)
+    return trees.Tree(np.array(parent, np.int64), np.array(length, np.int64))
+
+
+CASES = [
+    ("gqa_8_2", 300, 8, 2, 11),
+    ("mha_4_4", 260, 4, 4, 12),
+]
+
+
+@pytest.mark.parametrize("name,n_trees,hq,hkv,seed", CASES, ids=[c[0] for c in CASES])
+def test_persistent_forest_matches_oracle(tt, name, n_trees, hq, hkv, seed):
+    import torch
+    t = _forest(n_trees, seed)
+    pk = tt.tt_pack(t.parent, t.length)
+    N, d = pk.n_tokens, 128
+    nb = (N + 127) // 128
+    assert nb * hkv > 2 * 148 and ((nb + 1) // 2) * hq > 2 * 148  # several items per CTA in both kernels
+    q, k, v = tensors.qkv_tensors(N, hq, hkv, d, "bf16", seed=seed)
+    G = tensors.grad_tensor(N, hq, d, "bf16", seed=seed + 100)
+    qd, kd, vd, Gd = (x.cuda() for x in (q, k, v, G))
+    scale = 1.0 / math.sqrt(d)
+    o, lse = tt.tt_attn_fwd(pk, qd, kd, vd, scale)
+    nrm = torch.zeros(3, dtype=torch.float64, device="cuda")
+    dq, dk, dv = tt.tt_attn_bwd(pk, qd, kd, vd, o, lse, Gd, restore=True, softmax_scale=scale, sqnorm=nrm)
+    torch.cuda.synchronize()
+    opk = oracle.pack(t.parent, t.length)
+    oo, olse = oracle.attn_fwd(opk, q, k, v, scale)
+    odq, odk, odv = oracle.attn_bwd(opk, q, k, v, G, scale)
+    assert max_abs(o.cpu(), oo) <= TOL_O_BF16
+    assert max_abs(lse.cpu(), olse) <= TOL_O_BF16
+    for a, b in ((dq, odq), (dk, odk), (dv, odv)):
+        assert rel_l2(a.cpu(), b) <= TOL_G_BF16
+    # per kv head too: a mis-assigned item shows up as one head's block being wrong
+    for hk in range(hkv):
+        assert rel_l2(dk[:, hk].cpu(), odk[:, hk]) <= TOL_G_BF16
+        assert rel_l2(dv[:, hk].cpu(), odv[:, hk]) <= TOL_G_BF16
+    # fused a6 scalars equal the plain sums of squares of the stored gradients
+    for i, x in enumerate((dq, dk, dv)):
+        ref = float((x.double() ** 2).sum())
+        assert abs(float(nrm[i]) - ref) <= 1e-6 * ref
+
+
+def test_persistent_bitwise_reproducible(tt):
+    """Items are taken over dynamically, so which CTA runs an item changes from run to run; dK, dV, O,
+    LSE and the dK / dV norms must not."""
+    import torch
+    t = _forest(300, 21)
+    pk = tt.tt_pack(t.parent, t.length)
+    N, hq, hkv, d = pk.n_tokens, 8, 2, 128
+    q, k, v = (x.cuda() for x in tensors.qkv_tensors(N, hq, hkv, d, "bf16", seed=3))
+    G = tensors.grad_tensor(N, hq, d, "bf16", seed=4).cuda()
+    runs = []
+    for _ in range(3):
+        o, lse = tt.tt_attn_fwd(pk, q, k, v)
+        nrm = torch.zeros(3, dtype=torch.float64, device="cuda")
+        dq, dk, dv = tt.tt_attn_bwd(pk, q, k, v, o, lse, G, restore=True, sqnorm=nrm)
+        torch.cuda.synchronize()
+        runs.append((o.clone(), lse.clone(), dk.clone(), dv.clone(), nrm.clone()))
+    for r in runs[1:]:
+        for a, b in zip(runs[0][:4], r[:4]):
+            assert torch.equal(a, b)
+        assert torch.equal(runs[0][4][1:], r[4][1:])

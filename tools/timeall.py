@@ -12,7 +12,8 @@ def bench(fn, iters=20, warm=3):
         st.record(); fn(); en.record(); torch.cuda.synchronize(); ts.append(st.elapsed_time(en))
     ts.sort(); return ts[len(ts)//2]
 
-cfgs = [("agentic8k", 0), ("deep32k", 1), ("wide", None)] if len(sys.argv) < 2 else [(a, None) for a in sys.argv[1:]]
+cfgs = [("agentic8k", 0), ("deep32k", 1), ("wide", None)] if len(sys.argv) < 2 else \
+    [(a.split(":")[0], int(a.split(":")[1]) if ":" in a else None) for a in sys.argv[1:]]  # config[:seed]
 for cfg, seed in cfgs:
     t = trees.config_tree(cfg, seed); c = trees.CONFIGS[cfg]
     pk = tt.tt_pack(t.parent, t.length); N = pk.n_tokens; hq, hkv, d = c["hq"], c["hkv"], c["d"]
