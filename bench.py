@@ -745,8 +745,12 @@ def main():
                     r["tile_density"] = dens.get(main_kernel)
                 return r
 
-            cand = {"bwd": tensor_roof("bwd", "tt_attn_bwd (bwd_pre + tree_attn_bwd_sm100 + dq_convert)", 10,
-                                       per_op["bwd"], "tree_attn_bwd_sm100"),
+            # which backward kernel tt_attn_bwd dispatched to (persistent for short work items, flat for
+            # long ones: tt_attn_bwd_kernel), per tree of the rank
+            bks = sorted({tt.tt_attn_bwd_kernel(tt.tt_pack(j.tree.parent, j.tree.length), j.hq, j.hkv) for j in jobs})
+            bk = bks[0] if len(bks) == 1 else "tree_attn_bwd_sm100"
+            cand = {"bwd": tensor_roof("bwd", "tt_attn_bwd (bwd_pre + " + " / ".join(bks) + " + dq_convert)", 10,
+                                       per_op["bwd"], bk),
                     "fwd": tensor_roof("fwd", "tt_attn_fwd (tree_attn_fwd_sm100)", 4, per_op["fwd"],
                                        "tree_attn_fwd_sm100")}
             if with_loss:

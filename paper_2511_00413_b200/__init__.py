@@ -7,12 +7,12 @@ loaded, importing the binding raises.
 """
 from .binding import (  # noqa: F401
     TTError, PackedTree, lib, lib_path, tt_pack_plan, tt_pack, tt_pack_weights, tt_attn_fwd, tt_attn_bwd,
-    tt_attn_bwd_workspace, tt_restore_loss, tt_grad_sqnorm, tt_grad_sqnorm3, tt_launch_count, tt_launch_count_reset,
+    tt_attn_bwd_workspace, tt_attn_bwd_kernel, tt_restore_loss, tt_grad_sqnorm, tt_grad_sqnorm3, tt_launch_count, tt_launch_count_reset,
     tt_plan_traversals, tt_traversal_forest, tt_rope, tt_restore_grad, tt_lmhead_loss,
     tt_lmhead_loss_workspace, tt_gemm, TT_BLOCK,
 )
 
 __all__ = ["TTError", "PackedTree", "lib", "lib_path", "tt_pack_plan", "tt_pack", "tt_pack_weights", "tt_attn_fwd",
-           "tt_attn_bwd", "tt_attn_bwd_workspace", "tt_restore_loss", "tt_grad_sqnorm", "tt_grad_sqnorm3",
+           "tt_attn_bwd", "tt_attn_bwd_workspace", "tt_attn_bwd_kernel", "tt_restore_loss", "tt_grad_sqnorm", "tt_grad_sqnorm3",
            "tt_launch_count", "tt_launch_count_reset", "tt_plan_traversals", "tt_traversal_forest", "tt_rope",
            "tt_restore_grad", "tt_lmhead_loss", "tt_lmhead_loss_workspace", "TT_BLOCK"]

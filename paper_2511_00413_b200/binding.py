@@ -82,6 +82,8 @@ def lib():
                                       C.c_float, vp, vp, st]
             L.tt_attn_bwd_workspace.argtypes = [C.POINTER(TTPacked), C.c_int32, C.c_int32, C.c_int32, C.c_int,
                                                 C.POINTER(C.c_size_t)]
+            L.tt_attn_bwd_kernel.argtypes = [C.POINTER(TTPacked), C.c_int32, C.c_int32, C.c_int32, C.c_int,
+                                             C.POINTER(C.c_int32)]
             L.tt_attn_bwd.argtypes = [C.POINTER(TTPacked), vp, vp, vp, vp, vp, vp, C.c_int32, C.c_int, C.c_int32,
                                       C.c_int32, C.c_int32, C.c_float, vp, vp, vp, vp, vp, sz, st]
             L.tt_restore_loss_workspace.restype = C.c_size_t
@@ -108,7 +110,7 @@ def lib():
             L.tt_launch_count.argtypes = []
             L.tt_launch_count_reset.argtypes = []
             L.tt_launch_count_reset.restype = None
-            for fn in ("tt_pack_plan", "tt_pack", "tt_attn_fwd", "tt_attn_bwd_workspace", "tt_attn_bwd",
+            for fn in ("tt_pack_plan", "tt_pack", "tt_attn_fwd", "tt_attn_bwd_workspace", "tt_attn_bwd_kernel", "tt_attn_bwd",
                        "tt_restore_loss", "tt_grad_sqnorm", "tt_grad_sqnorm3", "tt_plan_traversals",
                        "tt_traversal_forest", "tt_rope", "tt_restore_grad", "tt_lmhead_loss_workspace",
                        "tt_lmhead_loss", "tt_gemm"):
@@ -304,6 +306,18 @@ def tt_attn_bwd_workspace(pk: PackedTree, hq, hkv, d, dtype) -> int:
     dt = TT_BF16 if dtype == torch.bfloat16 else TT_FP32
     _check("tt_attn_bwd_workspace", lib().tt_attn_bwd_workspace(C.byref(pk.c), hq, hkv, d, dt, C.byref(n)))
     return int(n.value)
+
+
+BWD_KERNELS = ("tree_attn_bwd_sm100", "tree_attn_bwd_flat_sm100", "attn_bwd_simt")
+
+
+def tt_attn_bwd_kernel(pk: PackedTree, hq, hkv, d=128, dtype=None) -> str:
+    """Name of the backward kernel tt_attn_bwd launches for this forest and head layout (host only)."""
+    import torch
+    dt = TT_FP32 if dtype == torch.float32 else TT_BF16
+    kern = C.c_int32()
+    _check("tt_attn_bwd_kernel", lib().tt_attn_bwd_kernel(C.byref(pk.c), hq, hkv, d, dt, C.byref(kern)))
+    return BWD_KERNELS[kern.value]
 
 
 def tt_attn_bwd(pk: PackedTree, q, k, v, o, lse, dout, restore=True, softmax_scale=None, dq=None, dk=None, dv=None,

@@ -805,7 +805,6 @@ size_t sm100_bwd_ws_bytes(int64_t N, int hq, int hkv, int d) {
 }
 
 // the non-persistent kernel for long work items (attn_sm100_bwd_flat.cu)
-constexpr double kFlatMinTilesPerItem = 96.0;
 tt_status launch_bwd_flat(const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv, const CUtensorMap& mdo,
                           const CUtensorMap& mdq, const tt_packed& pk, int hq, int hkv, int restore, bool fold,
                           float scale, int chunk, const float* L2p, const float* Dp, const float* wf, int64_t Np,
@@ -869,11 +868,10 @@ tt_status sm100_attn_bwd(const tt_packed& pk, const void* q, const void* k, cons
   prm.dk = static_cast<__nv_bfloat16*>(dk);
   prm.dv = static_cast<__nv_bfloat16*>(dv);
   prm.part_kv = sqnorm ? part_kv : nullptr;
-  // Long work items (mean query tiles per item >= kFlatMinTilesPerItem, from the pack's host schedule
+  // Long work items (mean query tiles per item >= kBwdFlatMinTilesPerItem, from the pack's host schedule
   // statistics) go to the non-persistent kernel (attn_sm100_bwd_flat.cu): item boundaries are rare there
   // and it measured 1-2% faster per tile; short items (small trees) take the persistent kernel.
-  const double tiles_per_item = (double)pk.sched_sum_nq * (hq / hkv) / std::max(1, pk.n_blk);
-  bool flat = tiles_per_item >= kFlatMinTilesPerItem;
+  bool flat = bwd_use_flat(pk, hq, hkv);
   if (const char* f = dev_getenv("TT_BWD_FLAT")) flat = atoi(f) != 0;  // development A/B: force either kernel
   if (flat) {
     s = launch_bwd_flat(mq, mk, mv, mdo, mdq, pk, hq, hkv, restore, fold, scale, prm.chunk, L2p, Dp, wf, Np, dq_acc, dk,

@@ -1,7 +1,7 @@
 // attn_sm100_bwd_flat.cu — the non-persistent tree-attention backward (one CTA per (key block, kv head),
 // K / V written into TMEM by the drain warpgroup from global memory): the round-2-start kernel, kept for
 // trees whose work items are long.  sm100_attn_bwd (attn_sm100_bwd.cu) dispatches here when the mean
-// query tiles per item is at least kFlatMinTilesPerItem: on those trees the persistent kernel gains
+// query tiles per item is at least kBwdFlatMinTilesPerItem (tt_internal.cuh): on those trees the persistent kernel gains
 // nothing at its item boundaries and measured 1-2% slower per tile (profiles/r2q_bwd_ab.txt); on small
 // trees (agentic8k) the persistent kernel is 8% faster.  Same workspace, preprocessing, dQ conversion
 // and a6 partials as the persistent kernel (attn_sm100_bwd.cu).

@@ -483,6 +483,15 @@ tt_status tt_attn_bwd_workspace(const tt_packed* pk, int32_t hq, int32_t hkv, in
   return TT_OK;
 }
 
+tt_status tt_attn_bwd_kernel(const tt_packed* pk, int32_t hq, int32_t hkv, int32_t d, tt_dtype dt, int32_t* kernel) {
+  clear_error();
+  tt_status s = check_attn_args("tt_attn_bwd_kernel", pk, dt, hq, hkv, d);
+  if (s) return s;
+  if (!kernel) { set_error("tt_attn_bwd_kernel: kernel is null"); return TT_ERR_INVALID_ARGUMENT; }
+  *kernel = (dt == TT_BF16 && d == 128) ? (bwd_use_flat(*pk, hq, hkv) ? 1 : 0) : 2;
+  return TT_OK;
+}
+
 tt_status tt_attn_bwd(const tt_packed* pk, const void* q, const void* k, const void* v, const void* o,
                       const float* lse, const void* dout, int32_t restore, tt_dtype dt, int32_t hq, int32_t hkv,
                       int32_t d, float softmax_scale, void* dq, void* dk, void* dv, double* sqnorm, void* d_ws,

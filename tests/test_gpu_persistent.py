@@ -51,6 +51,7 @@ def test_persistent_forest_matches_oracle(tt, name, n_trees, hq, hkv, seed):
     N, d = pk.n_tokens, 128
     nb = (N + 127) // 128
     assert nb * hkv > 2 * 148 and ((nb + 1) // 2) * hq > 2 * 148  # several items per CTA in both kernels
+    assert tt.tt_attn_bwd_kernel(pk, hq, hkv) == "tree_attn_bwd_sm100"  # short items: the persistent kernel
     q, k, v = tensors.qkv_tensors(N, hq, hkv, d, "bf16", seed=seed)
     G = tensors.grad_tensor(N, hq, d, "bf16", seed=seed + 100)
     qd, kd, vd, Gd = (x.cuda() for x in (q, k, v, G))
@@ -96,3 +97,25 @@ def test_persistent_bitwise_reproducible(tt):
         for a, b in zip(runs[0][:4], r[:4]):
             assert torch.equal(a, b)
         assert torch.equal(runs[0][4][1:], r[4][1:])
+
+
+def test_bwd_kernel_dispatch(tt):
+    """tt_attn_bwd_kernel reports the dispatch rule of DESIGN §5.3: the persistent kernel when the mean
+    number of 64-row query tiles per (key block, kv head) item is below 96, the flat kernel above, SIMT for
+    fp32 / d != 128; the rule is recomputed here from the tree (queries that see key block kb: [128 kb,
+    maxE_kb))."""
+    import torch
+    for name, hq, hkv in (("agentic8k", 32, 32), ("deep32k", 32, 8), ("wide", 32, 8)):
+        t = trees.config_tree(name)
+        pk = tt.tt_pack(t.parent, t.length)
+        opk = oracle.pack(t.parent, t.length)
+        E, N = np.asarray(opk["E"]), opk["n_tokens"]
+        nb = (N + 127) // 128
+        nq = [(int(E[kb * 128:(kb + 1) * 128].max()) + 63) // 64 - 2 * kb for kb in range(nb)]
+        per_item = sum(nq) * (hq // hkv) / nb
+        want = "tree_attn_bwd_flat_sm100" if per_item >= 96 else "tree_attn_bwd_sm100"
+        assert tt.tt_attn_bwd_kernel(pk, hq, hkv) == want, (name, per_item)
+    t = trees.config_tree("agentic8k")
+    pk = tt.tt_pack(t.parent, t.length)
+    assert tt.tt_attn_bwd_kernel(pk, 32, 32) == "tree_attn_bwd_sm100"
+    assert tt.tt_attn_bwd_kernel(pk, 4, 2, d=64, dtype=torch.float32) == "attn_bwd_simt"
