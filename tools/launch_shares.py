@@ -10,7 +10,7 @@ import sys
 from collections import OrderedDict
 
 OURS = ("pack_fill_kernel", "pack_tiles_kernel", "tree_attn_fwd_sm100", "loss_cluster_kernel", "loss_pipe_kernel", "loss_kernel",
-        "loss_sum_kernel", "bwd_pre_tc_kernel", "tree_attn_bwd_sm100", "dq_convert_kernel",
+        "loss_sum_kernel", "bwd_pre_tc_kernel", "tree_attn_bwd_sm100", "tree_attn_bwd_flat_sm100", "dq_convert_kernel",
         "sqnorm_partial_kernel", "sum_partials_kernel", "sqnorm_final_kernel", "rope_kernel",
         "restore_grad_kernel", "lm_", "simt_")
 
