@@ -119,3 +119,48 @@ def test_bwd_kernel_dispatch(tt):
     pk = tt.tt_pack(t.parent, t.length)
     assert tt.tt_attn_bwd_kernel(pk, 32, 32) == "tree_attn_bwd_sm100"
     assert tt.tt_attn_bwd_kernel(pk, 4, 2, d=64, dtype=torch.float32) == "attn_bwd_simt"
+
+
+def _random_big_forest(seed, n_parts):
+    """n_parts random forests (zero-length nodes, several roots, explicit trajectory counts term[])
+    concatenated: a forest with many short work items for the persistent kernels."""
+    rng = np.random.default_rng(seed)
+    parent, length, term = [], [], []
+    for _ in range(n_parts):
+        t = trees.gen_random_forest(rng, max_nodes=10, max_len=70, with_term=True)
+        off = len(parent)
+        parent.extend([-1 if p < 0 else int(p) + off for p in t.parent])
+        length.extend(int(x) for x in t.length)
+        term.extend(int(x) for x in t.term)
+    return trees.Tree(np.array(parent, np.int64), np.array(length, np.int64), np.array(term, np.int64))
+
+
+@pytest.mark.parametrize("seed,hq,hkv", [(31, 4, 4), (32, 8, 2), (33, 6, 3), (34, 4, 1)])
+def test_persistent_random_forests(tt, seed, hq, hkv):
+    """Random multi-item forests (ragged blocks, zero-length nodes, trajectories ending early or counted
+    twice) through both persistent kernels, whole tensors against the oracle on the tokens some trajectory
+    passes through (R12)."""
+    import torch
+    from _util import to64
+    t = _random_big_forest(seed, 400)
+    pk = tt.tt_pack(t.parent, t.length, t.term)
+    N, d = pk.n_tokens, 128
+    assert ((N + 127) // 128) * hkv > 148 and tt.tt_attn_bwd_kernel(pk, hq, hkv) == "tree_attn_bwd_sm100"
+    q, k, v = tensors.qkv_tensors(N, hq, hkv, d, "bf16", seed=seed)
+    G = tensors.grad_tensor(N, hq, d, "bf16", seed=seed + 100)
+    qd, kd, vd, Gd = (x.cuda() for x in (q, k, v, G))
+    scale = 1.0 / math.sqrt(d)
+    o, lse = tt.tt_attn_fwd(pk, qd, kd, vd, scale)
+    dq, dk, dv = tt.tt_attn_bwd(pk, qd, kd, vd, o, lse, Gd, restore=True, softmax_scale=scale)
+    torch.cuda.synchronize()
+    opk = oracle.pack(t.parent, t.length, t.term)
+    oo, olse = oracle.attn_fwd(opk, q, k, v, scale)
+    odq, odk, odv = oracle.attn_bwd(opk, q, k, v, G, scale)
+    c = np.zeros(opk["n_tokens"], np.int64)
+    for idx in oracle.paths(opk):
+        c[idx] += 1
+    m = c > 0
+    assert max_abs(o.cpu()[m], oo[m]) <= TOL_O_BF16
+    assert max_abs(lse.cpu()[:, m], olse[:, m]) <= TOL_O_BF16
+    for a, b in ((dq, odq), (dk, odk), (dv, odv)):
+        assert rel_l2(to64(a)[m], b[m]) <= TOL_G_BF16
