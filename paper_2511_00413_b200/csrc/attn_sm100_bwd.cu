@@ -512,7 +512,7 @@ __global__ void __maxnreg__(kNWG == 4 ? 80 : 128)  // 22 warps: 6 per SMSP x 80 
           fence_proxy_async_smem();
           named_bar_sync(1, 128);
           if (r == 0) {
-            if (!(dev_dbg(p.dbg) & 32)) tma_reduce_add_3d(&tmdQ, stg, 0, h, q0 + 32 * hh);  // dbg 32: staging only
+            if (!(dev_dbg(p.dbg) & 32)) tma_reduce_add_3d(&tmdQ, stg, 0, TT_DQ_HND ? q0 + 32 * hh : h, TT_DQ_HND ? h : q0 + 32 * hh);  // dbg 32: staging only
             bulk_commit();
           }
         }
@@ -739,10 +739,16 @@ __global__ void __maxnreg__(kNWG == 4 ? 80 : 128)  // 22 warps: 6 per SMSP x 80 
 // dQ fp32 accumulator -> bf16 output; optionally the per-block fp64 sum of squares of the rounded
 // values (fixed grid and grid-stride assignment: bitwise reproducible)
 __global__ void __launch_bounds__(256) dq_convert_kernel(const float4* __restrict__ acc, uint2* __restrict__ out,
-                                                         int64_t n4, double* __restrict__ part_q) {
+                                                         int64_t n4, double* __restrict__ part_q, int64_t N, int hq) {
   double sq = 0.0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
-    const float4 a = acc[i];
+    // output element i = (token, head, 4 dims); TT_DQ_HND reads it from the [hq][N][d] accumulator
+    int64_t ia = i;
+    if (TT_DQ_HND) {
+      const int64_t d4 = i & 31, th = i >> 5, t = th / hq, h = th - t * hq;
+      ia = ((int64_t)h * N + t) * 32 + d4;
+    }
+    const float4 a = acc[ia];
     const uint2 o = make_uint2(pack_bf16(a.x, a.y), pack_bf16(a.z, a.w));
     out[i] = o;
     if (part_q) {
@@ -836,8 +842,14 @@ tt_status sm100_attn_bwd(const tt_packed& pk, const void* q, const void* k, cons
   if ((s = make_tmap_thd(&mdo, dout, N, hq, d, kBQ, BF, 2, SW, 64))) return s;
   if ((s = make_tmap_thd(&mk, k, N, hkv, d, 128, BF, 2, SW, 64))) return s;
   if ((s = make_tmap_thd(&mv, v, N, hkv, d, 128, BF, 2, SW, 64))) return s;
-  if ((s = make_tmap_thd(&mdq, dq_acc, N, hq, d, 32, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, CU_TENSOR_MAP_SWIZZLE_NONE, kD)))
+  if (TT_DQ_HND) {
+    const int64_t dims[3] = {d, N, hq}, strides[2] = {d, N * d};
+    const int box[3] = {kD, 32, 1};
+    if ((s = make_tmap_3d(&mdq, dq_acc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, dims, strides, box))) return s;
+  } else if ((s = make_tmap_thd(&mdq, dq_acc, N, hq, d, 32, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
+                                CU_TENSOR_MAP_SWIZZLE_NONE, kD))) {
     return s;
+  }
   BwdParams prm;
   prm.N = N;
   prm.hq = hq;
@@ -889,7 +901,7 @@ tt_status sm100_attn_bwd(const tt_packed& pk, const void* q, const void* k, cons
   const int64_t n4 = N * hq * d / 4;
   const int nconv = (int)std::min<int64_t>((n4 + 255) / 256, kDqConvBlocks);
   dq_convert_kernel<<<(unsigned)nconv, 256, 0, st>>>(reinterpret_cast<const float4*>(dq_acc),
-                                                     reinterpret_cast<uint2*>(dq), n4, sqnorm ? part_q : nullptr);
+                                                     reinterpret_cast<uint2*>(dq), n4, sqnorm ? part_q : nullptr, N, hq);
   count_launch();
   if ((s = check_launch("dq_convert_kernel"))) return s;
   if (!sqnorm) return TT_OK;

@@ -489,7 +489,7 @@ __global__ void __maxnreg__(kNWG == 4 ? 80 : 128)  // 22 warps: 6 per SMSP x 80 
       tc_fence_before();
       mbar_arrive(&dq_free[0]);
       if (dev_dbg(p.dbg) & 1) continue;
-      if (dev_dbg(p.dbg) & 16) {
+      if ((dev_dbg(p.dbg) & 16) && !TT_DQ_HND) {  // ([N][hq][d] indexing)
         // variant: coalesced fp32 REDs straight from registers (a warp instruction covers 32
         // consecutive head dims of one query row = 128 contiguous bytes); no shared-memory staging
         float* base = p.dq_acc + ((int64_t)q0 * p.hq + h) * kD + r;
@@ -521,9 +521,9 @@ __global__ void __maxnreg__(kNWG == 4 ? 80 : 128)  // 22 warps: 6 per SMSP x 80 
           if (dev_dbg(p.dbg) & 32) {
             // dbg 32: staging only
           } else if (hint & 3) {
-            tma_reduce_add_3d_hint(&tmdQ, stg, 0, h, q0 + 32 * hh, (hint & 1) ? policy_evict_last() : policy_evict_first());
+            tma_reduce_add_3d_hint(&tmdQ, stg, 0, TT_DQ_HND ? q0 + 32 * hh : h, TT_DQ_HND ? h : q0 + 32 * hh, (hint & 1) ? policy_evict_last() : policy_evict_first());
           } else {
-            tma_reduce_add_3d(&tmdQ, stg, 0, h, q0 + 32 * hh);
+            tma_reduce_add_3d(&tmdQ, stg, 0, TT_DQ_HND ? q0 + 32 * hh : h, TT_DQ_HND ? h : q0 + 32 * hh);
           }
           bulk_commit();
         }

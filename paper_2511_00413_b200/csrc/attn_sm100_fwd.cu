@@ -622,6 +622,21 @@ tt_status make_tmap_thd(CUtensorMap* m, const void* ptr, int64_t rows, int heads
   return TT_OK;
 }
 
+// generic 3-D tensor map (dims / strides in elements of elem_bytes, innermost first), no swizzle
+tt_status make_tmap_3d(CUtensorMap* m, const void* ptr, CUtensorMapDataType dt, int elem_bytes, const int64_t dims3[3],
+                       const int64_t strides2[2], const int box3[3]) {
+  auto fn = encode_fn();
+  if (!fn) { set_error("cuTensorMapEncodeTiled unavailable"); return TT_ERR_CUDA; }
+  cuuint64_t dims[3] = {(cuuint64_t)dims3[0], (cuuint64_t)dims3[1], (cuuint64_t)dims3[2]};
+  cuuint64_t strides[2] = {(cuuint64_t)strides2[0] * elem_bytes, (cuuint64_t)strides2[1] * elem_bytes};
+  cuuint32_t box[3] = {(cuuint32_t)box3[0], (cuuint32_t)box3[1], (cuuint32_t)box3[2]};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = fn(m, dt, 3, const_cast<void*>(ptr), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) { set_error("cuTensorMapEncodeTiled failed (%d)", (int)r); return TT_ERR_CUDA; }
+  return TT_OK;
+}
+
 extern "C" int tt_debug_fwd_counters(unsigned long long* out, int reset) {
   cudaMemcpyFromSymbol(out, g_fwd_dbg, sizeof(g_fwd_dbg));
   if (reset) {

@@ -78,6 +78,13 @@ tt_status launch_bwd_pre(const void* o, const void* dout, tt_dtype dt, int64_t N
 bool sm100_available();
 tt_status make_tmap_thd(CUtensorMap* m, const void* ptr, int64_t rows, int heads, int d, int box_rows,
                         CUtensorMapDataType dt, int elem_bytes, CUtensorMapSwizzle sw, int box_inner);
+tt_status make_tmap_3d(CUtensorMap* m, const void* ptr, CUtensorMapDataType dt, int elem_bytes, const int64_t dims3[3],
+                       const int64_t strides2[2], const int box3[3]);
+// fp32 dQ accumulator of the tensor-core backward: [N][hq][d] (0) or [hq][N][d] (TT_DQ_HND=1: every 32-row
+// TMA reduce box one contiguous 16 KB run)
+#ifndef TT_DQ_HND
+#define TT_DQ_HND 0
+#endif
 tt_status sm100_attn_fwd(const tt_packed& pk, const void* q, const void* k, const void* v, int hq, int hkv,
                          int d, float scale, void* o, float* lse, cudaStream_t st);
 // ws: the tensor-core backward workspace (tt_attn_bwd_workspace bytes); see sm100_bwd_ws_bytes
