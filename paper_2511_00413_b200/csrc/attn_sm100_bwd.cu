@@ -92,7 +92,13 @@ constexpr uint32_t kOffBar = kOffStats + kQStages * kStatBytes;
 constexpr uint32_t kNumBars = 2 + 2 * kQStages + 1 + 1 + 2 + 1 + 1 + 1 + 1 + 1 + 2 + 4 + 1;
 // the next item is claimed (CLC) when its producer reaches this many tiles before the current item's
 // end, and published (info + K load) at kPrepareAhead tiles before it
-constexpr int kClaimAhead = 6, kPrepareAhead = 3;
+#ifndef TT_BWD_CLAIM_AHEAD
+#define TT_BWD_CLAIM_AHEAD 6
+#endif
+#ifndef TT_BWD_PREPARE_AHEAD
+#define TT_BWD_PREPARE_AHEAD 3
+#endif
+constexpr int kClaimAhead = TT_BWD_CLAIM_AHEAD, kPrepareAhead = TT_BWD_PREPARE_AHEAD;
 constexpr uint32_t kOffMisc = (kOffBar + kNumBars * 8 + 15) & ~15u;  // [0] TMEM base
 constexpr uint32_t kOffInfo = kOffMisc + 16;                     // item buffers [2]: {item, kb, hk, nq} (item -1: done)
 constexpr uint32_t kOffClc = kOffInfo + 2 * 16;                  // cluster-launch-control response

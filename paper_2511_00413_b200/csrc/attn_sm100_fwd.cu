@@ -59,7 +59,13 @@ constexpr uint32_t kOffTiles = kOffX + (2 * 2 * 2 * 128 + 2 * 2 * 128) * 4;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 // the next item is claimed (CLC) when the producer loads the current item's k-tile T - kClaimAhead and
 // its tile list built from k-tile T - kPrepareAhead on
-constexpr int kClaimAhead = 5, kPrepareAhead = 3;
+#ifndef TT_FWD_CLAIM_AHEAD
+#define TT_FWD_CLAIM_AHEAD 5
+#endif
+#ifndef TT_FWD_PREPARE_AHEAD
+#define TT_FWD_PREPARE_AHEAD 3
+#endif
+constexpr int kClaimAhead = TT_FWD_CLAIM_AHEAD, kPrepareAhead = TT_FWD_PREPARE_AHEAD;
 
 __device__ unsigned long long g_fwd_dbg[16];  // development instrumentation (TT_DEBUG_FWD & 8)
 
