@@ -202,6 +202,8 @@ tt_status tt_pack_weights(const int32_t* parent, const int32_t* len, const int32
  *   LSE_i = ln sum_{j : j <= i < E_j} exp(scale * q_i . k_j)      (natural log, R9)
  * q [N,hq,d], k/v [N,hkv,d] (dtype dt), o [N,hq,d] (dtype dt), lse [hq,N] fp32.
  * Empty tiles are skipped, full tiles run unmasked, partial tiles are masked in registers.
+ * bf16 / d = 128 runs persistent CTAs (cluster launch control takes over not-yet-launched CTAs' work
+ * items); results do not depend on which CTA runs an item (bitwise reproducible).
  * -------------------------------------------------------------------------------------- */
 tt_status tt_attn_fwd(const tt_packed* pk, const void* q, const void* k, const void* v, tt_dtype dt,
                       int32_t hq, int32_t hkv, int32_t d, float softmax_scale, void* o, float* lse,
