@@ -164,3 +164,42 @@ def test_persistent_random_forests(tt, seed, hq, hkv):
     assert max_abs(lse.cpu()[:, m], olse[:, m]) <= TOL_O_BF16
     for a, b in ((dq, odq), (dk, odk), (dv, odv)):
         assert rel_l2(to64(a)[m], b[m]) <= TOL_G_BF16
+
+
+def test_persistent_mixed_item_lengths(tt):
+    """One 4K-token tree (items of up to ~256 query tiles) among 250 small trees: the dispatch
+    still picks the persistent kernel (mean item length below the threshold), so long and short items
+    share the persistent CTAs; whole tensors against the oracle and bitwise repeat."""
+    import torch
+    big = trees.gen_agentic(4096, D=5, p_open=0.3, root_len=1024, seed=77)
+    small = _forest(250, 41)
+    off = len(big.parent)
+    parent = np.concatenate([np.asarray(big.parent, np.int64),
+                             np.array([-1 if p < 0 else p + off for p in small.parent], np.int64)])
+    length = np.concatenate([np.asarray(big.length, np.int64), np.asarray(small.length, np.int64)])
+    t = trees.Tree(parent, length)
+    pk = tt.tt_pack(t.parent, t.length)
+    N, hq, hkv, d = pk.n_tokens, 8, 2, 128
+    assert tt.tt_attn_bwd_kernel(pk, hq, hkv) == "tree_attn_bwd_sm100"
+    assert pk.c.sched_max_nq * (hq // hkv) >= 200  # some items are long
+    q, k, v = tensors.qkv_tensors(N, hq, hkv, d, "bf16", seed=5)
+    G = tensors.grad_tensor(N, hq, d, "bf16", seed=6)
+    qd, kd, vd, Gd = (x.cuda() for x in (q, k, v, G))
+    scale = 1.0 / math.sqrt(d)
+    outs = []
+    for _ in range(2):
+        o, lse = tt.tt_attn_fwd(pk, qd, kd, vd, scale)
+        dq, dk, dv = tt.tt_attn_bwd(pk, qd, kd, vd, o, lse, Gd, restore=True, softmax_scale=scale)
+        torch.cuda.synchronize()
+        outs.append((o.cpu(), lse.cpu(), dq.cpu(), dk.cpu(), dv.cpu()))
+    for a, b in zip(outs[0], outs[1]):
+        if a is not outs[0][2]:  # dQ follows the fp32 reduction order; everything else is bitwise
+            assert torch.equal(a, b)
+    opk = oracle.pack(t.parent, t.length)
+    oo, olse = oracle.attn_fwd(opk, q, k, v, scale)
+    odq, odk, odv = oracle.attn_bwd(opk, q, k, v, G, scale)
+    o, lse, dq, dk, dv = outs[0]
+    assert max_abs(o, oo) <= TOL_O_BF16
+    assert max_abs(lse, olse) <= TOL_O_BF16
+    for a, b in ((dq, odq), (dk, odk), (dv, odv)):
+        assert rel_l2(a, b) <= TOL_G_BF16
