@@ -757,7 +757,11 @@ tt_status launch_bwd_flat(const CUtensorMap& mq, const CUtensorMap& mk, const CU
   prm.nb = pk.n_blk;
   prm.restore = restore ? 1 : 0;
   prm.chunk = chunk;
-  prm.wait = prm.order = prm.l2hint = prm.walk = prm.dbg = 0;
+  prm.wait = prm.order = prm.l2hint = prm.walk = 0;
+  {
+    const char* e = dev_getenv("TT_DEBUG_BWD");  // development ablations (dev build only)
+    prm.dbg = e ? atoi(e) : 0;
+  }
   prm.scale = scale;
   prm.scale_log2 = scale * kLog2e;
   prm.E = pk.E;
