@@ -216,7 +216,7 @@ tt_status tt_attn_bwd_workspace(const tt_packed* pk, int32_t hq, int32_t hkv, in
 /* Which backward kernel tt_attn_bwd launches for this packed forest and head layout (host only, no CUDA
  * call): *kernel = 0 for tree_attn_bwd_sm100, the persistent kernel (cluster-launch-control work stealing
  * over (128-key block, kv head) items; chosen when the mean number of 64-row query tiles per item,
- * sched_sum_nq * (hq / hkv) / n_blk, is below 96: small trees), 1 for tree_attn_bwd_flat_sm100 (one CTA
+ * sched_sum_nq * (hq / hkv) / n_blk, is below 80: small trees), 1 for tree_attn_bwd_flat_sm100 (one CTA
  * per item; long items), 2 for the SIMT kernel (fp32 or d != 128).  Same result either way. */
 tt_status tt_attn_bwd_kernel(const tt_packed* pk, int32_t hq, int32_t hkv, int32_t d, tt_dtype dt,
                              int32_t* kernel);

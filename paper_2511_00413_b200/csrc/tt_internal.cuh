@@ -144,8 +144,8 @@ bool head_major_order(const tt_packed& pk, int hkv);
 inline int fwd_cta_chunk(const tt_packed& pk, int npairs, int hkv) { return head_major_order(pk, hkv) ? npairs : 1; }
 inline int bwd_cta_chunk(const tt_packed& pk, int hkv) { return head_major_order(pk, hkv) ? pk.n_blk : 1; }
 // backward kernel choice (tt_attn_bwd_kernel): the persistent kernel for short work items, the flat one for
-// long items (mean 64-row query tiles per (key block, kv head) item >= 96; profiles/r2q_bwd_ab.txt)
-constexpr double kBwdFlatMinTilesPerItem = 96.0;
+// long items (mean 64-row query tiles per (key block, kv head) item >= 80; profiles/r2q_bwd_ab.txt, r2ad_bwd_threshold.txt)
+constexpr double kBwdFlatMinTilesPerItem = 80.0;
 inline bool bwd_use_flat(const tt_packed& pk, int hq, int hkv) {
   const double tiles_per_item = (double)pk.sched_sum_nq * (hq / hkv) / (pk.n_blk > 0 ? pk.n_blk : 1);
   return tiles_per_item >= kBwdFlatMinTilesPerItem;

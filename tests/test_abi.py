@@ -112,7 +112,7 @@ def test_release_build_has_no_dev_switches(tt):
 def test_bwd_kernel_dispatch_rule_host(tt, name, hq, hkv):
     """tt_attn_bwd_kernel is host logic (no CUDA call): on a tt_packed carrying the pack's schedule
     statistics it picks the persistent backward when the mean number of 64-row query tiles per (key
-    block, kv head) item is below 96.  sched_sum_nq is recomputed here from the oracle's
+    block, kv head) item is below 80.  sched_sum_nq is recomputed here from the oracle's
     subtree ends (queries that see key block kb: [128 kb, max E over the block)); fp32 / d = 64 -> SIMT."""
     from paper_2511_00413_b200.binding import TTPacked, TT_BF16, TT_FP32
     t = trees.config_tree(name)
@@ -125,7 +125,7 @@ def test_bwd_kernel_dispatch_rule_host(tt, name, hq, hkv):
     kern = ctypes.c_int32(-1)
     L = tt.lib()
     assert L.tt_attn_bwd_kernel(ctypes.byref(c), hq, hkv, 128, TT_BF16, ctypes.byref(kern)) == 0
-    assert kern.value == (1 if sum(nq) * (hq // hkv) / nb >= 96 else 0)
+    assert kern.value == (1 if sum(nq) * (hq // hkv) / nb >= 80 else 0)
     assert L.tt_attn_bwd_kernel(ctypes.byref(c), hq, hkv, 64, TT_FP32, ctypes.byref(kern)) == 0
     assert kern.value == 2
     assert L.tt_attn_bwd_kernel(ctypes.byref(c), 32, 5, 128, TT_BF16, ctypes.byref(kern)) != 0  # hq % hkv != 0

@@ -101,7 +101,7 @@ def test_persistent_bitwise_reproducible(tt):
 
 def test_bwd_kernel_dispatch(tt):
     """tt_attn_bwd_kernel reports the dispatch rule of DESIGN §5.3: the persistent kernel when the mean
-    number of 64-row query tiles per (key block, kv head) item is below 96, the flat kernel above, SIMT for
+    number of 64-row query tiles per (key block, kv head) item is below 80, the flat kernel above, SIMT for
     fp32 / d != 128; the rule is recomputed here from the tree (queries that see key block kb: [128 kb,
     maxE_kb))."""
     import torch
@@ -113,7 +113,7 @@ def test_bwd_kernel_dispatch(tt):
         nb = (N + 127) // 128
         nq = [(int(E[kb * 128:(kb + 1) * 128].max()) + 63) // 64 - 2 * kb for kb in range(nb)]
         per_item = sum(nq) * (hq // hkv) / nb
-        want = "tree_attn_bwd_flat_sm100" if per_item >= 96 else "tree_attn_bwd_sm100"
+        want = "tree_attn_bwd_flat_sm100" if per_item >= 80 else "tree_attn_bwd_sm100"
         assert tt.tt_attn_bwd_kernel(pk, hq, hkv) == want, (name, per_item)
     t = trees.config_tree("agentic8k")
     pk = tt.tt_pack(t.parent, t.length)
